@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the rasterizer hot path (contract: see the task's bench.py rules).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+                    [--workload c1|c2|c3|c2-dense] [--mode views|bands]
+
+A *step* is one frame: one pass of preprocess -> emit -> sort -> ranges ->
+blend over one camera view of a synthetic scene that is already resident in
+HBM.  Default workload = BASELINE.json configs[1]: 1M Gaussians (generator
+`mixed`, seed 1, density-scaled per SURVEY.md 8(d)), SH degree 3, one
+1920x1080 view.  Metric = views/sec (whole job, all GPUs); ms/frame is
+`ms_per_step`.  With N > 1 (torchrun, one rank per GPU) every rank holds the
+whole scene and renders its own views -- independent units, no data-path
+collective ("scaling": "weak"); `--mode bands` instead splits ONE frame into
+tile-row bands and gathers them with NCCL.
+
+One JSON line is printed by rank 0.  `value` is device-timed (CUDA events per
+step, L2 flushed between steps); `e2e` is the same metric through the public
+API `Pipeline.render(camera)` with the frame read back to host memory every
+step; `roofline` is the dominant kernel, timed live with CUDA events recorded
+between the kernel launches of the timed steps; `cpu_baseline` is the CPU
+oracle (a C/OpenMP restatement of the reference algorithm, bit-identical to the
+reference on the golden vectors) on the same workload on this box's host cores.
+
+`--impl reference` times that CPU path alone (rank 0 only).
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (gaussians, width, height, density_scale, description)
+    "c1": (10_000, 256, 256, False, "BASELINE configs[0]: 10K Gaussians, SH3, 256x256 single view"),
+    "c2": (1_000_000, 1920, 1080, True,
+           "BASELINE configs[1]: 1M Gaussians (mixed, seed 1, density-scaled), SH3, 1920x1080 single view"),
+    "c2-dense": (1_000_000, 1920, 1080, False,
+                 "1M Gaussians as generated (33.5M pairs, sort-heavy stress), SH3, 1920x1080"),
+    "c3": (3_000_000, 3840, 2160, True,
+           "BASELINE configs[2]: 3M Gaussians (density-scaled), SH3, 3840x2160 single view"),
+    "c4": (10_000_000, 7680, 4320, True,
+           "BASELINE configs[3]: 10M Gaussians (density-scaled), SH3, 7680x4320"),
+    "c4-4k": (10_000_000, 3840, 2160, True,
+              "north_star target: 10M Gaussians (density-scaled), SH3, 3840x2160"),
+}
+METRIC, UNIT = "views_per_sec", "views/s"
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)", float(d.get("sm_max_mhz", 1965.0))
+    return 6650.0, "fallback (B200_PROFILING.md)", 1965.0
+
+
+class ClockSampler:
+    """Samples SM clock / throttle reasons through NVML while the timed region runs."""
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thr = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = int(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {"hw_slowdown": 0x8, "sw_power_cap": 0x4, "hw_thermal_slowdown": 0x40,
+                 "sw_thermal_slowdown": 0x20, "hw_power_brake": 0x80, "sync_boost": 0x10,
+                 "applications_clocks": 0x2}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(int(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = int(nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h))
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def start(self):
+        if self.nv is not None:
+            self._thr = threading.Thread(target=self._run, daemon=True)
+            self._thr.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._thr is not None:
+            self._thr.join()
+        med = int(np.median(self.samples)) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def make_scene(fgs, name):
+    n, w, h, dens, desc = WORKLOADS[name]
+    act = fgs.activate(fgs.gen_synthetic("mixed", n, 1, density_scale=dens))
+    return act, w, h, desc
+
+
+def cpu_arm(act, cam, steps, warmup, budget_s=30.0):
+    """The CPU path (oracle port of the reference) on this box's host cores."""
+    from oracle import oracle as orc
+    cores = orc.max_threads()
+    for _ in range(max(1, min(warmup, 2))):
+        orc.render(act, cam)
+    times, stages = [], []
+    t_begin = time.perf_counter()
+    for _ in range(max(1, steps)):
+        _, st = orc.render(act, cam)
+        times.append(st["total_ns"] / 1e9)
+        stages.append((st["preprocess_bin_ns"], st["sort_ns"], st["render_ns"]))
+        if time.perf_counter() - t_begin > budget_s:
+            break
+    t = float(np.mean(times))
+    sm = np.mean(np.asarray(stages, dtype=np.float64), axis=0) / 1e6
+    return {"value": 1.0 / t, "unit": UNIT, "cores": cores, "kind": "port",
+            "ms_per_frame": t * 1e3, "frames_timed": len(times),
+            "stage_ms": {"preprocess_bin": sm[0], "sort": sm[1], "render": sm[2]},
+            "sample": f"{len(times)} whole frame(s) of the same workload, OpenMP on {cores} threads "
+                      "(oracle/fgs_oracle.c: C restatement of the reference, bit-identical to it on "
+                      "tests/golden)"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    import paper_2408_07967_b200.scene as scene_mod
+    act, w, h, desc = make_scene(scene_mod, args.workload)
+    cam = scene_mod.orbit_cameras(1, 24.0, w, h)[0]
+    cb = cpu_arm(act, cam, args.steps, args.warmup, budget_s=150.0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+        "n_gpus": args.gpus, "steps": cb["frames_timed"], "warmup": args.warmup,
+        "ms_per_step": cb["ms_per_frame"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "strategy": "precise", "tau": 1.0 / 255.0, "sh_degree": 3},
+        "cpu_baseline": cb,
+        "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--mode", default="views", choices=["views", "bands"])
+    ap.add_argument("--exact", action="store_true", help="bit-exact blend mode")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2408_07967_b200 as fgs
+    from paper_2408_07967_b200 import _capi
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device (the product has no CPU fallback)")
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    act, W, H, desc = make_scene(fgs, args.workload)
+    P = act.count
+    ncam = max(world, 1)
+    cams = fgs.orbit_cameras(ncam, 24.0, W, H)
+    cam = cams[0] if args.mode == "bands" else cams[rank % ncam]
+    gh = -(-H // 16)
+    band = None
+    if args.mode == "bands" and world > 1:
+        per, extra = divmod(gh, world)
+        b0 = rank * per + min(rank, extra)
+        band = (b0, b0 + per + (1 if rank < extra else 0) - 1)
+
+    pipe = fgs.Pipeline(act)
+    L = _capi.lib()
+    hbm_peak, peak_src, sm_max = peaks()
+
+    # ---- warm-up through the public API (also sizes the workspace) -------------
+    for _ in range(args.warmup):
+        fb, st = pipe.render(cam, exact=args.exact, band=band)
+    M = st.pairs_emitted
+    stream = torch.cuda.current_stream(dev)
+    ws = pipe._take_ws(torch, W, H, pipe._default_capacity())
+    lay = ws.lay
+    npass = int(lay.sort_passes)
+    n_marks = 6 + npass                     # K1 K2 K3 hist pass*npass K5 K6
+    camc = _capi.camera_struct(cam)
+    kcut = pipe._cutoffs(torch, 1.0 / 255.0)
+    bg = (C.c_float * 3)(0.0, 0.0, 0.0)
+    flags = (_capi.BLEND_EXACT if args.exact else 0) | _capi.BLEND_CONTRIB
+    b0, b1 = band if band is not None else (0, gh - 1)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
+
+    def frame():
+        _capi.check(L.fgs_render(pipe.packed.data_ptr(), kcut.data_ptr(), P, C.byref(camc),
+                                 1.0 / 255.0, 3, 0, bg, flags, b0, b1, ws.next_epoch(),
+                                 ws.rgb.data_ptr(), None, None, C.c_void_p(ws.base),
+                                 C.byref(ws.lay), C.c_void_p(stream.cuda_stream)))
+
+    for _ in range(args.warmup):
+        frame()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-timed steps ------------------------------------------------------
+    K = args.steps
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(n_marks)] for _ in range(K)]
+    for e in ev0:
+        e.record(stream)               # materialise the handles
+    for row in marks:
+        for e in row:
+            e.record(stream)
+    handles = [(C.c_void_p * n_marks)(*[e.cuda_event for e in row]) for row in marks]
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.perf_counter()
+    for i in range(K):
+        flush.fill_(i & 0xff)          # evict L2 between steps (not timed)
+        ev0[i].record(stream)
+        L.fgs_profile_begin(handles[i], n_marks)
+        frame()
+        got = L.fgs_profile_end()
+        assert got == n_marks, (got, n_marks)
+    torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    step_ms = np.array([ev0[i].elapsed_time(marks[i][-1]) for i in range(K)])
+    kern = np.zeros((K, n_marks))
+    for i in range(K):
+        prev = ev0[i]
+        for j in range(n_marks):
+            kern[i, j] = prev.elapsed_time(marks[i][j])
+            prev = marks[i][j]
+    total_ms = float(step_ms.sum())
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    views_per_step = 1 if (args.mode == "bands") else world
+    value = views_per_step * K / (total_ms / 1e3)
+
+    # ---- end to end through the public API (host frame out every step) -----------
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(K):
+        fb, st_e = pipe.render(cam, exact=args.exact, band=band, timing=False)
+        assert fb.image.shape == (H, W, 3)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = views_per_step * K / e2e_s
+
+    # bands: gather the bands on rank 0 with NCCL (reporting the gather time)
+    gather_ms = None
+    if args.mode == "bands" and world > 1:
+        rows = [0] * world
+        per, extra = divmod(gh, world)
+        full = torch.empty((H, W, 3), dtype=torch.float32, device=dev) if rank == 0 else None
+        y0, y1 = b0 * 16, min((b1 + 1) * 16, H)
+        mine = ws.rgb[y0:y1].contiguous()
+        torch.cuda.synchronize(dev)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        if rank == 0:
+            full[y0:y1] = mine
+            ops = []
+            for r in range(1, world):
+                rb0 = r * per + min(r, extra)
+                rb1 = rb0 + per + (1 if r < extra else 0) - 1
+                ops.append(dist.P2POp(dist.irecv, full[rb0 * 16:min((rb1 + 1) * 16, H)], r))
+            for w_ in dist.batch_isend_irecv(ops):
+                w_.wait()
+        else:
+            for w_ in dist.batch_isend_irecv([dist.P2POp(dist.isend, mine, 0)]):
+                w_.wait()
+        g1.record()
+        torch.cuda.synchronize(dev)
+        gather_ms = g0.elapsed_time(g1)
+
+    if rank == 0:
+        names = ["preprocess", "scan", "emit", "sort_hist"] + [f"sort_pass{p}" for p in range(npass)] \
+            + ["ranges", "blend"]
+        kmean = kern.mean(axis=0)
+        R = int(st.gaussians_retained)
+        T_tiles = int(lay.tiles)
+        # algorithmic bytes per launch (packed scene reads 240+4 B/Gaussian)
+        alg = {
+            "preprocess": 236.0 * P + 52.0 * R,
+            "emit": 12.0 * M + 4.0 * P,
+            "sort_hist": 8.0 * M,
+            "ranges": 8.0 * M + 4.0 * (T_tiles + 1),
+            "blend": 52.0 * M + 12.0 * W * H,
+        }
+        for p_ in range(npass):
+            alg[f"sort_pass{p_}"] = 24.0 * M
+        kernels = []
+        for nme, ms in zip(names, kmean):
+            ent = {"name": nme, "ms": float(ms), "share": float(ms / kmean.sum())}
+            if nme in alg and ms > 0:
+                ent["alg_bytes"] = alg[nme]
+                ent["gbs"] = alg[nme] / (ms * 1e-3) / 1e9
+                ent["frac_hbm"] = ent["gbs"] / hbm_peak
+            kernels.append(ent)
+        # dominant kernel: sort passes are launches of ONE kernel -> judged together
+        sort_ms = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass")))
+        cand = {"blend": kmean[-1], "sort_pass": sort_ms, "preprocess": kmean[0], "emit": kmean[2]}
+        dom = max(cand, key=cand.get)
+        if dom == "sort_pass":
+            per_launch_ms = sort_ms / npass
+            ach = 24.0 * M / (per_launch_ms * 1e-3) / 1e9
+            roof = {"kernel": "k_sort_pass", "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                    "launches_per_step": npass, "ms_per_launch": per_launch_ms,
+                    "alg_bytes_per_launch": 24.0 * M}
+        elif dom == "blend":
+            # FP32-pipe bound (no dense contraction -> no tensor cores): also report the
+            # HBM view so the schema's fields are filled; `fp32` carries the pipe estimate.
+            ms = float(kmean[-1])
+            ach = alg["blend"] / (ms * 1e-3) / 1e9
+            roof = {"kernel": "k_blend", "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                    "launches_per_step": 1, "ms_per_launch": ms,
+                    "alg_bytes_per_launch": alg["blend"],
+                    "note": "blend is FP32-issue bound, not HBM bound: see profiles/ for "
+                            "sm__inst_executed_pipe_fma / issue-slot utilisation from ncu"}
+        else:
+            idx = 0 if dom == "preprocess" else 2
+            ms = float(kmean[idx])
+            ach = alg[dom] / (ms * 1e-3) / 1e9
+            roof = {"kernel": "k_" + dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                    "launches_per_step": 1, "ms_per_launch": ms, "alg_bytes_per_launch": alg[dom]}
+        roof["peak_source"] = peak_src
+
+        cpu = None
+        if not args.no_cpu and world == 1:
+            cpu = cpu_arm(act, cam, 3, 1, budget_s=25.0)
+
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak" if args.mode == "views" else "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": desc, "mode": args.mode, "strategy": "precise",
+                       "tau": 1.0 / 255.0, "sh_degree": 3, "gaussians": P, "width": W, "height": H,
+                       "pairs": M, "retained": R, "tiles": T_tiles, "sort_passes": npass,
+                       "blend": "exact" if args.exact else "ex2.approx+guard",
+                       "l2": "256 MiB buffer written between timed steps (flush, untimed); "
+                             "scene (240 B/Gaussian) is re-read from HBM every step",
+                       "timing": "CUDA events per step on the launch stream, max over ranks"},
+            "clocks": clocks,
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / K * 1e3,
+                    "h2d_bytes_per_step": C.sizeof(_capi.FgsCamera) + 12,
+                    "d2h_bytes_per_step": W * H * 12 + 64,
+                    "api": "Pipeline.render(camera) -> host numpy frame (pinned D2H) + FrameStats"},
+            "gpu_launches": int((n_marks) * K),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "kernels": kernels,
+            "stage_ms": {"preprocess_bin": float(kmean[0:3].sum()),
+                         "sort": float(kmean[3:4 + npass + 1].sum()), "render": float(kmean[-1])},
+            "wall_s_timed_region": t_wall,
+        }
+        if gather_ms is not None:
+            line["band_gather_ms"] = gather_ms
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,237 @@
+/*
+ * flashgs_b200.h -- C ABI of the B200-native FlashGS forward rasterizer.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `tilesplat` (a CPU NumPy/numba rasterizer; it has no FFI of its own, its
+ * boundary is the Python call surface of pipeline.py).  Each entry point
+ * below names the reference function it replaces (file:line under
+ * /root/reference/pkg/src/tilesplat).  INTEGRATION.md shows the ctypes stub a
+ * maintainer of the reference would add to route those functions here.
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer unless the name ends in `_host`;
+ *   - `stream` is a cudaStream_t passed as void* (0 = legacy default stream);
+ *   - every call is asynchronous on `stream`, never allocates, never
+ *     synchronises, never throws; it returns FGS_OK or a negative FGS_E_*;
+ *   - data-dependent conditions (pair-buffer overflow, unsorted keys, tile
+ *     index outside the grid, non-positive depth) are reported through the
+ *     device-side `fgs_stats` block, which the caller copies back after the
+ *     frame (the caller owns all memory; kernels only borrow it);
+ *   - float32 geometry follows the reference's NumPy operation order with no
+ *     FMA contraction, so the emitted (key, value) pair list and its sorted
+ *     order are bit-identical to the reference's.
+ */
+#ifndef FLASHGS_B200_H
+#define FLASHGS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FGS_ABI_VERSION 1
+#define FGS_TILE 16              /* constants.py:4  TILE_SIZE */
+
+enum {
+    FGS_OK = 0,
+    FGS_E_ARG = -1,              /* null pointer / negative size / bad enum  */
+    FGS_E_SH_DEGREE = -2,        /* render.py:58-59   ValueError             */
+    FGS_E_STRATEGY = -3,         /* binning.py:201-202 ValueError            */
+    FGS_E_CUDA = -4,             /* a launch failed; see fgs_last_cuda_error */
+    FGS_E_SIZE = -5,             /* size exceeds 32-bit pair / tile indexing */
+    FGS_E_WORKSPACE = -6         /* workspace too small for this call        */
+};
+
+/* binning.py:38  STRATEGIES */
+enum { FGS_PRECISE = 0, FGS_TIGHT_AABB = 1, FGS_BASELINE_CIRCLE_AABB = 2 };
+
+/* fgs_blend flags */
+enum {
+    FGS_BLEND_EXACT   = 1,  /* glibc-equivalent expf in FP64, no FMA: frame is
+                               bit-identical to the reference's; default is the
+                               ex2.approx path with an exact re-check at the
+                               alpha<tau threshold (max-abs error ~1e-6)      */
+    FGS_BLEND_CONTRIB = 2   /* fill the per-pair "touched a pixel" flags and
+                               stats.pairs_contributing (render.py:200-231)  */
+};
+
+/* model_io.py:226-254 Camera, flattened.  Doubles are the Python floats the
+ * reference keeps; they are rounded to float32 where the reference rounds
+ * them (projection.py:100-103). */
+typedef struct fgs_camera {
+    int32_t width, height;
+    float   view[16];            /* world_to_camera, row-major            */
+    float   proj[16];            /* full_projection, row-major            */
+    float   position[3];
+    float   reserved0;
+    double  tan_fovx, tan_fovy, focal_x, focal_y;
+} fgs_camera;
+
+/* Device-side counters of one frame (pipeline.py:28-48 FrameStats fields that
+ * are data, not time).  64 bytes; lives at fgs_layout.off_stats. */
+typedef struct fgs_stats {
+    uint32_t pairs_emitted;        /* M, exact even when it overflowed      */
+    uint32_t pairs_in_buffer;      /* M, or 0 when M > capacity             */
+    uint32_t gaussians_retained;
+    uint32_t gaussians_degenerate;
+    uint32_t tiles_nonempty;
+    uint32_t pairs_contributing;   /* only with FGS_BLEND_CONTRIB           */
+    uint32_t overflow;             /* M > capacity: grow and re-run
+                                      (binning.py:134-143 "never truncate") */
+    uint32_t bad_depth;            /* binning.py:50-51                      */
+    uint32_t unsorted;             /* sorting.py:146-147                    */
+    uint32_t tile_out_of_grid;     /* sorting.py:150-151                    */
+    uint32_t candidate_tiles_lo;   /* sum of nx*ny over retained, low/high  */
+    uint32_t candidate_tiles_hi;
+    uint32_t reserved[4];
+} fgs_stats;
+
+/* Byte offsets of every per-frame buffer inside the caller's workspace.
+ * A pure function of (P, width, height, capacity). */
+typedef struct fgs_layout {
+    uint64_t total_bytes;
+    uint64_t off_splat;        /* float  [P][12]  render.py:34-40 row layout  */
+    uint64_t off_depth;        /* float  [P]      camera-space z              */
+    uint64_t off_rects;        /* uint16 [P][4]   inclusive tx0,ty0,tx1,ty1   */
+    uint64_t off_flags;        /* uint8  [P]      bit0 retained, bit1 degen.  */
+    uint64_t off_counts;       /* uint32 [P]      emitted pairs per Gaussian  */
+    uint64_t off_blocksums;    /* uint32 [2][nblocks]  sums, exclusive bases  */
+    uint64_t off_keys[2];      /* uint64 [capacity]   ping / pong             */
+    uint64_t off_vals[2];      /* uint32 [capacity]                           */
+    uint64_t off_sortstate;    /* uint64 [sort tiles][256] look-back table    */
+    uint64_t off_hist;         /* uint32 [16][256] + tickets                  */
+    uint64_t off_starts;       /* int32  [tiles + 1]  sorting.py:139-152      */
+    uint64_t off_contrib;      /* uint8  [capacity]                           */
+    uint64_t off_stats;        /* fgs_stats                                   */
+    int64_t  gaussians, capacity;
+    int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
+    int32_t  preprocess_blocks, sort_passes, sorted_in;  /* sorted_in: 0/1 = which
+                                  keys/vals buffer holds the sorted pairs     */
+    int32_t  reserved;
+} fgs_layout;
+
+int         fgs_abi_version(void);
+const char *fgs_error_string(int code);
+const char *fgs_last_cuda_error(void);
+
+/* Profiling aid (pipeline.py:84-102 stage timers, at kernel granularity): after
+ * fgs_profile_begin, every kernel launched by the calling thread through this
+ * library is followed by a cudaEventRecord of the next event in `events`
+ * (cudaEvent_t handles, caller-owned) on the launch stream.  fgs_profile_end
+ * disarms and returns how many were recorded.  Frame order: preprocess, scan,
+ * emit, sort histogram, one per sort pass, ranges, blend. */
+void    fgs_profile_begin(void **events, int32_t n_events);
+int32_t fgs_profile_end(void);
+
+/* ---- per-scene (model_io.py:78-118 ActivatedScene; untimed in the reference,
+ *      pipeline.py:1-5) ------------------------------------------------------ */
+
+/* Bytes of the packed device scene for P Gaussians. */
+size_t fgs_scene_bytes(int64_t gaussians);
+
+/* Re-lay the reference's arrays (means (P,3), opacities (P,), scales (P,3),
+ * rotations (P,4) wxyz unit, sh (P,16,3)) into float4 planes so that the
+ * preprocess kernel's loads are coalesced: 240 B per Gaussian. */
+int fgs_scene_pack(const float *means, const float *opacities, const float *scales,
+                   const float *rotations, const float *sh, int64_t gaussians,
+                   void *packed_scene, void *stream);
+
+/* extent.py:19-30 power_cutoffs: k = min(9, 2 ln(alpha0 / tau)) with the log in
+ * float64, rounded once to float32.  One float per Gaussian; depends on the
+ * scene and tau only, so callers cache it per tau. */
+int fgs_power_cutoffs(const void *packed_scene, int64_t gaussians, double tau,
+                      float *k_out, void *stream);
+
+/* ---- per-frame ---------------------------------------------------------- */
+
+int fgs_workspace_layout(int64_t gaussians, int32_t width, int32_t height,
+                         int64_t capacity, fgs_layout *out_host);
+
+/* Must be called once after the workspace is allocated (zeroes the sort
+ * look-back table, whose entries are epoch-tagged afterwards). */
+int fgs_workspace_init(void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* binning.py:197-257 preprocess_and_bin, phase A + the count half of phase B:
+ * cull, project, conic, cutoff, extent rectangle, SH colour, and the number of
+ * candidate tiles that pass the strategy's test (intersect.py:63-94 for
+ * `precise`).  Writes splat rows, depth, rects, flags, counts, block sums.
+ * Tile rows outside [band_ty0, band_ty1] are not counted (row-band mode;
+ * pass 0 and grid_h-1 for a whole frame). */
+int fgs_preprocess(const void *packed_scene, const float *k_cut, int64_t gaussians,
+                   const fgs_camera *camera_host, double tau, int32_t sh_degree,
+                   int32_t strategy, int32_t band_ty0, int32_t band_ty1,
+                   void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* binning.py:292 (np.cumsum) / 129-147 (shared cursor): exclusive scan of the
+ * per-block pair counts; fixes M, the overflow flag, and resets sort counters. */
+int fgs_scan(void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* binning.py:264-354 phase B emit: key = tile << 32 | depth bits
+ * (binning.py:47-54), value = Gaussian index, written at the scanned offsets,
+ * i.e. in ascending Gaussian order (deterministic, unlike an atomic cursor). */
+int fgs_emit(const fgs_camera *camera_host, int32_t strategy, int32_t band_ty0,
+             int32_t band_ty1, void *workspace, const fgs_layout *layout_host,
+             void *stream);
+
+/* sorting.py:101-136 sort_pairs for the frame's pair buffer: stable LSD radix
+ * sort, 8-bit digits, over key bits [0,31) and [32, 32+tile_bits); emission
+ * order makes ties come out in ascending value, so the value passes of the
+ * reference are not needed.  `epoch` must increase by at least 16 per call on
+ * the same workspace. */
+int fgs_sort(void *workspace, const fgs_layout *layout_host, uint32_t epoch, void *stream);
+
+/* sorting.py:139-152 tile_range_table on the sorted buffer. */
+int fgs_ranges(void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* render.py:273-310 render_frame (+ 135-252 the pipelined compositor).
+ * out_rgb (H,W,3) float32 is required; out_alpha (H,W) = 1 - T_final and
+ * out_depth (H,W) = sum of blend weight * camera z are optional extras. */
+int fgs_blend(const float background[3], double tau, int32_t flags,
+              int32_t band_ty0, int32_t band_ty1,
+              float *out_rgb, float *out_alpha, float *out_depth,
+              void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* pipeline.py:77-111 Pipeline.render: the six calls above, back to back on
+ * `stream`, no host synchronisation in between. */
+int fgs_render(const void *packed_scene, const float *k_cut, int64_t gaussians,
+               const fgs_camera *camera_host, double tau, int32_t sh_degree,
+               int32_t strategy, const float background[3], int32_t blend_flags,
+               int32_t band_ty0, int32_t band_ty1, uint32_t epoch,
+               float *out_rgb, float *out_alpha, float *out_depth,
+               void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* ---- stand-alone stages on caller-supplied arrays (the reference exposes the
+ *      same stages so intermediates can be diffed) ---------- */
+
+/* Scratch bytes fgs_sort_pairs needs for n pairs. */
+size_t fgs_sort_pairs_scratch_bytes(int64_t n);
+
+/* sorting.py:101-136 on arbitrary input order: value bytes first
+ * (ceil(value_bits/8) passes), then key bits [0, 32+tile_bits).  keys_out /
+ * vals_out receive the result; inputs are not modified.  `scratch` must be
+ * zero-initialised once and may then be reused with increasing epochs. */
+int fgs_sort_pairs(const uint64_t *keys_in, const uint32_t *vals_in, int64_t n,
+                   int32_t tile_bits, int32_t value_bits,
+                   uint64_t *keys_out, uint32_t *vals_out,
+                   void *scratch, size_t scratch_bytes, uint32_t epoch, void *stream);
+
+/* sorting.py:139-152: starts[tiles+1] (int32) from sorted keys; sets
+ * stats->unsorted / stats->tile_out_of_grid instead of raising. */
+int fgs_tile_ranges(const uint64_t *sorted_keys, int64_t n, int32_t tiles,
+                    int32_t *starts, fgs_stats *stats, void *stream);
+
+/* render.py:273-310 on a caller-supplied splat table (P,12), sorted values
+ * and range table. */
+int fgs_blend_tiles(const float *splat, const float *gaussian_depth,
+                    const uint32_t *sorted_values, const int32_t *starts,
+                    int32_t width, int32_t height, const float background[3],
+                    double tau, int32_t flags, int32_t band_ty0, int32_t band_ty1,
+                    float *out_rgb, float *out_alpha, float *out_depth,
+                    uint8_t *contrib, fgs_stats *stats, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLASHGS_B200_H */

@@ -1,0 +1,25 @@
+"""B200-native FlashGS forward rasterizer behind the reference's call surface.
+
+``Pipeline.render`` (reference ``tilesplat/pipeline.py:77-111``) and its four
+stages run as hand-written sm_100a CUDA kernels reached through the C ABI in
+``include/flashgs_b200.h``.  Importing this package never touches the GPU;
+the first call that needs it loads ``_lib/libflashgs_b200.so`` and raises if
+it is absent -- there is no CPU fallback.
+"""
+
+from .pipeline import (BinOutput, Framebuffer, FrameStats, Pipeline, STRATEGIES,
+                       TAU_DEFAULT, TILE_SIZE, UnsortedPairsError, max_abs_diff,
+                       power_cutoffs, preprocess_and_bin, psnr, render_frame,
+                       run_frame, sort_pairs, tile_range_table)
+from .scene import (ActivatedScene, Camera, CameraValidationError, Scene, activate,
+                    gen_synthetic, look_at_camera, make_camera, orbit_cameras)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "ActivatedScene", "BinOutput", "Camera", "CameraValidationError", "Framebuffer",
+    "FrameStats", "Pipeline", "STRATEGIES", "Scene", "TAU_DEFAULT", "TILE_SIZE",
+    "UnsortedPairsError", "activate", "gen_synthetic", "look_at_camera", "make_camera",
+    "max_abs_diff", "orbit_cameras", "power_cutoffs", "preprocess_and_bin", "psnr",
+    "render_frame", "run_frame", "sort_pairs", "tile_range_table",
+]

@@ -1,0 +1,256 @@
+// K6 per-tile alpha blending.
+//
+// Replaces render.py:135-252 (_composite_pipelined), 273-310 (render_frame).
+//
+// One CTA per 16x16 tile, one thread per pixel.  The tile's sorted pair slice
+// is consumed in batches of 256 through a two-step prefetch pipeline (the
+// FlashGS scheme, at batch granularity): while batch i is
+// blended out of shared memory, the 48-byte splat rows of batch i+1 are in
+// flight as cp.async gathers (global -> shared, no register staging) and the
+// pair indices of batch i+2 are in flight as plain loads.
+//
+// Numerics.  The three skips of the reference (extent rectangle, power
+// cutoff, alpha < tau) are hard thresholds, so `s` is evaluated in the
+// reference's exact float32 operation order with individually rounded
+// operations (no FMA).  exp(-s):
+//   EXACT  : double-precision port of the published expf algorithm glibc uses
+//            (32-entry 2^(i/32) table + cubic), accumulations unfused: the
+//            frame is bit-identical to the reference's.
+//   default: ex2.approx.ftz.f32; when alpha lands within 1e-5 (relative) of
+//            tau the exact path decides, so the alpha<tau skip never flips.
+// Whole-tile early exit when every pixel's transmittance is below 1e-4
+// (render.py:154,178,228-229) via __syncthreads_and; a warp whose 32 pixels
+// are all finished skips the rest of a batch.
+
+#include "fgs_common.cuh"
+
+namespace {
+
+__device__ __constant__ unsigned long long c_exp2_tab[32] = {
+    0x3ff0000000000000ull, 0x3fefd9b0d3158574ull, 0x3fefb5586cf9890full, 0x3fef9301d0125b51ull,
+    0x3fef72b83c7d517bull, 0x3fef54873168b9aaull, 0x3fef387a6e756238ull, 0x3fef1e9df51fdee1ull,
+    0x3fef06fe0a31b715ull, 0x3feef1a7373aa9cbull, 0x3feedea64c123422ull, 0x3feece086061892dull,
+    0x3feebfdad5362a27ull, 0x3feeb42b569d4f82ull, 0x3feeab07dd485429ull, 0x3feea47eb03a5585ull,
+    0x3feea09e667f3bcdull, 0x3fee9f75e8ec5f74ull, 0x3feea11473eb0187ull, 0x3feea589994cce13ull,
+    0x3feeace5422aa0dbull, 0x3feeb737b0cdc5e5ull, 0x3feec49182a3f090ull, 0x3feed503b23e255dull,
+    0x3feee89f995ad3adull, 0x3feeff76f2fb5e47ull, 0x3fef199bdd85529cull, 0x3fef3720dcef9069ull,
+    0x3fef5818dcfba487ull, 0x3fef7c97337b9b5full, 0x3fefa4afa2a490daull, 0x3fefd0765b6e4540ull};
+
+// expf as glibc computes it for |x| < 88 (sysdeps/ieee754/flt-32/e_expf.c,
+// EXP2F_TABLE_BITS = 5): bit-equal to libm on 2e8 samples in [-11.5, 0.5].
+__device__ __forceinline__ float expf_exact(float x, const unsigned long long *tab)
+{
+    const double InvLn2N = 0x1.71547652b82fep+0 * 32.0, Shift = 0x1.8p52;
+    const double C0 = 0x1.c6af84b912394p-5 / 32.0 / 32.0 / 32.0;
+    const double C1 = 0x1.ebfce50fac4f3p-3 / 32.0 / 32.0;
+    const double C2 = 0x1.62e42ff0c52d6p-1 / 32.0;
+    const double z = dm(InvLn2N, (double)x);
+    double kd = da(z, Shift);
+    const unsigned long long ki = (unsigned long long)__double_as_longlong(kd);
+    kd = ds(kd, Shift);
+    const double r = ds(z, kd);
+    const unsigned long long t = tab[ki & 31ull] + (ki << 47);
+    const double s = __longlong_as_double((long long)t);
+    const double p = da(dm(C0, r), C1);
+    const double r2 = dm(r, r);
+    double y = da(dm(C2, r), 1.0);
+    y = da(dm(p, r2), y);
+    return (float)dm(y, s);
+}
+
+__device__ __forceinline__ float ex2_approx(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct BlendSmem {
+    float4 row[2][FGS_BLEND_BATCH][3];     // (cx,cy,a,b) (c,op,k,r) (g,b,hx,hy)
+    float  z[2][FGS_BLEND_BATCH];          // camera depth of the pair's Gaussian (extras)
+    uint32_t touched[2][FGS_BLEND_BATCH];  // contrib flags of the batch
+    unsigned long long tab[32];
+};
+
+template <bool EXACT, bool CONTRIB, bool EXTRAS>
+__global__ void __launch_bounds__(256)
+k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
+        const uint32_t *__restrict__ vals, const int32_t *__restrict__ starts, int width,
+        int height, int grid_w, int ty_first, float bg0, float bg1, float bg2, float tau,
+        float *__restrict__ rgb, float *__restrict__ alpha_out, float *__restrict__ depth_out,
+        uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
+{
+    __shared__ BlendSmem S;
+    const int tid = threadIdx.x;
+    const int tx = blockIdx.x, ty = ty_first + blockIdx.y;
+    const int tile = ty * grid_w + tx;
+    const int px = tx * FGS_TILE + (tid & 15), py = ty * FGS_TILE + (tid >> 4);
+    const bool inside = px < width && py < height;
+    const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
+
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    if (tid < 32) S.tab[tid] = c_exp2_tab[tid];
+
+    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, dz = 0.0f;
+    bool done = !inside;
+    uint32_t ncontrib = 0;
+
+    const int nb = (n + FGS_BLEND_BATCH - 1) / FGS_BLEND_BATCH;
+    // prologue: rows of batch 0 in flight, indices of batch 1 in flight
+    if (tid < n) {
+        const uint32_t g = vals[start + tid];
+        const float4 *src = (const float4 *)(splat + (size_t)g * 12);
+        cp_async16(&S.row[0][tid][0], src);
+        cp_async16(&S.row[0][tid][1], src + 1);
+        cp_async16(&S.row[0][tid][2], src + 2);
+        if (EXTRAS) S.z[0][tid] = gdepth ? gdepth[g] : 0.0f;
+    }
+    cp_async_commit();
+    uint32_t idx_next = (FGS_BLEND_BATCH + tid < n) ? vals[start + FGS_BLEND_BATCH + tid] : 0u;
+
+    int b = 0;
+    for (; b < nb; ++b) {
+        const int cur = b & 1, nxt = cur ^ 1;
+        // step 1: gather the rows of batch b+1 (their indices arrived during batch b-1)
+        if ((b + 1) * FGS_BLEND_BATCH + tid < n) {
+            const float4 *src = (const float4 *)(splat + (size_t)idx_next * 12);
+            cp_async16(&S.row[nxt][tid][0], src);
+            cp_async16(&S.row[nxt][tid][1], src + 1);
+            cp_async16(&S.row[nxt][tid][2], src + 2);
+            if (EXTRAS) S.z[nxt][tid] = gdepth ? gdepth[idx_next] : 0.0f;
+        }
+        cp_async_commit();
+        // step 2: indices of batch b+2
+        const int i2 = (b + 2) * FGS_BLEND_BATCH + tid;
+        const uint32_t idx_next2 = i2 < n ? vals[start + i2] : 0u;
+        if (CONTRIB) S.touched[cur][tid] = 0u;
+        cp_async_wait<1>();
+        __syncthreads();
+
+        // step 3: blend batch b
+        const int cnt = n - b * FGS_BLEND_BATCH < FGS_BLEND_BATCH ? n - b * FGS_BLEND_BATCH
+                                                                  : FGS_BLEND_BATCH;
+        for (int j0 = 0; j0 < cnt; j0 += 16) {
+            if (__all_sync(FGS_FULL, done)) break;
+            const int j1 = j0 + 16 < cnt ? j0 + 16 : cnt;
+            for (int j = j0; j < j1; ++j) {
+                const float4 r0 = S.row[cur][j][0];
+                const float4 r2 = S.row[cur][j][2];
+                const float dx = fs(fx, r0.x), dy = fs(fy, r0.y);
+                // render.py:211 extent rectangle, exact float32 compares
+                if (done || fabsf(dx) > r2.z || fabsf(dy) > r2.w) continue;
+                const float4 r1 = S.row[cur][j][1];
+                // render.py:213  s = 0.5*(a dx dx + c dy dy) + b dx dy, unfused
+                const float s = fa(fm(0.5f, fa(fm(fm(r0.z, dx), dx), fm(fm(r1.x, dy), dy))),
+                                   fm(fm(r0.w, dx), dy));
+                if (s > fm(0.5f, r1.z)) continue;                 // render.py:214
+                float al;
+                if (EXACT) {
+                    al = fm(r1.y, expf_exact(-s, S.tab));
+                } else {
+                    al = r1.y * ex2_approx(-s * 1.4426950408889634f);
+                    if (fabsf(al - tau) <= tau * 1e-5f) al = fm(r1.y, expf_exact(-s, S.tab));
+                }
+                al = al > FGS_ALPHA_CAP ? FGS_ALPHA_CAP : al;     // render.py:217-218
+                if (al < tau) continue;                           // render.py:219
+                if (EXACT) {
+                    const float wgt = fm(al, T);
+                    cr = fa(cr, fm(r1.w, wgt));
+                    cg = fa(cg, fm(r2.x, wgt));
+                    cb = fa(cb, fm(r2.y, wgt));
+                    if (EXTRAS) dz = fa(dz, fm(S.z[cur][j], wgt));
+                    T = fm(T, fs(1.0f, al));
+                } else {
+                    const float wgt = al * T;
+                    cr = fmaf(r1.w, wgt, cr);
+                    cg = fmaf(r2.x, wgt, cg);
+                    cb = fmaf(r2.y, wgt, cb);
+                    if (EXTRAS) dz = fmaf(S.z[cur][j], wgt, dz);
+                    T = T * (1.0f - al);
+                }
+                if (CONTRIB) S.touched[cur][j] = 1u;
+                done = T < FGS_T_STOP;                            // render.py:228
+            }
+        }
+        const bool all_done = __syncthreads_and(done);
+        if (CONTRIB) {
+            if (tid < cnt) {
+                const uint32_t t = S.touched[cur][tid];
+                contrib[start + b * FGS_BLEND_BATCH + tid] = (uint8_t)t;
+                ncontrib += t;
+            }
+        }
+        idx_next = idx_next2;
+        if (all_done) { ++b; break; }
+    }
+    cp_async_wait<0>();
+    if (CONTRIB)   // pairs behind a whole-tile early exit never touched a pixel
+        for (int i = b * FGS_BLEND_BATCH + tid; i < n; i += FGS_BLEND_BATCH) contrib[start + i] = 0;
+
+    if (inside) {
+        const size_t o = (size_t)py * width + px;
+        if (EXACT) {
+            rgb[3 * o + 0] = fa(cr, fm(T, bg0));                  // render.py:250-252
+            rgb[3 * o + 1] = fa(cg, fm(T, bg1));
+            rgb[3 * o + 2] = fa(cb, fm(T, bg2));
+        } else {
+            rgb[3 * o + 0] = fmaf(T, bg0, cr);
+            rgb[3 * o + 1] = fmaf(T, bg1, cg);
+            rgb[3 * o + 2] = fmaf(T, bg2, cb);
+        }
+        if (EXTRAS) {
+            if (alpha_out) alpha_out[o] = 1.0f - T;
+            if (depth_out) depth_out[o] = dz;
+        }
+    }
+    if (CONTRIB) {
+        ncontrib = __reduce_add_sync(FGS_FULL, ncontrib);
+        if ((tid & 31) == 0 && ncontrib) atomicAdd(&stats->pairs_contributing, ncontrib);
+    }
+}
+
+template <bool EXACT, bool CONTRIB>
+int launch(bool extras, dim3 grid, cudaStream_t st, const float *splat, const float *gdepth,
+           const uint32_t *vals, const int32_t *starts, int width, int height, int grid_w,
+           int ty_first, const float bg[3], float tau, float *rgb, float *alpha, float *depth,
+           uint8_t *contrib, fgs_stats *stats)
+{
+    if (extras)
+        k_blend<EXACT, CONTRIB, true><<<grid, 256, 0, st>>>(splat, gdepth, vals, starts, width,
+            height, grid_w, ty_first, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+    else
+        k_blend<EXACT, CONTRIB, false><<<grid, 256, 0, st>>>(splat, gdepth, vals, starts, width,
+            height, grid_w, ty_first, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+    FGS_AFTER_LAUNCH(st);
+    return FGS_OK;
+}
+
+}  // namespace
+
+int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
+                     const int32_t *starts, int width, int height, const float bg[3], double tau,
+                     int flags, int band0, int band1, float *rgb, float *alpha, float *depth,
+                     uint8_t *contrib, fgs_stats *stats, cudaStream_t st)
+{
+    const int grid_w = (width + FGS_TILE - 1) / FGS_TILE;
+    if (band1 < band0) return FGS_OK;
+    const dim3 grid((unsigned)grid_w, (unsigned)(band1 - band0 + 1));
+    const bool exact = flags & FGS_BLEND_EXACT, want_contrib = (flags & FGS_BLEND_CONTRIB) && contrib;
+    const bool extras = (alpha != nullptr) || (depth != nullptr && gdepth != nullptr);
+    if (depth != nullptr && gdepth == nullptr) return FGS_E_ARG;
+    const float tau32 = (float)tau;
+#define FGS_GO(E, C) launch<E, C>(extras, grid, st, splat, gdepth, vals, starts, width, height, \
+                                  grid_w, band0, bg, tau32, rgb, alpha, depth, contrib, stats)
+    if (exact) return want_contrib ? FGS_GO(true, true) : FGS_GO(true, false);
+    return want_contrib ? FGS_GO(false, true) : FGS_GO(false, false);
+#undef FGS_GO
+}

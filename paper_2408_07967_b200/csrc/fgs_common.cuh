@@ -1,0 +1,201 @@
+// Shared device/host definitions for the sm_100a rasterizer kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/flashgs_b200.h"
+
+#define FGS_WARP 32
+#define FGS_FULL 0xffffffffu
+
+// ---- constants.py:4-32, as float32 / float64 literals --------------------
+#define FGS_Z_NEAR        0.2f
+#define FGS_DILATION      0.3f
+#define FGS_MAX_CUTOFF    9.0
+#define FGS_ALPHA_CAP     0.99f
+#define FGS_T_STOP        1e-4f
+#define FGS_CUTOFF_SLACK  1.5e-6f
+
+// ---- launch shapes ---------------------------------------------------------
+#define FGS_PRE_THREADS   256      // K1 / K3: one Gaussian per thread
+#define FGS_SORT_THREADS  256
+#define FGS_SORT_IPT      16
+#define FGS_SORT_TILE     (FGS_SORT_THREADS * FGS_SORT_IPT)   // 4096 pairs per CTA pass
+#define FGS_SORT_MAXPASS  16
+#define FGS_BLEND_BATCH   256
+
+// Camera as the kernels see it (passed by value: lives in the constant bank).
+struct CamDev {
+    float v[12];          // world_to_camera rows 0..2
+    float p0[4], p1[4], p3[4];   // full_projection rows 0, 1, 3
+    float pos[3];
+    float limx, limy;     // f32(1.3 * tan_fov)   projection.py:100-101
+    float fx, fy;         // f32(focal)           projection.py:104-105
+    float wf, hf;         // f32(width), f32(height)
+    int   width, height, grid_w, grid_h;
+};
+
+// Packed device scene: float4 planes of stride `n` (P rounded up to 32).
+//   g0[i] = (mean.xyz, opacity)   g1[i] = (scale.xyz, 0)   g2[i] = quat wxyz
+//   sh[j*n + i] = floats 4j..4j+3 of Gaussian i's 48 SH coefficients
+struct SceneDev {
+    const float4 *g0, *g1, *g2, *sh;
+    int64_t n;
+};
+
+static inline int64_t fgs_pad32(int64_t p) { return (p + 31) & ~(int64_t)31; }
+
+static inline SceneDev fgs_scene_view(const void *packed, int64_t P)
+{
+    SceneDev s;
+    s.n = fgs_pad32(P);
+    const float4 *b = (const float4 *)packed;
+    s.g0 = b;
+    s.g1 = b + s.n;
+    s.g2 = b + 2 * s.n;
+    s.sh = b + 3 * s.n;
+    return s;
+}
+
+// Frame buffers resolved from (workspace, layout).
+struct FrameDev {
+    float    *splat;
+    float    *depth;
+    ushort4  *rects;
+    uint8_t  *flags;
+    uint32_t *counts;
+    uint32_t *blocksums;    // [nblocks]
+    uint32_t *blockbase;    // [nblocks]
+    uint64_t *keys[2];
+    uint32_t *vals[2];
+    uint64_t *sortstate;
+    uint32_t *hist;         // [FGS_SORT_MAXPASS][256]
+    uint32_t *tickets;      // [FGS_SORT_MAXPASS]
+    int32_t  *starts;
+    uint8_t  *contrib;
+    fgs_stats *stats;
+};
+
+static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
+{
+    char *b = (char *)ws;
+    FrameDev f;
+    f.splat = (float *)(b + L->off_splat);
+    f.depth = (float *)(b + L->off_depth);
+    f.rects = (ushort4 *)(b + L->off_rects);
+    f.flags = (uint8_t *)(b + L->off_flags);
+    f.counts = (uint32_t *)(b + L->off_counts);
+    f.blocksums = (uint32_t *)(b + L->off_blocksums);
+    f.blockbase = f.blocksums + L->preprocess_blocks;
+    f.keys[0] = (uint64_t *)(b + L->off_keys[0]);
+    f.keys[1] = (uint64_t *)(b + L->off_keys[1]);
+    f.vals[0] = (uint32_t *)(b + L->off_vals[0]);
+    f.vals[1] = (uint32_t *)(b + L->off_vals[1]);
+    f.sortstate = (uint64_t *)(b + L->off_sortstate);
+    f.hist = (uint32_t *)(b + L->off_hist);
+    f.tickets = f.hist + FGS_SORT_MAXPASS * 256;
+    f.starts = (int32_t *)(b + L->off_starts);
+    f.contrib = (uint8_t *)(b + L->off_contrib);
+    f.stats = (fgs_stats *)(b + L->off_stats);
+    return f;
+}
+
+// Internal launchers (one translation unit per stage).
+int  fgs_launch_pack(const float *means, const float *opac, const float *scales,
+                     const float *rots, const float *sh, int64_t P, void *packed,
+                     cudaStream_t st);
+int  fgs_launch_cutoffs(const SceneDev &sc, int64_t P, double tau, float *k, cudaStream_t st);
+int  fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, const CamDev &cam,
+                           double tau, int sh_degree, int strategy, int band0, int band1,
+                           const FrameDev &f, cudaStream_t st);
+int  fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream_t st);
+int  fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int band1,
+                     const FrameDev &f, cudaStream_t st);
+
+struct SortPlan {
+    int npass;
+    int on_value[FGS_SORT_MAXPASS];
+    int shift[FGS_SORT_MAXPASS];
+    int bits[FGS_SORT_MAXPASS];
+    int compact;      // digits taken from ((key >> 32) << 31) | (key & 0x7fffffff)
+};
+SortPlan fgs_sort_plan(int tile_bits, int value_bits, int compact);
+int  fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev, int64_t n_max,
+                     const SortPlan &plan, uint64_t *state, uint32_t *hist, uint32_t *tickets,
+                     uint32_t epoch, cudaStream_t st);
+int  fgs_launch_ranges(const uint64_t *keys, const uint32_t *n_dev, int64_t n_max, int tiles,
+                       int32_t *starts, fgs_stats *stats, cudaStream_t st);
+int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
+                      const int32_t *starts, int width, int height, const float bg[3],
+                      double tau, int flags, int band0, int band1, float *rgb, float *alpha,
+                      float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st);
+
+void fgs_set_cuda_error(cudaError_t e);
+// Records the next caller-supplied profiling event on `st` (no-op unless
+// fgs_profile_begin armed this thread).  Called after every kernel launch.
+void fgs_prof_mark(cudaStream_t st);
+
+#define FGS_CHECK_LAUNCH()                                   \
+    do {                                                     \
+        cudaError_t e__ = cudaGetLastError();                \
+        if (e__ != cudaSuccess) {                            \
+            fgs_set_cuda_error(e__);                         \
+            return FGS_E_CUDA;                               \
+        }                                                    \
+    } while (0)
+
+// launch check + profiling mark, for the per-frame kernels
+#define FGS_AFTER_LAUNCH(st) \
+    do {                     \
+        FGS_CHECK_LAUNCH();  \
+        fgs_prof_mark(st);   \
+    } while (0)
+
+#ifdef __CUDACC__
+// Individually rounded float32 / float64 arithmetic: these intrinsics are never
+// contracted into FMAs, which is what keeps the geometry bit-identical to the
+// reference's NumPy ufunc chains.
+__device__ __forceinline__ float  fm(float a, float b)   { return __fmul_rn(a, b); }
+__device__ __forceinline__ float  fa(float a, float b)   { return __fadd_rn(a, b); }
+__device__ __forceinline__ float  fs(float a, float b)   { return __fsub_rn(a, b); }
+__device__ __forceinline__ float  fd(float a, float b)   { return __fdiv_rn(a, b); }
+__device__ __forceinline__ float  fsq(float a)           { return __fsqrt_rn(a); }
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __forceinline__ uint32_t lanemask_lt()
+{
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane)
+{
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(FGS_FULL, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// Exclusive scan over the 256 threads of a CTA; also returns the CTA total.
+// `scratch` is 8 uint32 in shared memory.  Contains two barriers.
+__device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t *scratch,
+                                                        uint32_t &total)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = warp_incl_scan(v, lane);
+    if (lane == 31) scratch[w] = incl;
+    __syncthreads();
+    uint32_t wsum = lane < 8 ? scratch[lane] : 0u;
+    uint32_t wincl = warp_incl_scan(wsum, lane);
+    uint32_t wbase = __shfl_sync(FGS_FULL, wincl - wsum, w);
+    total = __shfl_sync(FGS_FULL, wincl, 7);
+    __syncthreads();
+    return wbase + incl - v;
+}
+#endif

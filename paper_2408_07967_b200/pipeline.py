@@ -1,0 +1,599 @@
+"""Host side of the B200 rasterizer: the reference's Python call surface.
+
+Mirrors ``tilesplat.pipeline`` (reference ``pipeline.py``) name for name:
+
+* ``Pipeline(scene, sh_degree=3).render(camera, strategy, tau, background,
+  workers, initial_capacity, pipelined) -> (Framebuffer, FrameStats)``
+  -- ``pipeline.py:65-111``
+* ``run_frame`` -- ``pipeline.py:114-119``; ``psnr`` / ``max_abs_diff`` --
+  ``pipeline.py:122-139``
+* stage entry points ``preprocess_and_bin`` (``binning.py:197``),
+  ``sort_pairs`` (``sorting.py:101``), ``tile_range_table`` (``sorting.py:139``),
+  ``render_frame`` (``render.py:273``), ``power_cutoffs`` (``extent.py:19``)
+  so intermediates can be diffed against the oracle.
+
+All compute happens in ``libflashgs_b200.so`` (hand-written sm_100a CUDA)
+through the C ABI in ``include/flashgs_b200.h``; torch only owns device
+memory and streams.  There is no CPU fallback: without the library or a CUDA
+device these functions raise.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import time
+import weakref
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from . import _capi
+from .scene import activate, is_activated_scene, is_raw_scene
+
+TAU_DEFAULT = 1.0 / 255.0          # constants.py:8
+TILE_SIZE = 16                     # constants.py:4
+STRATEGIES = _capi.STRATEGIES
+
+
+class UnsortedPairsError(ValueError):
+    """Range extraction was handed keys that are not nondecreasing
+    (reference ``sorting.py:25-26``)."""
+
+
+def _torch():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2408_07967_b200 needs a CUDA device (no CPU fallback)")
+    return torch
+
+
+@dataclass
+class FrameStats:
+    """Same fields as the reference's FrameStats (``pipeline.py:28-48``); the
+    stage times are CUDA-event times of the kernels of each stage."""
+
+    strategy: str
+    tau: float
+    workers: int
+    preprocess_bin_ns: int = 0
+    sort_ns: int = 0
+    render_ns: int = 0
+    total_ns: int = 0
+    pairs_emitted: int = 0
+    pairs_contributing: int = 0
+    gaussians_retained: int = 0
+    gaussians_degenerate: int = 0
+    tiles_nonempty: int = 0
+    pair_buffer_bytes: int = 0
+    buffer_regrows: int = 0
+    # extras (not in the reference)
+    candidate_tiles: int = 0
+    e2e_ns: int = 0                # host wall clock of the call incl. the D2H copy
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+@dataclass
+class Framebuffer:
+    image: object                  # (H, W, 3) float32: numpy (default) or CUDA tensor
+    background: np.ndarray         # (3,) float32
+    alpha: object = None           # (H, W) = 1 - T_final           (extras=True)
+    depth: object = None           # (H, W) = sum blend weight * z  (extras=True)
+
+    @property
+    def width(self) -> int:
+        return int(self.image.shape[1])
+
+    @property
+    def height(self) -> int:
+        return int(self.image.shape[0])
+
+
+def _strategy_id(strategy):
+    if strategy not in _capi.STRATEGY_ID:
+        raise ValueError(f"unknown strategy {strategy!r}, expected one of {STRATEGIES}")
+    return _capi.STRATEGY_ID[strategy]
+
+
+def _check_sh_degree(d):
+    if not 0 <= int(d) <= 3:
+        raise ValueError("SH degree must be in 0..3")
+    return int(d)
+
+
+def _stream_ptr(torch, device):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class _PinnedPool:
+    """Recycles pinned host frames: a frame handed to the caller returns to the
+    pool when the caller's ndarray is garbage-collected."""
+
+    def __init__(self):
+        self._free = {}
+        self._lock = threading.Lock()
+
+    def take(self, torch, shape, dtype):
+        key = (tuple(shape), str(dtype))
+        with self._lock:
+            lst = self._free.get(key)
+            if lst:
+                return lst.pop()
+        return torch.empty(shape, dtype=dtype, pin_memory=True)
+
+    def give(self, t):
+        key = (tuple(t.shape), str(t.dtype))
+        with self._lock:
+            lst = self._free.setdefault(key, [])
+            if len(lst) < 4:
+                lst.append(t)
+
+    def as_numpy(self, t):
+        arr = t.numpy()
+        weakref.finalize(arr, self.give, t)
+        return arr
+
+
+_pinned = _PinnedPool()
+
+
+class _Workspace:
+    """Per-frame device buffers for one (P, W, H, capacity): allocated once,
+    reused every frame (the paper's static allocation)."""
+
+    def __init__(self, torch, device, P, width, height, capacity):
+        self.lay = _capi.layout(P, width, height, capacity)
+        self.capacity = int(capacity)
+        self.buf = torch.empty(int(self.lay.total_bytes), dtype=torch.uint8, device=device)
+        self.base = self.buf.data_ptr()
+        self.rgb = torch.empty((height, width, 3), dtype=torch.float32, device=device)
+        self.alpha = None
+        self.depthmap = None
+        self.h_stats = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+        self.epoch = 1
+        _capi.check(_capi.lib().fgs_workspace_init(C.c_void_p(self.base), C.byref(self.lay),
+                                                   _stream_ptr(torch, device)))
+
+    def next_epoch(self):
+        e = self.epoch
+        self.epoch += 16
+        if self.epoch > 0xfffffff0:
+            raise RuntimeError("workspace epoch exhausted; create a new Pipeline")
+        return e
+
+    def view(self, torch, off, nbytes, dtype):
+        return self.buf[int(off):int(off) + int(nbytes)].view(dtype)
+
+    def stats_tensor(self):
+        return self.buf[int(self.lay.off_stats):int(self.lay.off_stats) + 64]
+
+
+class Pipeline:
+    """Holds a scene resident in HBM; renders frames for arbitrary cameras.
+
+    ``scene`` may be a raw ``Scene`` or an ``ActivatedScene`` -- ours or the
+    reference's own dataclasses (matched on field names), as ``pipeline.py:68-75``.
+    ``render`` is safe to call from several threads on one object (each call
+    takes its own workspace, SURVEY.md §8(b) threading row).
+    """
+
+    def __init__(self, scene, sh_degree=3, device=None):
+        if is_raw_scene(scene):
+            act = activate(scene)
+        elif is_activated_scene(scene):
+            act = scene
+        else:
+            raise TypeError("scene must be a Scene or ActivatedScene")
+        torch = _torch()
+        self.sh_degree = int(sh_degree)
+        self.activated = act
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
+            else torch.device(device)
+        self.count = int(np.asarray(act.means).shape[0])
+        L = _capi.lib()
+        with torch.cuda.device(self.device):
+            f32 = lambda a, shape: torch.from_numpy(
+                np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(shape))).to(self.device)
+            P = self.count
+            means, opac = f32(act.means, (P, 3)), f32(act.opacities, (P,))
+            scales, rots = f32(act.scales, (P, 3)), f32(act.rotations, (P, 4))
+            sh = f32(act.sh, (P, 48))
+            self.scene_bytes = int(L.fgs_scene_bytes(P))
+            self.packed = torch.empty(max(self.scene_bytes, 16), dtype=torch.uint8, device=self.device)
+            _capi.check(L.fgs_scene_pack(means.data_ptr(), opac.data_ptr(), scales.data_ptr(),
+                                         rots.data_ptr(), sh.data_ptr(), P,
+                                         self.packed.data_ptr(), _stream_ptr(torch, self.device)))
+            torch.cuda.current_stream(self.device).synchronize()
+        self._kcut = {}
+        self._free = {}
+        self._lock = threading.Lock()
+        self._last_pairs = 0
+
+    # -- per-tau cutoff table (extent.py:19-30), cached -------------------------
+    def _cutoffs(self, torch, tau):
+        key = float(tau)
+        with self._lock:
+            k = self._kcut.get(key)
+        if k is None:
+            k = torch.empty(max(self.count, 1), dtype=torch.float32, device=self.device)
+            _capi.check(_capi.lib().fgs_power_cutoffs(self.packed.data_ptr(), self.count, key,
+                                                      k.data_ptr(), _stream_ptr(torch, self.device)))
+            with self._lock:
+                if len(self._kcut) > 8:
+                    self._kcut.clear()
+                self._kcut[key] = k
+        return k
+
+    # -- workspace pool ---------------------------------------------------------
+    def _default_capacity(self):
+        return int(max(1 << 16, 8 * self.count, 1.25 * self._last_pairs + 4096))
+
+    def _take_ws(self, torch, width, height, capacity):
+        key = (int(width), int(height))
+        with self._lock:
+            lst = self._free.get(key, [])
+            for i, ws in enumerate(lst):
+                if ws.capacity >= capacity:
+                    return lst.pop(i)
+            if lst:
+                lst.pop()          # too small: drop one, allocate a bigger one
+        return _Workspace(torch, self.device, self.count, width, height, capacity)
+
+    def _give_ws(self, ws):
+        key = (int(ws.lay.width), int(ws.lay.height))
+        with self._lock:
+            lst = self._free.setdefault(key, [])
+            if len(lst) < 4:
+                lst.append(ws)
+
+    # -- the hot path -----------------------------------------------------------
+    def render(self, camera, strategy="precise", tau=TAU_DEFAULT,
+               background=(0.0, 0.0, 0.0), workers=1, initial_capacity=None,
+               pipelined=True, *, exact=False, extras=False, contrib=True,
+               as_numpy=True, band=None, timing=True):
+        """bin -> sort -> render on the GPU; returns (Framebuffer, FrameStats).
+
+        ``workers`` and ``pipelined`` are accepted for signature compatibility
+        and do not change the result (the reference guarantees the same).
+        Keyword-only extras: ``exact`` (bit-identical frame, FP64 expf),
+        ``extras`` (alpha + depth maps), ``contrib`` (pairs_contributing),
+        ``as_numpy`` (False: CUDA tensors, no D2H), ``band=(ty0, ty1)`` tile-row
+        band for multi-GPU row splitting.
+        """
+        torch = _torch()
+        t_host0 = time.perf_counter_ns()
+        sid = _strategy_id(strategy)
+        deg = _check_sh_degree(self.sh_degree)
+        L = _capi.lib()
+        cam = _capi.camera_struct(camera)
+        W, H = int(camera.width), int(camera.height)
+        gh = -(-H // TILE_SIZE)
+        b0, b1 = (0, gh - 1) if band is None else (int(band[0]), int(band[1]))
+        if not (0 <= b0 <= b1 < gh):
+            raise ValueError(f"band {band!r} outside the {gh} tile rows")
+        bg = np.asarray(background, dtype=np.float32).reshape(3)
+        bg_c = (C.c_float * 3)(*bg.tolist())
+        flags = (_capi.BLEND_EXACT if exact else 0) | (_capi.BLEND_CONTRIB if contrib else 0)
+        stats = FrameStats(strategy=strategy, tau=float(tau), workers=max(1, int(workers)))
+        capacity = int(initial_capacity) if initial_capacity is not None else self._default_capacity()
+        capacity = max(capacity, 1)
+
+        with torch.cuda.device(self.device):
+            st = _stream_ptr(torch, self.device)
+            kcut = self._cutoffs(torch, tau)
+            while True:
+                ws = self._take_ws(torch, W, H, capacity)
+                lay = C.byref(ws.lay)
+                base = C.c_void_p(ws.base)
+                if extras:
+                    if ws.alpha is None:
+                        ws.alpha = torch.empty((H, W), dtype=torch.float32, device=self.device)
+                        ws.depthmap = torch.empty((H, W), dtype=torch.float32, device=self.device)
+                    a_ptr, d_ptr = ws.alpha.data_ptr(), ws.depthmap.data_ptr()
+                else:
+                    a_ptr = d_ptr = None
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing else None
+                if timing:
+                    ev[0].record()
+                _capi.check(L.fgs_preprocess(self.packed.data_ptr(), kcut.data_ptr(), self.count,
+                                             C.byref(cam), float(tau), deg, sid, b0, b1, base, lay, st))
+                _capi.check(L.fgs_scan(base, lay, st))
+                _capi.check(L.fgs_emit(C.byref(cam), sid, b0, b1, base, lay, st))
+                if timing:
+                    ev[1].record()
+                _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
+                _capi.check(L.fgs_ranges(base, lay, st))
+                if timing:
+                    ev[2].record()
+                _capi.check(L.fgs_blend(bg_c, float(tau), flags, b0, b1, ws.rgb.data_ptr(),
+                                        a_ptr, d_ptr, base, lay, st))
+                if timing:
+                    ev[3].record()
+                ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
+                h_rgb = None
+                if as_numpy:
+                    h_rgb = _pinned.take(torch, (H, W, 3), torch.float32)
+                    h_rgb.copy_(ws.rgb, non_blocking=True)
+                    if extras:
+                        h_a = _pinned.take(torch, (H, W), torch.float32)
+                        h_d = _pinned.take(torch, (H, W), torch.float32)
+                        h_a.copy_(ws.alpha, non_blocking=True)
+                        h_d.copy_(ws.depthmap, non_blocking=True)
+                torch.cuda.current_stream(self.device).synchronize()
+                s = np.frombuffer(ws.h_stats.numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+                if int(s["overflow"]):
+                    # binning.py:134-143: grow, never truncate; counted in the stats
+                    stats.buffer_regrows += 1
+                    need = int(s["pairs_emitted"])
+                    capacity = max(int(capacity * 1.5) + 16, need + need // 8 + 4096)
+                    if h_rgb is not None:
+                        _pinned.give(h_rgb)
+                    continue
+                break
+            if int(s["bad_depth"]):
+                self._give_ws(ws)
+                raise ValueError("depths must be positive and finite (cull failed upstream)")
+            if timing:
+                stats.preprocess_bin_ns = int(ev[0].elapsed_time(ev[1]) * 1e6)
+                stats.sort_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
+                stats.render_ns = int(ev[2].elapsed_time(ev[3]) * 1e6)
+                stats.total_ns = int(ev[0].elapsed_time(ev[3]) * 1e6)
+            stats.pairs_emitted = int(s["pairs_emitted"])
+            stats.pairs_contributing = int(s["pairs_contributing"])
+            stats.gaussians_retained = int(s["gaussians_retained"])
+            stats.gaussians_degenerate = int(s["gaussians_degenerate"])
+            stats.tiles_nonempty = int(s["tiles_nonempty"])
+            stats.pair_buffer_bytes = 12 * stats.pairs_emitted
+            stats.candidate_tiles = int(s["candidate_tiles_lo"]) | (int(s["candidate_tiles_hi"]) << 32)
+            self._last_pairs = max(self._last_pairs, stats.pairs_emitted)
+            if as_numpy:
+                fb = Framebuffer(_pinned.as_numpy(h_rgb), bg)
+                if extras:
+                    fb.alpha, fb.depth = _pinned.as_numpy(h_a), _pinned.as_numpy(h_d)
+            else:
+                fb = Framebuffer(ws.rgb.clone(), bg)
+                if extras:
+                    fb.alpha, fb.depth = ws.alpha.clone(), ws.depthmap.clone()
+            self._give_ws(ws)
+        stats.e2e_ns = time.perf_counter_ns() - t_host0
+        return fb, stats
+
+
+def run_frame(scene, camera, strategy="precise", tau=TAU_DEFAULT,
+              background=(0.0, 0.0, 0.0), workers=1, sh_degree=3, **kwargs):
+    """One-shot convenience wrapper (``pipeline.py:114-119``)."""
+    return Pipeline(scene, sh_degree=sh_degree).render(
+        camera, strategy, tau, background, workers, **kwargs)
+
+
+def _img(a):
+    x = a.image if isinstance(a, Framebuffer) else a
+    if hasattr(x, "detach"):
+        x = x.detach().cpu().numpy()
+    return np.asarray(x)
+
+
+def psnr(a, b):
+    """PSNR in dB over [0, 1] channels; "identical" when MSE is 0 (``pipeline.py:122-131``)."""
+    ia, ib = _img(a), _img(b)
+    if ia.shape != ib.shape:
+        raise ValueError(f"shape mismatch: {ia.shape} vs {ib.shape}")
+    mse = float(np.mean((ia.astype(np.float64) - ib.astype(np.float64)) ** 2))
+    if mse == 0.0:
+        return "identical"
+    return 10.0 * math.log10(1.0 / mse)
+
+
+def max_abs_diff(a, b) -> float:
+    ia, ib = _img(a), _img(b)
+    if ia.size == 0:
+        return 0.0
+    return float(np.max(np.abs(ia.astype(np.float64) - ib.astype(np.float64))))
+
+
+# ----------------------------------------------------------------------------
+# stage-level entry points (numpy in / numpy out), for diffing against the oracle
+# ----------------------------------------------------------------------------
+
+@dataclass
+class BinOutput:
+    """Same fields as the reference's BinOutput (``binning.py:150-173``)."""
+
+    splat: np.ndarray
+    depth: np.ndarray
+    retained: np.ndarray
+    tile_rects: np.ndarray
+    tile_counts: np.ndarray
+    keys: np.ndarray
+    values: np.ndarray
+    emitted_count: int
+    gaussians_retained: int
+    gaussians_degenerate: int
+    buffer_regrows: int
+    capacity: int
+    grid_w: int
+    grid_h: int
+    strategy: str
+    tau: float
+    pair_counts: np.ndarray = field(default=None, repr=False)
+
+    @property
+    def pair_buffer_bytes(self) -> int:
+        return self.emitted_count * 12
+
+
+def power_cutoffs(alpha0, tau=TAU_DEFAULT):
+    """(k float32, keep mask) on the GPU (``extent.py:19-30``)."""
+    torch = _torch()
+    a = np.ascontiguousarray(np.atleast_1d(alpha0), dtype=np.float32)
+    n = a.shape[0]
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L = _capi.lib()
+    # pack a throw-away scene whose only live field is the opacity
+    z3, z4, zs = np.zeros((n, 3), np.float32), np.zeros((n, 4), np.float32), np.zeros((n, 48), np.float32)
+    t = [torch.from_numpy(x).to(dev) for x in (z3, a, z3, z4, zs)]
+    packed = torch.empty(max(int(L.fgs_scene_bytes(n)), 16), dtype=torch.uint8, device=dev)
+    st = _stream_ptr(torch, dev)
+    _capi.check(L.fgs_scene_pack(*[x.data_ptr() for x in t], n, packed.data_ptr(), st))
+    k = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
+    _capi.check(L.fgs_power_cutoffs(packed.data_ptr(), n, float(tau), k.data_ptr(), st))
+    return k[:n].cpu().numpy(), a > np.float32(tau)
+
+
+def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, workers=1,
+                       sh_degree=3, chunk_size=None, initial_capacity=None,
+                       band=None) -> BinOutput:
+    """K1 + K2 + K3 for one camera; pairs come back in emission order
+    (ascending Gaussian index), unsorted (``binning.py:197-372``)."""
+    torch = _torch()
+    sid = _strategy_id(strategy)
+    deg = _check_sh_degree(sh_degree)
+    pipe = scene if isinstance(scene, Pipeline) else Pipeline(scene, sh_degree=deg)
+    L = _capi.lib()
+    cam = _capi.camera_struct(camera)
+    W, H = int(camera.width), int(camera.height)
+    gw, gh = -(-W // TILE_SIZE), -(-H // TILE_SIZE)
+    b0, b1 = (0, gh - 1) if band is None else (int(band[0]), int(band[1]))
+    capacity = max(1, int(initial_capacity) if initial_capacity is not None
+                   else pipe._default_capacity())
+    regrows = 0
+    P = pipe.count
+    with torch.cuda.device(pipe.device):
+        st = _stream_ptr(torch, pipe.device)
+        kcut = pipe._cutoffs(torch, tau)
+        while True:
+            ws = pipe._take_ws(torch, W, H, capacity)
+            lay, base = C.byref(ws.lay), C.c_void_p(ws.base)
+            _capi.check(L.fgs_preprocess(pipe.packed.data_ptr(), kcut.data_ptr(), P, C.byref(cam),
+                                         float(tau), deg, sid, b0, b1, base, lay, st))
+            _capi.check(L.fgs_scan(base, lay, st))
+            _capi.check(L.fgs_emit(C.byref(cam), sid, b0, b1, base, lay, st))
+            s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+            if int(s["overflow"]):
+                regrows += 1
+                need = int(s["pairs_emitted"])
+                capacity = max(int(capacity * 1.5) + 16, need)
+                continue
+            break
+        if int(s["bad_depth"]):
+            raise ValueError("depths must be positive and finite (cull failed upstream)")
+        M = int(s["pairs_emitted"])
+        lay = ws.lay
+        flags = ws.view(torch, lay.off_flags, P, torch.uint8).cpu().numpy()
+        retained = (flags & 1).astype(bool)
+        splat = ws.view(torch, lay.off_splat, P * 48, torch.float32).cpu().numpy().reshape(P, 12).copy()
+        splat[~retained] = 0.0                           # binning.py:208 zero rows
+        depth = ws.view(torch, lay.off_depth, P * 4, torch.float32).cpu().numpy().copy()
+        rects = ws.view(torch, lay.off_rects, P * 8, torch.int16).cpu().numpy() \
+            .view(np.uint16).reshape(P, 4).astype(np.int32)
+        counts = ws.view(torch, lay.off_counts, P * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
+        keys = ws.view(torch, lay.off_keys[0], M * 8, torch.int64).cpu().numpy().view(np.uint64).copy()
+        vals = ws.view(torch, lay.off_vals[0], M * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
+        cap = ws.capacity
+        pipe._give_ws(ws)
+    nx = rects[:, 2] - rects[:, 0] + 1
+    ny = rects[:, 3] - rects[:, 1] + 1
+    return BinOutput(
+        splat=splat, depth=depth, retained=retained, tile_rects=rects,
+        tile_counts=np.where(retained, (nx * ny).astype(np.int64), 0),
+        keys=keys, values=vals, emitted_count=M,
+        gaussians_retained=int(s["gaussians_retained"]),
+        gaussians_degenerate=int(s["gaussians_degenerate"]),
+        buffer_regrows=regrows, capacity=int(cap), grid_w=gw, grid_h=gh,
+        strategy=strategy, tau=float(tau), pair_counts=counts.astype(np.int64))
+
+
+def _byte_width(max_exclusive: int) -> int:
+    if max_exclusive <= 1:
+        return 0
+    return ((int(max_exclusive) - 1).bit_length() + 7) // 8
+
+
+_sort_epoch = [1]
+
+
+def sort_pairs(keys, values, workers=1, grid_tiles=None, max_value=None):
+    """Sort pairs by key, ties by ascending value, on the GPU (``sorting.py:101-136``).
+    Inputs are not mutated; returns new numpy arrays."""
+    torch = _torch()
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    values = np.ascontiguousarray(values, dtype=np.uint32)
+    n = keys.shape[0]
+    if values.shape[0] != n:
+        raise ValueError("keys and values must have equal length")
+    if n == 0:
+        return keys.copy(), values.copy()
+    value_bits = 32 if max_value is None else 8 * _byte_width(int(max_value))
+    tile_bits = 32 if grid_tiles is None else 8 * _byte_width(int(grid_tiles))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    L = _capi.lib()
+    k_in = torch.from_numpy(keys.view(np.int64)).to(dev)
+    v_in = torch.from_numpy(values.view(np.int32)).to(dev)
+    k_out, v_out = torch.empty_like(k_in), torch.empty_like(v_in)
+    nbytes = int(L.fgs_sort_pairs_scratch_bytes(n))
+    scratch = torch.zeros(nbytes, dtype=torch.uint8, device=dev)
+    _sort_epoch[0] += 64
+    _capi.check(L.fgs_sort_pairs(k_in.data_ptr(), v_in.data_ptr(), n, tile_bits, value_bits,
+                                 k_out.data_ptr(), v_out.data_ptr(), scratch.data_ptr(), nbytes,
+                                 _sort_epoch[0], _stream_ptr(torch, dev)))
+    return k_out.cpu().numpy().view(np.uint64), v_out.cpu().numpy().view(np.uint32)
+
+
+def tile_range_table(sorted_keys, grid_w, grid_h) -> np.ndarray:
+    """Half-open per-tile ranges as a (tiles + 1,) int64 array (``sorting.py:139-152``)."""
+    torch = _torch()
+    keys = np.ascontiguousarray(sorted_keys, dtype=np.uint64)
+    tiles = int(grid_w) * int(grid_h)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    k = torch.from_numpy(keys.view(np.int64)).to(dev)
+    starts = torch.empty(tiles + 1, dtype=torch.int32, device=dev)
+    stats = torch.zeros(64, dtype=torch.uint8, device=dev)
+    _capi.check(_capi.lib().fgs_tile_ranges(k.data_ptr() if keys.size else None, keys.shape[0],
+                                            tiles, starts.data_ptr(), stats.data_ptr(),
+                                            _stream_ptr(torch, dev)))
+    s = np.frombuffer(stats.cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+    if int(s["unsorted"]):
+        raise UnsortedPairsError("pair keys are not nondecreasing")
+    if int(s["tile_out_of_grid"]):
+        raise ValueError("tile index exceeds the grid")
+    return starts.cpu().numpy().astype(np.int64)
+
+
+def render_frame(splat, sorted_values, starts, width, height, background, tau,
+                 workers=1, pipelined=True, *, exact=False, gaussian_depth=None):
+    """K6 on caller-supplied arrays (``render.py:273-310``).  Returns
+    (image (H,W,3) float32, contrib flags per pair, nonempty tile count), plus
+    (alpha, depth) maps when ``gaussian_depth`` is given."""
+    torch = _torch()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    sp = torch.from_numpy(np.ascontiguousarray(splat, dtype=np.float32)).to(dev)
+    vals_np = np.ascontiguousarray(sorted_values, dtype=np.uint32)
+    vals = torch.from_numpy(vals_np.view(np.int32)).to(dev)
+    st_np = np.ascontiguousarray(starts, dtype=np.int64)
+    st32 = torch.from_numpy(st_np.astype(np.int32)).to(dev)
+    bg = np.asarray(background, dtype=np.float32).reshape(3)
+    bg_c = (C.c_float * 3)(*bg.tolist())
+    rgb = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
+    contrib = torch.zeros(max(vals_np.shape[0], 1), dtype=torch.uint8, device=dev)
+    stats = torch.zeros(64, dtype=torch.uint8, device=dev)
+    extras = gaussian_depth is not None
+    if extras:
+        gd = torch.from_numpy(np.ascontiguousarray(gaussian_depth, dtype=np.float32)).to(dev)
+        alpha = torch.empty((height, width), dtype=torch.float32, device=dev)
+        dmap = torch.empty((height, width), dtype=torch.float32, device=dev)
+    gh = -(-int(height) // TILE_SIZE)
+    flags = (_capi.BLEND_EXACT if exact else 0) | _capi.BLEND_CONTRIB
+    _capi.check(_capi.lib().fgs_blend_tiles(
+        sp.data_ptr() if sp.numel() else None, gd.data_ptr() if extras else None,
+        vals.data_ptr() if vals.numel() else None, st32.data_ptr(), int(width), int(height),
+        bg_c, float(tau), flags, 0, gh - 1, rgb.data_ptr(),
+        alpha.data_ptr() if extras else None, dmap.data_ptr() if extras else None,
+        contrib.data_ptr(), stats.data_ptr(), _stream_ptr(torch, dev)))
+    nonempty = int(np.count_nonzero(np.diff(st_np) > 0))
+    out = (rgb.cpu().numpy(), contrib[:vals_np.shape[0]].cpu().numpy(), nonempty)
+    if extras:
+        out = out + (alpha.cpu().numpy(), dmap.cpu().numpy())
+    return out

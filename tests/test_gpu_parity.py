@@ -1,0 +1,311 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the CPU oracle on
+the same inputs, and against the reference's own golden vectors.
+
+Bars (BASELINE.json north_star): pair lists and sorted key order BIT-EXACT;
+pixels max-abs <= 1e-3 and PSNR >= 60 dB in the default (ex2.approx) mode,
+and bit-identical in exact mode.
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_2408_07967_b200 as fgs
+from oracle import oracle as orc
+from fgs_testlib import identity_camera, make_raw_scene
+
+pytestmark = pytest.mark.gpu
+
+STRATS = ("precise", "tight-aabb", "baseline-circle-aabb")
+PIX_TOL = 1e-3          # north_star: max-abs 1e-3
+PSNR_MIN = 60.0         # north_star: PSNR >= 60 dB
+
+
+def _sorted_pairs(b, count):
+    order = np.lexsort((b.values, b.keys))
+    return b.keys[order], b.values[order]
+
+
+def _psnr_ok(a, b):
+    p = fgs.psnr(a, b)
+    return p == "identical" or p >= PSNR_MIN
+
+
+# ---------------------------------------------------------------------------
+# against the reference's golden vectors
+# ---------------------------------------------------------------------------
+def test_golden_cutoffs(golden):
+    k, _ = fgs.power_cutoffs(golden.act.opacities, golden.tau)
+    assert np.array_equal(k.view(np.uint32), golden.z["k"].view(np.uint32))
+
+
+def test_golden_every_stage(golden):
+    g = golden
+    pipe = fgs.Pipeline(g.act, sh_degree=g.sh_degree)
+    for ci in range(g.ncam):
+        cam = g.camera(ci)
+        for s in STRATS:
+            b = fgs.preprocess_and_bin(pipe, cam, s, g.tau, sh_degree=g.sh_degree)
+            assert b.emitted_count == int(g.z[f"c{ci}_{s}_pairs"]), (ci, s)
+            if not g.has(ci, "keys", s):
+                continue
+            ret = g.retained(ci, s)
+            assert np.array_equal(b.retained, ret)
+            assert np.array_equal(b.depth.view(np.uint32), g.get(ci, "depth", s).view(np.uint32))
+            assert np.array_equal(b.tile_rects[ret], g.get(ci, "rects", s).astype(np.int32)[ret])
+            # splat rows bit-exact (geometry AND SH colours)
+            sha = np.frombuffer(hashlib.sha256(b.splat.tobytes()).digest(), np.uint8)
+            assert np.array_equal(sha, g.get(ci, "splat_sha", s))
+            keys, vals = fgs.sort_pairs(b.keys, b.values, 1, b.grid_w * b.grid_h,
+                                        max(g.act.count, 1))
+            assert np.array_equal(keys, g.get(ci, "keys", s))
+            assert np.array_equal(vals, g.get(ci, "values", s))
+            starts = fgs.tile_range_table(keys, b.grid_w, b.grid_h)
+            assert np.array_equal(starts, g.get(ci, "starts", s).astype(np.int64))
+            img, contrib, nonempty = fgs.render_frame(b.splat, vals, starts, cam.width,
+                                                      cam.height, g.bg, g.tau, exact=True)
+            sha = np.frombuffer(hashlib.sha256(img.tobytes()).digest(), np.uint8)
+            assert np.array_equal(sha, g.get(ci, "image_sha", s)), "exact-mode frame not bit-identical"
+            assert np.array_equal(contrib, g.contrib(ci, s))
+            st = g.get(ci, "stats", s)
+            assert (b.emitted_count, int(contrib.sum()), b.gaussians_retained,
+                    b.gaussians_degenerate, nonempty) == tuple(int(v) for v in st)
+
+
+def test_golden_pipeline_render(golden):
+    g = golden
+    pipe = fgs.Pipeline(g.act, sh_degree=g.sh_degree)
+    for ci in range(g.ncam):
+        cam = g.camera(ci)
+        ref = g.get(ci, "image")
+        want = tuple(int(v) for v in g.get(ci, "stats"))
+        fb, st = pipe.render(cam, "precise", g.tau, g.bg)
+        assert fb.image.shape == ref.shape and fb.image.dtype == np.float32
+        assert fgs.max_abs_diff(fb.image, ref) <= PIX_TOL
+        assert _psnr_ok(fb.image, ref)
+        assert (st.pairs_emitted, st.gaussians_retained, st.gaussians_degenerate,
+                st.tiles_nonempty) == (want[0], want[2], want[3], want[4])
+        assert abs(st.pairs_contributing - want[1]) <= max(2, want[1] // 10000)
+        assert st.pair_buffer_bytes == 12 * want[0]
+        fbx, stx = pipe.render(cam, "precise", g.tau, g.bg, exact=True)
+        assert np.array_equal(fbx.image.view(np.uint32), ref.view(np.uint32))
+        assert stx.pairs_contributing == want[1]
+
+
+def test_c1_survey_fingerprints(golden_c1):
+    g = golden_c1
+    fb, st = fgs.Pipeline(g.act).render(g.camera(0), exact=True)
+    assert (st.gaussians_retained, st.pairs_emitted, st.pairs_contributing,
+            st.tiles_nonempty, st.candidate_tiles) == (10000, 47264, 34034, 236, 52466)
+    assert hashlib.sha256(fb.image.tobytes()).hexdigest()[:16] == "57807ea6520ab90c"
+    b = fgs.preprocess_and_bin(g.act, g.camera(0))
+    assert hashlib.sha256(np.sort(b.keys).tobytes()).hexdigest()[:16] == "985b4149ce95e8e8"
+
+
+# ---------------------------------------------------------------------------
+# against the oracle on fresh seeded inputs
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("preset,n,seed,w,h,radius,tau,deg,bg", [
+    ("mixed", 20000, 2, 640, 360, 24.0, 1 / 255, 3, (0, 0, 0)),
+    ("elongated", 30000, 4, 512, 288, 12.0, 1 / 255, 3, (0.1, 0.2, 0.3)),
+    ("isotropic", 5000, 6, 200, 120, 14.0, 0.01, 1, (1, 1, 1)),
+    ("mixed", 6000, 8, 70, 42, 6.0, 1 / 255, 0, (0, 0, 0)),          # ragged edge tiles
+    ("mixed", 3000, 10, 1000, 40, 10.0, 0.02, 2, (0, 0, 0)),         # wide strip
+])
+def test_oracle_parity_all_stages(preset, n, seed, w, h, radius, tau, deg, bg):
+    act = fgs.activate(fgs.gen_synthetic(preset, n, seed))
+    pipe = fgs.Pipeline(act, sh_degree=deg)
+    for cam in fgs.orbit_cameras(2, radius, w, h):
+        for s in STRATS:
+            ob = orc.preprocess_and_bin(act, cam, s, tau, deg)
+            gb = fgs.preprocess_and_bin(pipe, cam, s, tau, sh_degree=deg)
+            assert np.array_equal(gb.retained, ob.retained)
+            assert np.array_equal(gb.depth.view(np.uint32), ob.depth.view(np.uint32))
+            assert np.array_equal(gb.splat.view(np.uint32), ob.splat.view(np.uint32))
+            assert np.array_equal(gb.tile_rects[ob.retained], ob.tile_rects[ob.retained])
+            assert np.array_equal(gb.pair_counts, ob.pair_counts)
+            # emission order: ascending Gaussian index
+            assert np.all(np.diff(gb.values.astype(np.int64)) >= 0)
+            ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, max(n, 1))
+            gk, gv = _sorted_pairs(gb, n)
+            assert np.array_equal(gk, ok) and np.array_equal(gv, ov)
+        # whole frame (precise)
+        oimg, ost, oalpha, odepth = orc.render(act, cam, "precise", tau, bg, deg, extras=True)
+        fb, st = pipe.render(cam, "precise", tau, bg, extras=True)
+        assert fgs.max_abs_diff(fb.image, oimg) <= PIX_TOL and _psnr_ok(fb.image, oimg)
+        assert np.abs(fb.alpha - oalpha).max() <= PIX_TOL
+        assert np.abs(fb.depth - odepth).max() <= PIX_TOL * max(1.0, float(odepth.max()))
+        assert st.pairs_emitted == ost["pairs_emitted"]
+        assert st.tiles_nonempty == ost["tiles_nonempty"]
+        fbx, stx = pipe.render(cam, "precise", tau, bg, exact=True, extras=True)
+        assert np.array_equal(fbx.image.view(np.uint32), oimg.view(np.uint32))
+        assert np.array_equal(fbx.alpha.view(np.uint32), oalpha.view(np.uint32))
+        assert np.array_equal(fbx.depth.view(np.uint32), odepth.view(np.uint32))
+        assert stx.pairs_contributing == ost["pairs_contributing"]
+
+
+def test_sorted_buffer_matches_oracle_order():
+    """The frame path's stable sort on key bits alone must reproduce the
+    reference's (key, value) order."""
+    import ctypes as C
+    import torch
+    from paper_2408_07967_b200 import _capi
+    act = fgs.activate(fgs.gen_synthetic("mixed", 50000, 12))
+    cam = fgs.orbit_cameras(1, 20.0, 800, 448)[0]
+    pipe = fgs.Pipeline(act)
+    ob = orc.preprocess_and_bin(act, cam)
+    ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, act.count)
+    ostarts = orc.tile_range_table(ok, ob.grid_w, ob.grid_h)
+    fb, st = pipe.render(cam)
+    ws = pipe._free[(800, 448)][0]
+    lay, M = ws.lay, st.pairs_emitted
+    assert M == ok.shape[0]
+    si = int(lay.sorted_in)
+    keys = ws.view(torch, lay.off_keys[si], M * 8, torch.int64).cpu().numpy().view(np.uint64)
+    vals = ws.view(torch, lay.off_vals[si], M * 4, torch.int32).cpu().numpy().view(np.uint32)
+    starts = ws.view(torch, lay.off_starts, (lay.tiles + 1) * 4, torch.int32).cpu().numpy()
+    assert np.array_equal(keys, ok)
+    assert np.array_equal(vals, ov)
+    assert np.array_equal(starts.astype(np.int64), ostarts)
+
+
+# ---------------------------------------------------------------------------
+# stage-level behaviour mirrored from the reference's own tests
+# ---------------------------------------------------------------------------
+def test_sort_pairs_vs_lexsort_and_ties():
+    # test_sorting.py:38-60: arbitrary order in, (key, value) order out
+    rng = np.random.default_rng(0)
+    n = 100_000
+    keys = (rng.integers(0, 300, n).astype(np.uint64) << np.uint64(32)) \
+        | rng.integers(0, 1 << 32, n).astype(np.uint64)
+    keys[::7] = keys[0]                                   # heavy ties
+    vals = rng.integers(0, 70000, n).astype(np.uint32)
+    k, v = fgs.sort_pairs(keys, vals, 1, 300, 70000)
+    order = np.lexsort((vals, keys))
+    assert np.array_equal(k, keys[order]) and np.array_equal(v, vals[order])
+    k2, v2 = fgs.sort_pairs(keys, vals)                   # no bounds: all bytes
+    assert np.array_equal(k2, k) and np.array_equal(v2, v)
+    ko, vo = orc.sort_pairs(keys, vals, 300, 70000)
+    assert np.array_equal(k, ko) and np.array_equal(v, vo)
+
+
+@pytest.mark.parametrize("n", [0, 1, 31, 4095, 4096, 4097, 12289, 1_000_003])
+def test_sort_pairs_sizes(n):
+    rng = np.random.default_rng(n)
+    keys = (rng.integers(0, 8160, n).astype(np.uint64) << np.uint64(32)) \
+        | rng.integers(0, 1 << 31, n).astype(np.uint64)
+    vals = rng.integers(0, 1 << 20, n).astype(np.uint32)
+    k, v = fgs.sort_pairs(keys, vals, 1, 8160, 1 << 20)
+    order = np.lexsort((vals, keys))
+    assert np.array_equal(k, keys[order]) and np.array_equal(v, vals[order])
+
+
+def test_sort_pairs_errors():
+    with pytest.raises(ValueError):
+        fgs.sort_pairs(np.zeros(3, np.uint64), np.zeros(2, np.uint32))
+
+
+def test_tile_range_table_examples():
+    # test_sorting.py:94-109
+    keys = np.array([0, 0, 3], np.uint64) << np.uint64(32)
+    assert fgs.tile_range_table(keys, 2, 2).tolist() == [0, 2, 2, 2, 3]
+    assert fgs.tile_range_table(np.zeros(0, np.uint64), 2, 2).tolist() == [0, 0, 0, 0, 0]
+    with pytest.raises(fgs.UnsortedPairsError):
+        fgs.tile_range_table(keys[::-1].copy(), 2, 2)
+    with pytest.raises(ValueError):
+        fgs.tile_range_table(np.array([9], np.uint64) << np.uint64(32), 2, 2)
+
+
+def test_binning_known_answers():
+    # test_binning.py:23-77: single tile; 16/4/4; rotated 16/9/7
+    import math
+    cam = identity_camera(64, 64, focal=32)
+    z = 16.0
+    ndc = (2 * 24 + 1) / 64 - 1
+    scene = make_raw_scene([[ndc * z, ndc * z, z]], [0.4, 0.4, 0.4], [0.9])
+    for s in STRATS:
+        out = fgs.preprocess_and_bin(scene, cam, s)
+        assert out.emitted_count == 1
+        assert int(out.keys[0] >> np.uint64(32)) == 5
+        assert np.uint32(out.keys[0] & np.uint64(0xffffffff)) == np.float32(16.0).view(np.uint32)
+        assert out.values[0] == 0
+    z = 32.0
+    scene = make_raw_scene([[((2 * 32 + 1) / 64 - 1) * z, ((2 * 24 + 1) / 64 - 1) * z, z]],
+                           [10.0, 1.0, 0.01], [0.6])
+    c = {s: fgs.preprocess_and_bin(scene, cam, s).emitted_count for s in STRATS}
+    assert (c["baseline-circle-aabb"], c["tight-aabb"], c["precise"]) == (16, 4, 4)
+    q = [math.cos(math.pi / 8), 0.0, 0.0, math.sin(math.pi / 8)]
+    scene = make_raw_scene([[((2 * 40 + 1) / 64 - 1) * z, ((2 * 40 + 1) / 64 - 1) * z, z]],
+                           [10.0, 0.6, 0.01], [0.6], quats=[q])
+    c = {s: fgs.preprocess_and_bin(scene, cam, s).emitted_count for s in STRATS}
+    assert (c["baseline-circle-aabb"], c["tight-aabb"], c["precise"]) == (16, 9, 7)
+
+
+def test_empty_scene_is_background():
+    # test_binning.py:16-21, test_render.py:161-166
+    cam = identity_camera(48, 32)
+    fb, st = fgs.Pipeline(fgs.gen_synthetic("mixed", 0, 1)).render(cam, background=(0.25, 0.5, 0.75))
+    assert st.pairs_emitted == 0 and st.gaussians_retained == 0 and st.tiles_nonempty == 0
+    assert np.array_equal(fb.image, np.broadcast_to(np.float32([0.25, 0.5, 0.75]), (32, 48, 3)))
+
+
+def test_forced_regrow_never_truncates():
+    # test_binning.py:166-175
+    act = fgs.activate(fgs.gen_synthetic("mixed", 5000, 21))
+    cam = fgs.orbit_cameras(1, 24.0, 256, 256)[0]
+    pipe = fgs.Pipeline(act)
+    fb0, st0 = pipe.render(cam, exact=True)
+    fb1, st1 = fgs.Pipeline(act).render(cam, exact=True, initial_capacity=10)
+    assert st1.buffer_regrows >= 1 and st0.buffer_regrows == 0
+    assert st1.pairs_emitted == st0.pairs_emitted
+    assert np.array_equal(fb0.image, fb1.image)
+    b = fgs.preprocess_and_bin(act, cam, initial_capacity=7)
+    assert b.buffer_regrows >= 1 and b.emitted_count == st0.pairs_emitted
+
+
+def test_argument_errors():
+    act = fgs.activate(fgs.gen_synthetic("mixed", 10, 1))
+    cam = identity_camera()
+    with pytest.raises(ValueError):
+        fgs.Pipeline(act).render(cam, strategy="nope")
+    with pytest.raises(ValueError):
+        fgs.Pipeline(act, sh_degree=4).render(cam)
+    with pytest.raises(TypeError):
+        fgs.Pipeline(object())
+
+
+def test_repeatable_and_thread_safe():
+    # test_pipeline.py:28-35; SURVEY 8(b) threading row
+    import threading
+    act = fgs.activate(fgs.gen_synthetic("mixed", 20000, 5))
+    cams = fgs.orbit_cameras(4, 24.0, 320, 240)
+    pipe = fgs.Pipeline(act)
+    want = [pipe.render(c)[0].image.copy() for c in cams]
+    got = [None] * 16
+
+    def job(i):
+        got[i] = pipe.render(cams[i % 4])[0].image.copy()
+    th = [threading.Thread(target=job, args=(i,)) for i in range(16)]
+    [t.start() for t in th]
+    [t.join() for t in th]
+    for i in range(16):
+        assert np.array_equal(got[i], want[i % 4])
+
+
+def test_row_bands_equal_full_frame():
+    """the union of band renders is bit-identical to the full frame."""
+    act = fgs.activate(fgs.gen_synthetic("mixed", 20000, 7))
+    cam = fgs.orbit_cameras(1, 20.0, 512, 400)[0]
+    pipe = fgs.Pipeline(act)
+    full, st = pipe.render(cam)
+    gh = -(-400 // 16)
+    out = np.zeros_like(full.image)
+    total = 0
+    for b0, b1 in ((0, 7), (8, 15), (16, gh - 1)):
+        fb, s = pipe.render(cam, band=(b0, b1))
+        y0, y1 = b0 * 16, min((b1 + 1) * 16, 400)
+        out[y0:y1] = fb.image[y0:y1]
+        total += s.pairs_emitted
+    assert np.array_equal(out, full.image)
+    assert total == st.pairs_emitted
