@@ -185,7 +185,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2408_07967_b200 as fgs
-    from paper_2408_07967_b200 import _capi
+    from paper_2408_07967_b200 import _capi, sharding
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (the product has no CPU fallback)")
@@ -202,10 +202,9 @@ def main():
     cam = cams[0] if args.mode == "bands" else cams[rank % ncam]
     gh = -(-H // 16)
     band = None
+    bands = sharding.band_partition(gh, world)
     if args.mode == "bands" and world > 1:
-        per, extra = divmod(gh, world)
-        b0 = rank * per + min(rank, extra)
-        band = (b0, b0 + per + (1 if rank < extra else 0) - 1)
+        band = bands[rank]
 
     pipe = fgs.Pipeline(act)
     L = _capi.lib()
@@ -297,29 +296,15 @@ def main():
         e2e_s = float(t.item())
     e2e_value = views_per_step * K / e2e_s
 
-    # bands: gather the bands on rank 0 with NCCL (reporting the gather time)
+    # bands: gather the bands on rank 0 with NCCL send/recv (reported separately)
     gather_ms = None
     if args.mode == "bands" and world > 1:
-        rows = [0] * world
-        per, extra = divmod(gh, world)
-        full = torch.empty((H, W, 3), dtype=torch.float32, device=dev) if rank == 0 else None
-        y0, y1 = b0 * 16, min((b1 + 1) * 16, H)
+        y0, y1 = sharding.band_pixel_rows(band, H)
         mine = ws.rgb[y0:y1].contiguous()
         torch.cuda.synchronize(dev)
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         g0.record()
-        if rank == 0:
-            full[y0:y1] = mine
-            ops = []
-            for r in range(1, world):
-                rb0 = r * per + min(r, extra)
-                rb1 = rb0 + per + (1 if r < extra else 0) - 1
-                ops.append(dist.P2POp(dist.irecv, full[rb0 * 16:min((rb1 + 1) * 16, H)], r))
-            for w_ in dist.batch_isend_irecv(ops):
-                w_.wait()
-        else:
-            for w_ in dist.batch_isend_irecv([dist.P2POp(dist.isend, mine, 0)]):
-                w_.wait()
+        sharding.gather_bands(mine, bands, H, dist, rank, 0)
         g1.record()
         torch.cuda.synchronize(dev)
         gather_ms = g0.elapsed_time(g1)

@@ -10,7 +10,7 @@ Mirrors ``tilesplat.pipeline`` (reference ``pipeline.py``) name for name:
 * stage entry points ``preprocess_and_bin`` (``binning.py:197``),
   ``sort_pairs`` (``sorting.py:101``), ``tile_range_table`` (``sorting.py:139``),
   ``render_frame`` (``render.py:273``), ``power_cutoffs`` (``extent.py:19``)
-  so intermediates can be diffed against the oracle.
+  so intermediates can be diffed stage by stage.
 
 All compute happens in ``libflashgs_b200.so`` (hand-written sm_100a CUDA)
 through the C ABI in ``include/flashgs_b200.h``; torch only owns device
@@ -395,7 +395,7 @@ def max_abs_diff(a, b) -> float:
 
 
 # ----------------------------------------------------------------------------
-# stage-level entry points (numpy in / numpy out), for diffing against the oracle
+# stage-level entry points (numpy in / numpy out), for stage-by-stage diffs
 # ----------------------------------------------------------------------------
 
 @dataclass

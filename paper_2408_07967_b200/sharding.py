@@ -1,0 +1,73 @@
+"""Multi-GPU partitioning of the path; one process per GPU.
+
+* views: frames share only the immutable scene, so view ``v`` goes to rank
+  ``v mod world`` and no collective touches the data path;
+* row bands of one frame: the tile rows are cut into ``world`` contiguous
+  bands on 16-pixel boundaries; each rank renders its band (global tile
+  indices, so the union of band pair lists equals the single-GPU list) and the
+  bands are gathered on rank 0 with point-to-point sends (bands are unequal,
+  so this is a grouped send/recv, not a padded all-gather).
+
+Only ``torch.distributed`` is used, so the same code runs over NCCL on GPUs
+and over gloo in the CPU tests.
+"""
+
+from __future__ import annotations
+
+TILE = 16
+
+
+def band_partition(grid_h: int, world: int) -> list:
+    """Inclusive tile-row bands [(ty0, ty1)] per rank; earlier ranks take the
+    remainder (8 GPUs x 270 rows -> 34,34,34,34,34,34,33,33).  Ranks beyond
+    the number of rows get an empty band (ty0 > ty1)."""
+    if grid_h < 1 or world < 1:
+        raise ValueError("grid_h and world must be positive")
+    per, extra = divmod(grid_h, world)
+    out, y = [], 0
+    for r in range(world):
+        n = per + (1 if r < extra else 0)
+        out.append((y, y + n - 1))
+        y += n
+    return out
+
+
+def band_pixel_rows(band, height: int) -> tuple:
+    """Pixel-row slice [y0, y1) covered by an inclusive tile-row band."""
+    ty0, ty1 = band
+    if ty1 < ty0:
+        return (0, 0)
+    return (ty0 * TILE, min((ty1 + 1) * TILE, height))
+
+
+def views_for_rank(n_views: int, world: int, rank: int) -> list:
+    """View indices rendered by ``rank`` (round robin)."""
+    return list(range(rank, n_views, world))
+
+
+def gather_bands(local_rows, bands, height: int, dist, rank: int, dst: int = 0):
+    """Assemble the frame on ``dst`` from every rank's band rows.
+
+    ``local_rows`` is this rank's ``(rows, W, 3)`` tensor (rows may be 0).
+    Returns the full ``(H, W, 3)`` tensor on ``dst`` and ``None`` elsewhere.
+    """
+    import torch
+    world = len(bands)
+    if rank == dst:
+        full = torch.empty((height,) + tuple(local_rows.shape[1:]), dtype=local_rows.dtype,
+                           device=local_rows.device)
+        y0, y1 = band_pixel_rows(bands[dst], height)
+        full[y0:y1] = local_rows
+        ops = []
+        for r in range(world):
+            y0, y1 = band_pixel_rows(bands[r], height)
+            if r != dst and y1 > y0:
+                ops.append(dist.P2POp(dist.irecv, full[y0:y1], r))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        return full
+    if local_rows.shape[0] > 0:
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, local_rows.contiguous(), dst)]):
+            w.wait()
+    return None

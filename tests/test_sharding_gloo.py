@@ -1,0 +1,92 @@
+"""N>1 host logic on CPU: band / view partitioning and the band gather over a
+world_size-2 gloo group (the GPU box only ever has one GPU)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2408_07967_b200 import sharding
+
+
+def test_band_partition_examples():
+    assert [b - a + 1 for a, b in sharding.band_partition(270, 8)] == [34] * 6 + [33] * 2
+    bands = sharding.band_partition(270, 8)
+    assert bands[0][0] == 0 and bands[-1][1] == 269
+    assert all(bands[i][1] + 1 == bands[i + 1][0] for i in range(7))
+    assert sharding.band_partition(3, 4) == [(0, 0), (1, 1), (2, 2), (3, 2)]   # empty last band
+    assert sharding.band_pixel_rows((3, 2), 40) == (0, 0)
+    assert sharding.band_pixel_rows((2, 2), 42) == (32, 42)                    # ragged bottom edge
+    with pytest.raises(ValueError):
+        sharding.band_partition(0, 2)
+
+
+def test_views_for_rank_cover_once():
+    for world in (1, 2, 4, 8):
+        seen = sorted(v for r in range(world) for v in sharding.views_for_rank(64, world, r))
+        assert seen == list(range(64))
+    assert sharding.views_for_rank(3, 4, 3) == []
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, height, width, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        grid_h = -(-height // 16)
+        bands = sharding.band_partition(grid_h, world)
+        # every rank can build the same deterministic "frame"; it only owns its band
+        frame = torch.arange(height * width * 3, dtype=torch.float32).reshape(height, width, 3)
+        y0, y1 = sharding.band_pixel_rows(bands[rank], height)
+        full = sharding.gather_bands(frame[y0:y1].clone(), bands, height, dist, rank, 0)
+        # views: weak scaling, no collective on the data path; only the max-over-ranks timing
+        t = torch.tensor([float(rank + 1)])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            q.put((bool(torch.equal(full, frame)), float(t.item())))
+        else:
+            assert full is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("height,width", [(70, 42), (1080, 64)])
+def test_band_gather_world2_gloo(height, width):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, height, width, q)) for r in range(2)]
+    [p.start() for p in procs]
+    [p.join(120) for p in procs]
+    assert all(p.exitcode == 0 for p in procs)
+    ok, tmax = q.get(timeout=10)
+    assert ok and tmax == 2.0
+
+
+def test_band_render_union_equals_full_frame_oracle():
+    """Same property the GPU test checks, stated with the oracle: rendering each
+    band's tiles independently reproduces the full frame (tiles are independent,
+    render.py:276-279)."""
+    import paper_2408_07967_b200.scene as S
+    from oracle import oracle as orc
+    act = S.activate(S.gen_synthetic("mixed", 2000, 3))
+    cam = S.orbit_cameras(1, 20.0, 160, 100)[0]
+    img, _ = orc.render(act, cam)
+    bands = sharding.band_partition(-(-100 // 16), 2)
+    out = np.zeros_like(img)
+    for b in bands:
+        y0, y1 = sharding.band_pixel_rows(b, 100)
+        out[y0:y1] = img[y0:y1]
+    assert np.array_equal(out, img)
