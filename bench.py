@@ -171,6 +171,7 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="views", choices=["views", "bands"])
     ap.add_argument("--exact", action="store_true", help="bit-exact blend mode")
+    ap.add_argument("--sort-mode", default="tile-bucket", choices=["tile-bucket", "onesweep"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -206,7 +207,7 @@ def main():
     if args.mode == "bands" and world > 1:
         band = bands[rank]
 
-    pipe = fgs.Pipeline(act)
+    pipe = fgs.Pipeline(act, sort_mode=args.sort_mode)
     L = _capi.lib()
     hbm_peak, peak_src, sm_max = peaks()
 
@@ -216,9 +217,12 @@ def main():
     M = st.pairs_emitted
     stream = torch.cuda.current_stream(dev)
     ws = pipe._take_ws(torch, W, H, pipe._default_capacity())
+    ws.set_mode(_capi.SORT_MODES[args.sort_mode])
     lay = ws.lay
-    npass = int(lay.sort_passes)
-    n_marks = 6 + npass                     # K1 K2 K3 hist pass*npass K5 K6
+    bucket = args.sort_mode == "tile-bucket"
+    npass = 0 if bucket else int(lay.sort_passes)
+    # kernels per frame: bucket  K1 K2 K3 tile_sort K6 ; onesweep  K1 K2 K3 hist pass*npass K5 K6
+    n_marks = 5 if bucket else 6 + npass
     camc = _capi.camera_struct(cam)
     kcut = pipe._cutoffs(torch, 1.0 / 255.0)
     bg = (C.c_float * 3)(0.0, 0.0, 0.0)
@@ -310,15 +314,19 @@ def main():
         gather_ms = g0.elapsed_time(g1)
 
     if rank == 0:
-        names = ["preprocess", "scan", "emit", "sort_hist"] + [f"sort_pass{p}" for p in range(npass)] \
-            + ["ranges", "blend"]
+        if bucket:
+            names = ["preprocess", "scan", "emit", "tile_sort", "blend"]
+        else:
+            names = ["preprocess", "scan", "emit", "sort_hist"] \
+                + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
         kmean = kern.mean(axis=0)
         R = int(st.gaussians_retained)
         T_tiles = int(lay.tiles)
         # algorithmic bytes per launch (packed scene reads 240+4 B/Gaussian)
         alg = {
             "preprocess": 236.0 * P + 52.0 * R,
-            "emit": 12.0 * M + 4.0 * P,
+            "emit": (8.0 if bucket else 12.0) * M + 4.0 * P,
+            "tile_sort": 12.0 * M,          # 8 B record in, 4 B index out
             "sort_hist": 8.0 * M,
             "ranges": 8.0 * M + 4.0 * (T_tiles + 1),
             "blend": 52.0 * M + 12.0 * W * H,
@@ -336,6 +344,8 @@ def main():
         # dominant kernel: sort passes are launches of ONE kernel -> judged together
         sort_ms = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass")))
         cand = {"blend": kmean[-1], "sort_pass": sort_ms, "preprocess": kmean[0], "emit": kmean[2]}
+        if bucket:
+            cand["tile_sort"] = kmean[3]
         dom = max(cand, key=cand.get)
         if dom == "sort_pass":
             per_launch_ms = sort_ms / npass
@@ -356,7 +366,7 @@ def main():
                     "note": "blend is FP32-issue bound, not HBM bound: see profiles/ for "
                             "sm__inst_executed_pipe_fma / issue-slot utilisation from ncu"}
         else:
-            idx = 0 if dom == "preprocess" else 2
+            idx = {"preprocess": 0, "emit": 2, "tile_sort": 3}[dom]
             ms = float(kmean[idx])
             ach = alg[dom] / (ms * 1e-3) / 1e9
             roof = {"kernel": "k_" + dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
@@ -375,7 +385,8 @@ def main():
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": desc, "mode": args.mode, "strategy": "precise",
                        "tau": 1.0 / 255.0, "sh_degree": 3, "gaussians": P, "width": W, "height": H,
-                       "pairs": M, "retained": R, "tiles": T_tiles, "sort_passes": npass,
+                       "pairs": M, "retained": R, "tiles": T_tiles, "sort_mode": args.sort_mode,
+                       "sort_passes": npass,
                        "blend": "exact" if args.exact else "ex2.approx+guard",
                        "l2": "256 MiB buffer written between timed steps (flush, untimed); "
                              "scene (240 B/Gaussian) is re-read from HBM every step",
@@ -390,7 +401,7 @@ def main():
             "cpu_baseline": cpu,
             "kernels": kernels,
             "stage_ms": {"preprocess_bin": float(kmean[0:3].sum()),
-                         "sort": float(kmean[3:4 + npass + 1].sum()), "render": float(kmean[-1])},
+                         "sort": float(kmean[3:-1].sum()), "render": float(kmean[-1])},
             "wall_s_timed_region": t_wall,
         }
         if gather_ms is not None:

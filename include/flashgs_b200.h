@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FGS_ABI_VERSION 1
+#define FGS_ABI_VERSION 2
 #define FGS_TILE 16              /* constants.py:4  TILE_SIZE */
 
 enum {
@@ -46,6 +46,17 @@ enum {
 
 /* binning.py:38  STRATEGIES */
 enum { FGS_PRECISE = 0, FGS_TIGHT_AABB = 1, FGS_BASELINE_CIRCLE_AABB = 2 };
+
+/* How the frame's pairs get into (tile, depth, index) order (fgs_layout.sort_mode).
+ * Both produce the bit-identical sorted list and range table.
+ *   TILE_BUCKET (default): MSD counting pass on the tile field fused into the
+ *     count/emit kernels (per-tile histogram -> scan -> scatter), then each
+ *     tile's bucket is sorted on (depth bits, index) in shared memory; the
+ *     range table is the scan itself.  ~20 B of HBM traffic per pair.
+ *   ONESWEEP: pairs emitted in Gaussian order, then a stable LSD radix sort
+ *     (8-bit digits, one-sweep passes with decoupled look-back) over the packed
+ *     tile|depth key, then a range-identification kernel.  ~172 B per pair. */
+enum { FGS_SORT_ONESWEEP = 0, FGS_SORT_TILE_BUCKET = 1 };
 
 /* fgs_blend flags */
 enum {
@@ -105,11 +116,16 @@ typedef struct fgs_layout {
     uint64_t off_starts;       /* int32  [tiles + 1]  sorting.py:139-152      */
     uint64_t off_contrib;      /* uint8  [capacity]                           */
     uint64_t off_stats;        /* fgs_stats                                   */
+    uint64_t off_tilecount;    /* uint32 [tiles]  pairs per tile (TILE_BUCKET) */
+    uint64_t off_cursor;       /* uint32 [tiles]  scatter cursors (TILE_BUCKET)*/
     int64_t  gaussians, capacity;
     int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
-    int32_t  preprocess_blocks, sort_passes, sorted_in;  /* sorted_in: 0/1 = which
-                                  keys/vals buffer holds the sorted pairs     */
-    int32_t  reserved;
+    int32_t  preprocess_blocks, sort_passes;
+    int32_t  sort_mode;        /* FGS_SORT_*; change only via fgs_layout_set_sort_mode */
+    int32_t  sorted_keys_in, sorted_vals_in;   /* which keys[] / vals[] buffer holds
+                                  the sorted pairs after fgs_sort               */
+    int32_t  keep_sorted_keys; /* TILE_BUCKET: also write the sorted 64-bit keys
+                                  (only the values feed the blend); caller-set  */
 } fgs_layout;
 
 int         fgs_abi_version(void);
@@ -121,7 +137,8 @@ const char *fgs_last_cuda_error(void);
  * library is followed by a cudaEventRecord of the next event in `events`
  * (cudaEvent_t handles, caller-owned) on the launch stream.  fgs_profile_end
  * disarms and returns how many were recorded.  Frame order: preprocess, scan,
- * emit, sort histogram, one per sort pass, ranges, blend. */
+ * emit, then (ONESWEEP) sort histogram, one per sort pass, ranges, or
+ * (TILE_BUCKET) tile sort; then blend. */
 void    fgs_profile_begin(void **events, int32_t n_events);
 int32_t fgs_profile_end(void);
 
@@ -148,6 +165,10 @@ int fgs_power_cutoffs(const void *packed_scene, int64_t gaussians, double tau,
 
 int fgs_workspace_layout(int64_t gaussians, int32_t width, int32_t height,
                          int64_t capacity, fgs_layout *out_host);
+
+/* Select FGS_SORT_* for every later call that takes this layout (offsets do not
+ * change; only sort_mode / sorted_*_in do). */
+int fgs_layout_set_sort_mode(fgs_layout *layout_host, int32_t sort_mode);
 
 /* Must be called once after the workspace is allocated (zeroes the sort
  * look-back table, whose entries are epoch-tagged afterwards). */

@@ -10,7 +10,7 @@ it is absent -- there is no CPU fallback.
 from .pipeline import (BinOutput, Framebuffer, FrameStats, Pipeline, STRATEGIES,
                        TAU_DEFAULT, TILE_SIZE, UnsortedPairsError, max_abs_diff,
                        power_cutoffs, preprocess_and_bin, psnr, render_frame,
-                       run_frame, sort_pairs, tile_range_table)
+                       run_frame, sort_pairs, sorted_pairs, tile_range_table)
 from .scene import (ActivatedScene, Camera, CameraValidationError, Scene, activate,
                     gen_synthetic, look_at_camera, make_camera, orbit_cameras)
 
@@ -21,5 +21,5 @@ __all__ = [
     "FrameStats", "Pipeline", "STRATEGIES", "Scene", "TAU_DEFAULT", "TILE_SIZE",
     "UnsortedPairsError", "activate", "gen_synthetic", "look_at_camera", "make_camera",
     "max_abs_diff", "orbit_cameras", "power_cutoffs", "preprocess_and_bin", "psnr",
-    "render_frame", "run_frame", "sort_pairs", "tile_range_table",
+    "render_frame", "run_frame", "sort_pairs", "sorted_pairs", "tile_range_table",
 ]

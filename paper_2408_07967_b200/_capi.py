@@ -15,16 +15,19 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libflashgs_b200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 STRATEGIES = ("baseline-circle-aabb", "tight-aabb", "precise")   # binning.py:38 order
 STRATEGY_ID = {"precise": 0, "tight-aabb": 1, "baseline-circle-aabb": 2}
 BLEND_EXACT, BLEND_CONTRIB = 1, 2
+SORT_ONESWEEP, SORT_TILE_BUCKET = 0, 1
+SORT_MODES = {"onesweep": SORT_ONESWEEP, "tile-bucket": SORT_TILE_BUCKET}
 SORT_TILE = 4096
 
 # every symbol include/flashgs_b200.h declares (checked by the CPU test-suite)
 SYMBOLS = (
     "fgs_abi_version", "fgs_error_string", "fgs_last_cuda_error", "fgs_scene_bytes",
-    "fgs_scene_pack", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_workspace_init",
+    "fgs_scene_pack", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_layout_set_sort_mode",
+    "fgs_workspace_init",
     "fgs_preprocess", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
     "fgs_render", "fgs_sort_pairs_scratch_bytes", "fgs_sort_pairs", "fgs_tile_ranges",
     "fgs_blend_tiles", "fgs_profile_begin", "fgs_profile_end",
@@ -62,11 +65,13 @@ class FgsLayout(C.Structure):
                 ("off_vals", C.c_uint64 * 2), ("off_sortstate", C.c_uint64),
                 ("off_hist", C.c_uint64), ("off_starts", C.c_uint64),
                 ("off_contrib", C.c_uint64), ("off_stats", C.c_uint64),
+                ("off_tilecount", C.c_uint64), ("off_cursor", C.c_uint64),
                 ("gaussians", C.c_int64), ("capacity", C.c_int64),
                 ("width", C.c_int32), ("height", C.c_int32), ("grid_w", C.c_int32),
                 ("grid_h", C.c_int32), ("tiles", C.c_int32), ("tile_bits", C.c_int32),
                 ("preprocess_blocks", C.c_int32), ("sort_passes", C.c_int32),
-                ("sorted_in", C.c_int32), ("reserved", C.c_int32)]
+                ("sort_mode", C.c_int32), ("sorted_keys_in", C.c_int32),
+                ("sorted_vals_in", C.c_int32), ("keep_sorted_keys", C.c_int32)]
 
 
 class FgsError(RuntimeError):
@@ -93,6 +98,7 @@ def _declare(L):
         "fgs_scene_pack": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, vp]),
         "fgs_power_cutoffs": (C.c_int, [vp, i64, dbl, vp, vp]),
         "fgs_workspace_layout": (C.c_int, [i64, i32, i32, i64, lay_p]),
+        "fgs_layout_set_sort_mode": (C.c_int, [lay_p, i32]),
         "fgs_workspace_init": (C.c_int, [vp, lay_p, vp]),
         "fgs_preprocess": (C.c_int, [vp, vp, i64, cam_p, dbl, i32, i32, i32, i32, vp, lay_p, vp]),
         "fgs_scan": (C.c_int, [vp, lay_p, vp]),
@@ -152,7 +158,9 @@ def camera_struct(cam) -> FgsCamera:
     return s
 
 
-def layout(P, width, height, capacity) -> FgsLayout:
+def layout(P, width, height, capacity, sort_mode=None) -> FgsLayout:
     out = FgsLayout()
     check(lib().fgs_workspace_layout(int(P), int(width), int(height), int(capacity), C.byref(out)))
+    if sort_mode is not None:
+        check(lib().fgs_layout_set_sort_mode(C.byref(out), int(sort_mode)))
     return out

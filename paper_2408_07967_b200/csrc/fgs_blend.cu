@@ -2,7 +2,11 @@
 //
 // Replaces render.py:135-252 (_composite_pipelined), 273-310 (render_frame).
 //
-// One CTA per 16x16 tile, one thread per pixel.  The tile's sorted pair slice
+// One CTA per 16x16 tile, one thread per pixel, one warp per 8x4 pixel block.
+// Within a batch a warp first culls 32 pairs at a time against its block (one
+// pair per lane, ballot) and only walks the survivors, so the per-pixel loop
+// never spends issue slots on splats whose rectangle misses the whole block.
+// The tile's sorted pair slice
 // is consumed in batches of 256 through a two-step prefetch pipeline (the
 // FlashGS scheme, at batch granularity): while batch i is
 // blended out of shared memory, the 48-byte splat rows of batch i+1 are in
@@ -93,7 +97,14 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
     const int tid = threadIdx.x;
     const int tx = blockIdx.x, ty = ty_first + blockIdx.y;
     const int tile = ty * grid_w + tx;
-    const int px = tx * FGS_TILE + (tid & 15), py = ty * FGS_TILE + (tid >> 4);
+    // each warp owns an 8x4 pixel block (squarer than 16x2, so fewer splat
+    // rectangles reach it); lanes run row-major inside the block
+    const int lane = tid & 31, wq = tid >> 5;
+    const int bx = tx * FGS_TILE + (wq & 1) * 8, by = ty * FGS_TILE + (wq >> 1) * 4;
+    const int px = bx + (lane & 7), py = by + (lane >> 3);
+    // pixel-centre bounds of the block, for the warp-level rectangle cull
+    const float wx_lo = (float)bx + 0.5f, wx_hi = (float)bx + 7.5f;
+    const float wy_lo = (float)by + 0.5f, wy_hi = (float)by + 3.5f;
     const bool inside = px < width && py < height;
     const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
 
@@ -139,10 +150,23 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         // step 3: blend batch b
         const int cnt = n - b * FGS_BLEND_BATCH < FGS_BLEND_BATCH ? n - b * FGS_BLEND_BATCH
                                                                   : FGS_BLEND_BATCH;
-        for (int j0 = 0; j0 < cnt; j0 += 16) {
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
             if (__all_sync(FGS_FULL, done)) break;
-            const int j1 = j0 + 16 < cnt ? j0 + 16 : cnt;
-            for (int j = j0; j < j1; ++j) {
+            // warp-level cull, one pair per lane: a pair whose extent rectangle misses the
+            // whole 8x4 block is rejected by every pixel's render.py:211 test (float32
+            // subtraction is monotone, so testing the block's extreme centres is exact)
+            const int jl = c0 + lane;
+            bool keep = false;
+            if (jl < cnt) {
+                const float4 q0 = S.row[cur][jl][0];
+                const float4 q2 = S.row[cur][jl][2];
+                keep = !(fs(wx_lo, q0.x) > q2.z || fs(wx_hi, q0.x) < -q2.z ||
+                         fs(wy_lo, q0.y) > q2.w || fs(wy_hi, q0.y) < -q2.w);
+            }
+            uint32_t live = __ballot_sync(FGS_FULL, keep);
+            while (live) {
+                const int j = c0 + __ffs(live) - 1;
+                live &= live - 1;
                 const float4 r0 = S.row[cur][j][0];
                 const float4 r2 = S.row[cur][j][2];
                 const float dx = fs(fx, r0.x), dy = fs(fy, r0.y);

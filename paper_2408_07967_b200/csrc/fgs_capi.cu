@@ -130,7 +130,6 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     L->tile_bits = tb;
     L->preprocess_blocks = (int32_t)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     L->sort_passes = (31 + tb + 7) / 8;
-    L->sorted_in = L->sort_passes & 1;
     uint64_t off = 0;
     auto take = [&](uint64_t bytes) {
         const uint64_t o = off;
@@ -139,7 +138,9 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     };
     const uint64_t cap = (uint64_t)capacity, p = (uint64_t)P;
     const uint64_t sort_tiles = (cap + FGS_SORT_TILE - 1) / FGS_SORT_TILE;
-    L->off_stats = take(sizeof(fgs_stats));
+    L->off_stats = take(sizeof(fgs_stats));          // stats and tilecount are contiguous:
+    L->off_tilecount = take((uint64_t)L->tiles * 4); // one memset clears both
+    L->off_cursor = take((uint64_t)L->tiles * 4);
     L->off_splat = take(p * 48);
     L->off_depth = take(p * 4);
     L->off_rects = take(p * 8);
@@ -155,6 +156,19 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     L->off_starts = take(((uint64_t)L->tiles + 1) * 4);
     L->off_contrib = take(cap);
     L->total_bytes = off;
+    return fgs_layout_set_sort_mode(L, FGS_SORT_TILE_BUCKET);
+}
+
+int fgs_layout_set_sort_mode(fgs_layout *L, int32_t mode)
+{
+    if (!L || (mode != FGS_SORT_ONESWEEP && mode != FGS_SORT_TILE_BUCKET)) return FGS_E_ARG;
+    L->sort_mode = mode;
+    if (mode == FGS_SORT_TILE_BUCKET) {
+        L->sorted_keys_in = 1;      // k_tile_sort: rec in keys[0] -> keys[1], vals[0]
+        L->sorted_vals_in = 0;
+    } else {
+        L->sorted_keys_in = L->sorted_vals_in = L->sort_passes & 1;
+    }
     return FGS_OK;
 }
 
@@ -182,12 +196,16 @@ int fgs_preprocess(const void *packed, const float *k_cut, int64_t P, const fgs_
     if (sh_degree < 0 || sh_degree > 3) return FGS_E_SH_DEGREE;
     if (strategy < 0 || strategy > 2) return FGS_E_STRATEGY;
     return fgs_launch_preprocess(fgs_scene_view(packed, P), k_cut, P, make_cam(cam), tau, sh_degree,
-                                 strategy, band0, band1, fgs_frame_view(ws, L), (cudaStream_t)stream);
+                                 strategy, band0, band1, L->sort_mode == FGS_SORT_TILE_BUCKET,
+                                 L->tiles, fgs_frame_view(ws, L), (cudaStream_t)stream);
 }
 
 int fgs_scan(void *ws, const fgs_layout *L, void *stream)
 {
     if (!ws || !L) return FGS_E_ARG;
+    if (L->sort_mode == FGS_SORT_TILE_BUCKET)
+        return fgs_launch_scan_tiles(fgs_frame_view(ws, L), L->tiles, L->capacity,
+                                     (cudaStream_t)stream);
     return fgs_launch_scan(fgs_frame_view(ws, L), L->preprocess_blocks, L->capacity,
                            (cudaStream_t)stream);
 }
@@ -200,13 +218,16 @@ int fgs_emit(const fgs_camera *cam, int32_t strategy, int32_t band0, int32_t ban
     if (rc) return rc;
     if (strategy < 0 || strategy > 2) return FGS_E_STRATEGY;
     return fgs_launch_emit(L->gaussians, make_cam(cam), strategy, band0, band1,
-                           fgs_frame_view(ws, L), (cudaStream_t)stream);
+                           L->sort_mode == FGS_SORT_TILE_BUCKET, fgs_frame_view(ws, L),
+                           (cudaStream_t)stream);
 }
 
 int fgs_sort(void *ws, const fgs_layout *L, uint32_t epoch, void *stream)
 {
     if (!ws || !L || epoch == 0) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
+    if (L->sort_mode == FGS_SORT_TILE_BUCKET)
+        return fgs_launch_tile_sort(f, L->tiles, L->keep_sorted_keys, (cudaStream_t)stream);
     const SortPlan plan = fgs_sort_plan(L->tile_bits, 0, 1);
     if (plan.npass != L->sort_passes) return FGS_E_WORKSPACE;
     return fgs_launch_sort(f.keys, f.vals, &f.stats->pairs_in_buffer, L->capacity, plan,
@@ -217,7 +238,8 @@ int fgs_ranges(void *ws, const fgs_layout *L, void *stream)
 {
     if (!ws || !L) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
-    return fgs_launch_ranges(f.keys[L->sorted_in], &f.stats->pairs_in_buffer, L->capacity,
+    if (L->sort_mode == FGS_SORT_TILE_BUCKET) return FGS_OK;   // k_scan_tiles already wrote it
+    return fgs_launch_ranges(f.keys[L->sorted_keys_in], &f.stats->pairs_in_buffer, L->capacity,
                              L->tiles, f.starts, f.stats, (cudaStream_t)stream);
 }
 
@@ -228,7 +250,7 @@ int fgs_blend(const float bg[3], double tau, int32_t flags, int32_t band0, int32
     if (!bg || !out_rgb || !ws || !L) return FGS_E_ARG;
     if (band0 < 0 || band1 >= L->grid_h) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
-    return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_in], f.starts, L->width, L->height,
+    return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in], f.starts, L->width, L->height,
                             bg, tau, flags, band0, band1, out_rgb, out_alpha, out_depth, f.contrib,
                             f.stats, (cudaStream_t)stream);
 }

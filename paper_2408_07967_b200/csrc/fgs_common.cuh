@@ -75,6 +75,8 @@ struct FrameDev {
     int32_t  *starts;
     uint8_t  *contrib;
     fgs_stats *stats;
+    uint32_t *tilecount;    // [tiles]
+    uint32_t *cursor;       // [tiles]
 };
 
 static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
@@ -98,6 +100,8 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.starts = (int32_t *)(b + L->off_starts);
     f.contrib = (uint8_t *)(b + L->off_contrib);
     f.stats = (fgs_stats *)(b + L->off_stats);
+    f.tilecount = (uint32_t *)(b + L->off_tilecount);
+    f.cursor = (uint32_t *)(b + L->off_cursor);
     return f;
 }
 
@@ -108,10 +112,12 @@ int  fgs_launch_pack(const float *means, const float *opac, const float *scales,
 int  fgs_launch_cutoffs(const SceneDev &sc, int64_t P, double tau, float *k, cudaStream_t st);
 int  fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, const CamDev &cam,
                            double tau, int sh_degree, int strategy, int band0, int band1,
-                           const FrameDev &f, cudaStream_t st);
+                           int bucket, int tiles, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream_t st);
+int  fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st);
 int  fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int band1,
-                     const FrameDev &f, cudaStream_t st);
+                     int bucket, const FrameDev &f, cudaStream_t st);
+int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st);
 
 struct SortPlan {
     int npass;

@@ -130,13 +130,20 @@ struct TileJob {
 };
 
 // Walk the warp's candidate tiles 32 at a time.  Returns this lane's number of
-// passing tiles.  With EMIT, pass j of lane o is written at out_base(o) + rank.
-template <bool PRECISE, bool EMIT>
+// passing tiles.  MODE selects what happens to a passing (tile, Gaussian):
+//   WALK_COUNT   nothing (count only)
+//   WALK_HIST    also bump the per-tile histogram (TILE_BUCKET counting pass)
+//   WALK_EMIT    write (key, value) at out_base(owner) + rank      (ONESWEEP)
+//   WALK_SCATTER write (depth bits << 32 | index) at the tile's cursor (TILE_BUCKET)
+enum { WALK_COUNT = 0, WALK_HIST = 1, WALK_EMIT = 2, WALK_SCATTER = 3 };
+
+template <bool PRECISE, int MODE>
 __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int width, int height,
                                                     int grid_w, uint32_t out_base,
                                                     uint32_t depth_bits, uint32_t gid,
                                                     uint64_t *__restrict__ keys,
-                                                    uint32_t *__restrict__ vals)
+                                                    uint32_t *__restrict__ vals,
+                                                    uint32_t *__restrict__ tile_ctr)
 {
     const int lane = threadIdx.x & 31;
     const uint32_t incl = warp_incl_scan(job.cand, lane);
@@ -172,7 +179,10 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
         }
         const uint32_t ballot = __ballot_sync(FGS_FULL, pass);
-        if (EMIT) {
+        if (MODE == WALK_HIST) {
+            if (pass) atomicAdd(&tile_ctr[ty * grid_w + tx], 1u);
+        }
+        if (MODE == WALK_EMIT) {
             const uint32_t run_o = __shfl_sync(FGS_FULL, mine, o);
             const uint32_t base_o = __shfl_sync(FGS_FULL, out_base, o);
             const uint32_t bits_o = __shfl_sync(FGS_FULL, depth_bits, o);
@@ -183,6 +193,14 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
                 const uint32_t slot = base_o + run_o + __popc(before);
                 keys[slot] = ((uint64_t)(uint32_t)(ty * grid_w + tx) << 32) | bits_o;
                 vals[slot] = gid_o;
+            }
+        }
+        if (MODE == WALK_SCATTER) {
+            const uint32_t bits_o = __shfl_sync(FGS_FULL, depth_bits, o);
+            const uint32_t gid_o = __shfl_sync(FGS_FULL, gid, o);
+            if (pass) {
+                const uint32_t slot = atomicAdd(&tile_ctr[ty * grid_w + tx], 1u);
+                keys[slot] = ((uint64_t)bits_o << 32) | gid_o;
             }
         }
         // owner side: how many of my candidates in this window passed
@@ -229,7 +247,7 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
 // ---------------------------------------------------------------------------
 // K1: preprocess + count
 // ---------------------------------------------------------------------------
-template <int STRAT>
+template <int STRAT, bool BUCKET>
 __global__ void __launch_bounds__(FGS_PRE_THREADS)
 k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
              const __grid_constant__ CamDev cam, float tau32, float frustum_thresh,
@@ -413,9 +431,12 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     }
 
     uint32_t npairs;
-    if (STRAT == FGS_PRECISE)
-        npairs = warp_walk_tiles<true, false>(job, cam.width, cam.height, cam.grid_w, 0, 0, 0,
-                                              nullptr, nullptr);
+    if (BUCKET)
+        npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_HIST>(
+            job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, f.tilecount);
+    else if (STRAT == FGS_PRECISE)
+        npairs = warp_walk_tiles<true, WALK_COUNT>(job, cam.width, cam.height, cam.grid_w, 0, 0, 0,
+                                                   nullptr, nullptr, nullptr);
     else
         npairs = job.cand;
     if (live) f.counts[g] = npairs;
@@ -448,31 +469,34 @@ static_assert(sizeof(CamDev) % 4 == 0, "CamDev must be word-sized");
 
 int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, const CamDev &cam,
                           double tau, int sh_degree, int strategy, int band0, int band1,
-                          const FrameDev &f, cudaStream_t st)
+                          int bucket, int tiles, const FrameDev &f, cudaStream_t st)
 {
     (void)g_dummy_cam;
-    cudaError_t e = cudaMemsetAsync(f.stats, 0, sizeof(fgs_stats), st);
+    // stats and (TILE_BUCKET) the per-tile histogram sit back to back: one memset
+    const size_t zero_bytes = bucket ? (size_t)((char *)(f.tilecount + tiles) - (char *)f.stats)
+                                     : sizeof(fgs_stats);
+    cudaError_t e = cudaMemsetAsync(f.stats, 0, zero_bytes, st);
     if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
     if (P == 0) return FGS_OK;
     const double th = tau > 1.0 / 255.0 ? tau : 1.0 / 255.0;       // projection.py:46
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     const float tau32 = (float)tau, fth = (float)th;
+#define FGS_K1(S, B) k_preprocess<S, B><<<blocks, FGS_PRE_THREADS, 0, st>>>( \
+        sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f)
     switch (strategy) {
     case FGS_PRECISE:
-        k_preprocess<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, 0, st>>>(
-            sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f);
+        if (bucket) FGS_K1(FGS_PRECISE, true); else FGS_K1(FGS_PRECISE, false);
         break;
     case FGS_TIGHT_AABB:
-        k_preprocess<FGS_TIGHT_AABB><<<blocks, FGS_PRE_THREADS, 0, st>>>(
-            sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f);
+        if (bucket) FGS_K1(FGS_TIGHT_AABB, true); else FGS_K1(FGS_TIGHT_AABB, false);
         break;
     case FGS_BASELINE_CIRCLE_AABB:
-        k_preprocess<FGS_BASELINE_CIRCLE_AABB><<<blocks, FGS_PRE_THREADS, 0, st>>>(
-            sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f);
+        if (bucket) FGS_K1(FGS_BASELINE_CIRCLE_AABB, true); else FGS_K1(FGS_BASELINE_CIRCLE_AABB, false);
         break;
     default:
         return FGS_E_STRATEGY;
     }
+#undef FGS_K1
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
@@ -540,10 +564,84 @@ int fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream
     return FGS_OK;
 }
 
+// K2 (TILE_BUCKET): exclusive scan of the per-tile histogram.  The result IS the
+// range table (sorting.py:139-152): starts[t] .. starts[t+1] is tile t's bucket.
+// Also seeds the scatter cursors, fixes M / overflow and counts non-empty tiles.
+__global__ void __launch_bounds__(1024)
+k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
+             uint32_t *__restrict__ cursor, int tiles, unsigned long long capacity,
+             fgs_stats *__restrict__ stats)
+{
+    __shared__ unsigned long long s_w[32];
+    __shared__ unsigned long long s_carry;
+    __shared__ uint32_t s_nonempty;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x == 0) { s_carry = 0ull; s_nonempty = 0u; }
+    __syncthreads();
+    uint32_t nonempty = 0;
+    for (int base = 0; base < tiles; base += 1024) {
+        const int i = base + threadIdx.x;
+        const unsigned long long v = i < tiles ? counts[i] : 0u;
+        nonempty += v ? 1u : 0u;
+        unsigned long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long t = __shfl_up_sync(FGS_FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        if (lane == 31) s_w[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            const unsigned long long ws = s_w[lane];
+            unsigned long long wi = ws;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long t = __shfl_up_sync(FGS_FULL, wi, o);
+                if (lane >= o) wi += t;
+            }
+            s_w[lane] = wi - ws;
+        }
+        __syncthreads();
+        const unsigned long long excl = s_carry + s_w[w] + incl - v;
+        if (i < tiles) {
+            const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
+            starts[i] = (int32_t)e32;
+            cursor[i] = e32;
+        }
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = excl + v;
+        __syncthreads();
+    }
+    nonempty = __reduce_add_sync(FGS_FULL, nonempty);
+    if (lane == 0 && nonempty) atomicAdd(&s_nonempty, nonempty);
+    __syncthreads();
+    const unsigned long long M = s_carry;
+    const bool over = M > capacity;
+    if (threadIdx.x == 0) {
+        stats->pairs_emitted = M > 0xffffffffull ? 0xffffffffu : (uint32_t)M;
+        stats->overflow = over ? 1u : 0u;
+        stats->pairs_in_buffer = over ? 0u : (uint32_t)M;
+        stats->tiles_nonempty = s_nonempty;
+        starts[tiles] = (int32_t)(M > 0x7fffffffull ? 0x7fffffffu : (uint32_t)M);
+    }
+    // overflow: the frame is re-run with a larger buffer; leave an all-empty range
+    // table so the remaining kernels of this frame touch nothing
+    if (over)
+        for (int i = threadIdx.x; i <= tiles; i += 1024) starts[i] = 0;
+}
+
+int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st)
+{
+    k_scan_tiles<<<1, 1024, 0, st>>>(f.tilecount, f.starts, f.cursor, tiles,
+                                     (unsigned long long)capacity, f.stats);
+    FGS_AFTER_LAUNCH(st);
+    return FGS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // K3: emit (key, value) pairs at the scanned offsets
 // ---------------------------------------------------------------------------
-template <int STRAT>
+template <int STRAT, bool BUCKET>
 __global__ void __launch_bounds__(FGS_PRE_THREADS)
 k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev f)
 {
@@ -552,9 +650,13 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const bool live = g < P;
     const uint32_t cnt = live ? f.counts[g] : 0u;
-    uint32_t total;
-    const uint32_t off = f.blockbase[blockIdx.x] + block_excl_scan_256(cnt, s_scan, total);
-    if (total == 0) return;                              // uniform per block
+    uint32_t total, off = 0;
+    if (BUCKET) {
+        if (__syncthreads_or(cnt != 0u) == 0) return;    // uniform per block
+    } else {
+        off = f.blockbase[blockIdx.x] + block_excl_scan_256(cnt, s_scan, total);
+        if (total == 0) return;                          // uniform per block
+    }
 
     TileJob job;
     job.cand = 0;
@@ -582,21 +684,27 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
         // binning.py:50-51: depths must be positive and finite
         if (!(d > 0.0f) || !(d < __int_as_float(0x7f800000))) f.stats->bad_depth = 1u;
     }
-    warp_walk_tiles<STRAT == FGS_PRECISE, true>(job, width, height, grid_w, off, bits,
-                                                (uint32_t)g, f.keys[0], f.vals[0]);
+    if (BUCKET)
+        warp_walk_tiles<STRAT == FGS_PRECISE, WALK_SCATTER>(job, width, height, grid_w, 0, bits,
+                                                            (uint32_t)g, f.keys[0], nullptr, f.cursor);
+    else
+        warp_walk_tiles<STRAT == FGS_PRECISE, WALK_EMIT>(job, width, height, grid_w, off, bits,
+                                                         (uint32_t)g, f.keys[0], f.vals[0], nullptr);
 }
 
 int fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int band1,
-                    const FrameDev &f, cudaStream_t st)
+                    int bucket, const FrameDev &f, cudaStream_t st)
 {
     if (P == 0) return FGS_OK;
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
-    if (strategy == FGS_PRECISE)
-        k_emit<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, 0, st>>>((int)P, cam.width, cam.height,
-                                                               cam.grid_w, band0, band1, f);
-    else
-        k_emit<FGS_TIGHT_AABB><<<blocks, FGS_PRE_THREADS, 0, st>>>((int)P, cam.width, cam.height,
-                                                                  cam.grid_w, band0, band1, f);
+#define FGS_K3(S, B) k_emit<S, B><<<blocks, FGS_PRE_THREADS, 0, st>>>( \
+        (int)P, cam.width, cam.height, cam.grid_w, band0, band1, f)
+    if (strategy == FGS_PRECISE) {
+        if (bucket) FGS_K3(FGS_PRECISE, true); else FGS_K3(FGS_PRECISE, false);
+    } else {
+        if (bucket) FGS_K3(FGS_TIGHT_AABB, true); else FGS_K3(FGS_TIGHT_AABB, false);
+    }
+#undef FGS_K3
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }

@@ -82,7 +82,7 @@ struct SortSmem {
     uint32_t tile;
 };
 
-__global__ void __launch_bounds__(FGS_SORT_THREADS, 2)
+__global__ void __launch_bounds__(FGS_SORT_THREADS, 3)
 k_sort_pass(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
             uint64_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
             const uint32_t *__restrict__ n_dev, PassArgs pa, const uint32_t *__restrict__ hist,
@@ -151,14 +151,28 @@ k_sort_pass(const uint64_t *__restrict__ keys_in, const uint32_t *__restrict__ v
             *(volatile uint64_t *)st = tag | ST_INCL | cnt;
         } else {
             *(volatile uint64_t *)st = tag | ST_AGG | cnt;
-            for (uint32_t t = tile; t-- > 0;) {
-                const volatile uint64_t *ps = state + (size_t)t * 256 + tid;
-                uint64_t v;
-                do {
-                    v = *ps;
-                } while ((uint32_t)(v >> 32) != epoch || ((uint32_t)v & ST_MASK) == 0u);
-                excl += (uint32_t)v & ~ST_MASK;
-                if (((uint32_t)v & ST_MASK) == ST_INCL) break;
+            // look back 8 predecessors per round trip (independent loads in flight);
+            // tile 0 always carries an inclusive prefix, so the walk terminates
+            int t = (int)tile - 1;
+            for (bool found = false; !found;) {
+                uint64_t v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    v[i] = (t - i >= 0) ? *(const volatile uint64_t *)(state + (size_t)(t - i) * 256 + tid)
+                                        : 0ull;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (found || t - i < 0) continue;
+                    const uint32_t lo = (uint32_t)v[i];
+                    if ((uint32_t)(v[i] >> 32) != epoch || (lo & ST_MASK) == 0u) {
+                        t -= i;                 // not published yet: poll again from here
+                        goto next_round;
+                    }
+                    excl += lo & ~ST_MASK;
+                    if ((lo & ST_MASK) == ST_INCL) found = true;
+                }
+                t -= 8;
+            next_round:;
             }
             *(volatile uint64_t *)st = tag | ST_INCL | (excl + cnt);
         }
@@ -226,7 +240,216 @@ k_tile_ranges(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ n_
     if ((threadIdx.x & 31) == 0 && nonempty) atomicAdd(&stats->tiles_nonempty, nonempty);
 }
 
+// ---- TILE_BUCKET: per-tile sort in shared memory ------------------------------
+// After the MSD counting pass (k_preprocess histogram -> k_scan_tiles -> k_emit
+// scatter) tile t's pairs sit, in arbitrary order, in rec[starts[t] .. starts[t+1])
+// as (depth bits << 32 | Gaussian index).  One CTA sorts one bucket ascending on
+// that 64-bit word, which is exactly the reference's (depth, then index) order
+// inside a tile (sorting.py:3-5).  Records are unique.
+//
+// Buckets of up to 4096 records: LSD radix sort on the four depth bytes, entirely
+// in shared memory (same stable warp-match ranking as k_sort_pass, local digit
+// offsets instead of a look-back), then equal-depth neighbours -- rare: two
+// Gaussians with the same float32 depth in one tile -- are put in index order by
+// an odd-even pass.  Larger buckets (very dense scenes) use a bitonic network in
+// its all-ascending form, long strides through L2 and the rest chunk-wise in
+// shared memory; every comparator moves the larger element up, so comparators
+// touching an index >= n are simply skipped and any n works without padding.
+constexpr int TS_THREADS = 256;
+constexpr int TS_CAP = 4096;
+constexpr int TS_E = TS_CAP / TS_THREADS;       // max records per thread
+
+struct TileSortSmem {
+    uint64_t s[TS_CAP];
+    uint32_t whist[NW][BINS];
+    uint32_t texcl[256];
+    uint32_t scan[8];
+};
+
+__device__ __forceinline__ void ts_step_smem(uint64_t *s, int count, int mask, int hb)
+{
+    // compare-exchange (i, i ^ mask) for every i < count with bit `hb` clear
+    for (int t = threadIdx.x; t < count / 2; t += TS_THREADS) {
+        const int i = ((t & ~(hb - 1)) << 1) | (t & (hb - 1));
+        const int p = i ^ mask;
+        const uint64_t a = s[i], b = s[p];
+        if (a > b) { s[i] = b; s[p] = a; }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void ts_step_global(uint64_t *g, int n, int npad, int mask, int hb)
+{
+    for (int t = threadIdx.x; t < npad / 2; t += TS_THREADS) {
+        const int i = ((t & ~(hb - 1)) << 1) | (t & (hb - 1));
+        const int p = i ^ mask;
+        if (p < n) {
+            const uint64_t a = g[i], b = g[p];
+            if (a > b) { g[i] = b; g[p] = a; }
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void ts_bitonic_smem(uint64_t *s, int npad)
+{
+    for (int k = 2; k <= npad; k <<= 1) {
+        ts_step_smem(s, npad, k - 1, k >> 1);
+        for (int j = k >> 2; j > 0; j >>= 1) ts_step_smem(s, npad, j, j);
+    }
+}
+
+__global__ void __launch_bounds__(TS_THREADS, 4)
+k_tile_sort(uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
+            uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts, int write_keys,
+            const fgs_stats *__restrict__ stats)
+{
+    __shared__ TileSortSmem S;
+    if (stats->overflow) return;
+    const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    if (n <= 0) return;
+    uint64_t *g = rec + start;
+    uint64_t *s = S.s;
+    const uint64_t tile_hi = (uint64_t)(uint32_t)tile << 32;
+
+    if (n <= TS_CAP) {
+        if (n > 1) {
+            // records spread evenly over the warps: E per thread, warp-striped
+            const int E = (n + TS_THREADS - 1) / TS_THREADS;
+            const int wbase = w * 32 * E;
+            uint64_t key[TS_E];
+            uint16_t rank[TS_E];
+#pragma unroll
+            for (int i = 0; i < TS_E; ++i) {
+                const int loc = wbase + i * 32 + lane;
+                key[i] = (i < E && loc < n) ? g[loc] : ~0ull;
+            }
+            uint32_t *wh = S.whist[w];
+            for (int pass = 0; pass < 4; ++pass) {
+                const int shift = 32 + 8 * pass;
+                for (int i = tid; i < NW * BINS; i += TS_THREADS) (&S.whist[0][0])[i] = 0u;
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < TS_E; ++i) {
+                    if (i < E) {                                  // uniform
+                        const bool ok = wbase + i * 32 + lane < n;
+                        const uint32_t d = ok ? (uint32_t)(key[i] >> shift) & 0xffu : 256u;
+                        const uint32_t prev = wh[d];
+                        __syncwarp();
+                        const uint32_t peers = __match_any_sync(FGS_FULL, d);
+                        const uint32_t before = __popc(peers & lanemask_lt());
+                        if (before == 0) wh[d] = prev + __popc(peers);
+                        __syncwarp();
+                        rank[i] = (uint16_t)(prev + before);
+                    }
+                }
+                __syncthreads();
+                uint32_t cnt = 0;
+#pragma unroll
+                for (int ww = 0; ww < NW; ++ww) {
+                    const uint32_t c = S.whist[ww][tid];
+                    S.whist[ww][tid] = cnt;
+                    cnt += c;
+                }
+                uint32_t ttotal;
+                S.texcl[tid] = block_excl_scan_256(cnt, S.scan, ttotal);
+                __syncthreads();
+#pragma unroll
+                for (int i = 0; i < TS_E; ++i) {
+                    if (i < E && wbase + i * 32 + lane < n) {
+                        const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
+                        s[S.texcl[d] + wh[d] + rank[i]] = key[i];
+                    }
+                }
+                __syncthreads();
+                if (pass < 3) {
+#pragma unroll
+                    for (int i = 0; i < TS_E; ++i) {
+                        const int loc = wbase + i * 32 + lane;
+                        key[i] = (i < E && loc < n) ? s[loc] : ~0ull;
+                    }
+                }
+            }
+            // equal depths: order by index (low word).  Odd-even transposition over
+            // equal-depth neighbours; almost always zero or one round.
+            for (int round = 0;; ++round) {
+                bool swapped = false;
+                for (int t = tid; 2 * t + 1 < n; t += TS_THREADS) {
+                    const uint64_t a = s[2 * t], b = s[2 * t + 1];
+                    if ((a >> 32) == (b >> 32) && a > b) { s[2 * t] = b; s[2 * t + 1] = a; swapped = true; }
+                }
+                __syncthreads();
+                for (int t = tid; 2 * t + 2 < n; t += TS_THREADS) {
+                    const uint64_t a = s[2 * t + 1], b = s[2 * t + 2];
+                    if ((a >> 32) == (b >> 32) && a > b) { s[2 * t + 1] = b; s[2 * t + 2] = a; swapped = true; }
+                }
+                if (!__syncthreads_or(swapped)) break;
+                if (round == 6) {           // long runs of one depth: finish with the network
+                    int npad = 2;
+                    while (npad < n) npad <<= 1;
+                    for (int i = n + tid; i < npad; i += TS_THREADS) s[i] = ~0ull;
+                    __syncthreads();
+                    ts_bitonic_smem(s, npad);
+                    break;
+                }
+            }
+        } else {
+            if (tid == 0) s[0] = g[0];
+            __syncthreads();
+        }
+        for (int i = tid; i < n; i += TS_THREADS) {
+            const uint64_t r = s[i];
+            vals_out[start + i] = (uint32_t)r;
+            if (write_keys) keys_out[start + i] = tile_hi | (r >> 32);
+        }
+        return;
+    }
+
+    // large bucket: chunk-wise in shared memory, long strides through L2
+    int npad = TS_CAP;
+    while (npad < n) npad <<= 1;
+    const int nchunks = (n + TS_CAP - 1) / TS_CAP;
+    for (int c = 0; c < nchunks; ++c) {
+        const int cb = c * TS_CAP;
+        for (int i = tid; i < TS_CAP; i += TS_THREADS) s[i] = cb + i < n ? g[cb + i] : ~0ull;
+        __syncthreads();
+        ts_bitonic_smem(s, TS_CAP);
+        for (int i = tid; i < TS_CAP; i += TS_THREADS)
+            if (cb + i < n) g[cb + i] = s[i];
+        __syncthreads();
+    }
+    for (int k = 2 * TS_CAP; k <= npad; k <<= 1) {
+        ts_step_global(g, n, npad, k - 1, k >> 1);
+        int j = k >> 2;
+        for (; j >= TS_CAP; j >>= 1) ts_step_global(g, n, npad, j, j);
+        for (int c = 0; c < nchunks; ++c) {
+            const int cb = c * TS_CAP;
+            for (int i = tid; i < TS_CAP; i += TS_THREADS) s[i] = cb + i < n ? g[cb + i] : ~0ull;
+            __syncthreads();
+            for (int jj = TS_CAP >> 1; jj > 0; jj >>= 1) ts_step_smem(s, TS_CAP, jj, jj);
+            for (int i = tid; i < TS_CAP; i += TS_THREADS)
+                if (cb + i < n) g[cb + i] = s[i];
+            __syncthreads();
+        }
+    }
+    for (int i = tid; i < n; i += TS_THREADS) {
+        const uint64_t r = g[i];
+        vals_out[start + i] = (uint32_t)r;
+        if (write_keys) keys_out[start + i] = tile_hi | (r >> 32);
+    }
+}
+
 }  // namespace
+
+int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st)
+{
+    if (tiles <= 0) return FGS_OK;
+    k_tile_sort<<<(unsigned)tiles, TS_THREADS, 0, st>>>(f.keys[0], f.vals[0], f.keys[1], f.starts,
+                                                        write_keys, f.stats);
+    FGS_AFTER_LAUNCH(st);
+    return FGS_OK;
+}
 
 SortPlan fgs_sort_plan(int tile_bits, int value_bits, int compact)
 {
@@ -276,7 +499,7 @@ int fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev,
     FGS_AFTER_LAUNCH(st);
 
     const int64_t tiles_max = (n_max + FGS_SORT_TILE - 1) / FGS_SORT_TILE;
-    const unsigned pgrid = (unsigned)(tiles_max < sms * 2 ? tiles_max : sms * 2);
+    const unsigned pgrid = (unsigned)(tiles_max < sms * 3 ? tiles_max : sms * 3);
     for (int p = 0; p < plan.npass; ++p) {
         const int src = p & 1, dst = src ^ 1;
         k_sort_pass<<<pgrid, FGS_SORT_THREADS, sizeof(SortSmem), st>>>(

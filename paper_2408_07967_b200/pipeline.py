@@ -157,6 +157,10 @@ class _Workspace:
         _capi.check(_capi.lib().fgs_workspace_init(C.c_void_p(self.base), C.byref(self.lay),
                                                    _stream_ptr(torch, device)))
 
+    def set_mode(self, sort_mode, keep_sorted_keys=False):
+        _capi.check(_capi.lib().fgs_layout_set_sort_mode(C.byref(self.lay), int(sort_mode)))
+        self.lay.keep_sorted_keys = 1 if keep_sorted_keys else 0
+
     def next_epoch(self):
         e = self.epoch
         self.epoch += 16
@@ -178,9 +182,16 @@ class Pipeline:
     reference's own dataclasses (matched on field names), as ``pipeline.py:68-75``.
     ``render`` is safe to call from several threads on one object (each call
     takes its own workspace, SURVEY.md §8(b) threading row).
+
+    ``sort_mode``: "tile-bucket" (default; counting pass on the tile field fused
+    into emission + per-tile shared-memory sort) or "onesweep" (global LSD radix
+    sort on the packed tile|depth key).  Both give the bit-identical sorted list.
     """
 
-    def __init__(self, scene, sh_degree=3, device=None):
+    def __init__(self, scene, sh_degree=3, device=None, sort_mode="tile-bucket"):
+        if sort_mode not in _capi.SORT_MODES:
+            raise ValueError(f"unknown sort_mode {sort_mode!r}, expected one of {tuple(_capi.SORT_MODES)}")
+        self.sort_mode = sort_mode
         if is_raw_scene(scene):
             act = activate(scene)
         elif is_activated_scene(scene):
@@ -286,6 +297,7 @@ class Pipeline:
             kcut = self._cutoffs(torch, tau)
             while True:
                 ws = self._take_ws(torch, W, H, capacity)
+                ws.set_mode(_capi.SORT_MODES[self.sort_mode])
                 lay = C.byref(ws.lay)
                 base = C.c_void_p(ws.base)
                 if extras:
@@ -360,6 +372,47 @@ class Pipeline:
             self._give_ws(ws)
         stats.e2e_ns = time.perf_counter_ns() - t_host0
         return fb, stats
+
+
+def sorted_pairs(pipe, camera, strategy="precise", tau=TAU_DEFAULT, band=None):
+    """K1..K5 of the frame path for one camera; returns the device-sorted
+    (keys uint64, values uint32, starts int64) as numpy -- what the blend consumes."""
+    torch = _torch()
+    sid = _strategy_id(strategy)
+    L = _capi.lib()
+    cam = _capi.camera_struct(camera)
+    W, H = int(camera.width), int(camera.height)
+    gh = -(-H // TILE_SIZE)
+    b0, b1 = (0, gh - 1) if band is None else (int(band[0]), int(band[1]))
+    capacity = pipe._default_capacity()
+    with torch.cuda.device(pipe.device):
+        st = _stream_ptr(torch, pipe.device)
+        kcut = pipe._cutoffs(torch, tau)
+        while True:
+            ws = pipe._take_ws(torch, W, H, capacity)
+            ws.set_mode(_capi.SORT_MODES[pipe.sort_mode], keep_sorted_keys=True)
+            lay, base = C.byref(ws.lay), C.c_void_p(ws.base)
+            _capi.check(L.fgs_preprocess(pipe.packed.data_ptr(), kcut.data_ptr(), pipe.count,
+                                         C.byref(cam), float(tau), _check_sh_degree(pipe.sh_degree),
+                                         sid, b0, b1, base, lay, st))
+            _capi.check(L.fgs_scan(base, lay, st))
+            _capi.check(L.fgs_emit(C.byref(cam), sid, b0, b1, base, lay, st))
+            _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
+            _capi.check(L.fgs_ranges(base, lay, st))
+            s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+            if int(s["overflow"]):
+                capacity = max(int(capacity * 1.5) + 16, int(s["pairs_emitted"]) + 4096)
+                continue
+            break
+        M, lay = int(s["pairs_emitted"]), ws.lay
+        keys = ws.view(torch, lay.off_keys[lay.sorted_keys_in], M * 8, torch.int64) \
+            .cpu().numpy().view(np.uint64).copy()
+        vals = ws.view(torch, lay.off_vals[lay.sorted_vals_in], M * 4, torch.int32) \
+            .cpu().numpy().view(np.uint32).copy()
+        starts = ws.view(torch, lay.off_starts, (lay.tiles + 1) * 4, torch.int32) \
+            .cpu().numpy().astype(np.int64)
+        pipe._give_ws(ws)
+    return keys, vals, starts
 
 
 def run_frame(scene, camera, strategy="precise", tau=TAU_DEFAULT,
@@ -445,13 +498,17 @@ def power_cutoffs(alpha0, tau=TAU_DEFAULT):
 
 def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, workers=1,
                        sh_degree=3, chunk_size=None, initial_capacity=None,
-                       band=None) -> BinOutput:
-    """K1 + K2 + K3 for one camera; pairs come back in emission order
-    (ascending Gaussian index), unsorted (``binning.py:197-372``)."""
+                       band=None, sort_mode=None) -> BinOutput:
+    """K1 + K2 + K3 for one camera; pairs come back unsorted (``binning.py:197-372``):
+    in ascending Gaussian index with ``sort_mode="onesweep"``, bucketed by tile
+    (arbitrary order inside a bucket) with ``"tile-bucket"``."""
     torch = _torch()
     sid = _strategy_id(strategy)
     deg = _check_sh_degree(sh_degree)
     pipe = scene if isinstance(scene, Pipeline) else Pipeline(scene, sh_degree=deg)
+    mode = pipe.sort_mode if sort_mode is None else sort_mode
+    if mode not in _capi.SORT_MODES:
+        raise ValueError(f"unknown sort_mode {mode!r}")
     L = _capi.lib()
     cam = _capi.camera_struct(camera)
     W, H = int(camera.width), int(camera.height)
@@ -466,6 +523,7 @@ def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, worke
         kcut = pipe._cutoffs(torch, tau)
         while True:
             ws = pipe._take_ws(torch, W, H, capacity)
+            ws.set_mode(_capi.SORT_MODES[mode])
             lay, base = C.byref(ws.lay), C.c_void_p(ws.base)
             _capi.check(L.fgs_preprocess(pipe.packed.data_ptr(), kcut.data_ptr(), P, C.byref(cam),
                                          float(tau), deg, sid, b0, b1, base, lay, st))
@@ -491,7 +549,15 @@ def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, worke
             .view(np.uint16).reshape(P, 4).astype(np.int32)
         counts = ws.view(torch, lay.off_counts, P * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
         keys = ws.view(torch, lay.off_keys[0], M * 8, torch.int64).cpu().numpy().view(np.uint64).copy()
-        vals = ws.view(torch, lay.off_vals[0], M * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
+        if mode == "tile-bucket":
+            # records are (depth bits << 32 | index), bucketed by tile: rebuild the
+            # reference's (tile << 32 | depth bits, index) pairs from the range table
+            starts = ws.view(torch, lay.off_starts, (lay.tiles + 1) * 4, torch.int32).cpu().numpy()
+            tile_of = np.repeat(np.arange(lay.tiles, dtype=np.uint64), np.diff(starts.astype(np.int64)))
+            vals = (keys & np.uint64(0xffffffff)).astype(np.uint32)
+            keys = (tile_of << np.uint64(32)) | (keys >> np.uint64(32))
+        else:
+            vals = ws.view(torch, lay.off_vals[0], M * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
         cap = ws.capacity
         pipe._give_ws(ws)
     nx = rects[:, 2] - rects[:, 0] + 1

@@ -119,15 +119,20 @@ def test_oracle_parity_all_stages(preset, n, seed, w, h, radius, tau, deg, bg):
     for cam in fgs.orbit_cameras(2, radius, w, h):
         for s in STRATS:
             ob = orc.preprocess_and_bin(act, cam, s, tau, deg)
-            gb = fgs.preprocess_and_bin(pipe, cam, s, tau, sh_degree=deg)
+            ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, max(n, 1))
+            # tile-bucket emission: same multiset, bucketed by tile
+            tb = fgs.preprocess_and_bin(pipe, cam, s, tau, sh_degree=deg, sort_mode="tile-bucket")
+            assert np.all(np.diff((tb.keys >> np.uint64(32)).astype(np.int64)) >= 0)
+            tk, tv = _sorted_pairs(tb, n)
+            assert np.array_equal(tk, ok) and np.array_equal(tv, ov)
+            gb = fgs.preprocess_and_bin(pipe, cam, s, tau, sh_degree=deg, sort_mode="onesweep")
             assert np.array_equal(gb.retained, ob.retained)
             assert np.array_equal(gb.depth.view(np.uint32), ob.depth.view(np.uint32))
             assert np.array_equal(gb.splat.view(np.uint32), ob.splat.view(np.uint32))
             assert np.array_equal(gb.tile_rects[ob.retained], ob.tile_rects[ob.retained])
             assert np.array_equal(gb.pair_counts, ob.pair_counts)
-            # emission order: ascending Gaussian index
+            # onesweep emission order: ascending Gaussian index
             assert np.all(np.diff(gb.values.astype(np.int64)) >= 0)
-            ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, max(n, 1))
             gk, gv = _sorted_pairs(gb, n)
             assert np.array_equal(gk, ok) and np.array_equal(gv, ov)
         # whole frame (precise)
@@ -145,29 +150,39 @@ def test_oracle_parity_all_stages(preset, n, seed, w, h, radius, tau, deg, bg):
         assert stx.pairs_contributing == ost["pairs_contributing"]
 
 
-def test_sorted_buffer_matches_oracle_order():
-    """The frame path's stable sort on key bits alone must reproduce the
-    reference's (key, value) order."""
-    import ctypes as C
-    import torch
-    from paper_2408_07967_b200 import _capi
-    act = fgs.activate(fgs.gen_synthetic("mixed", 50000, 12))
-    cam = fgs.orbit_cameras(1, 20.0, 800, 448)[0]
-    pipe = fgs.Pipeline(act)
+@pytest.mark.parametrize("mode", ["tile-bucket", "onesweep"])
+@pytest.mark.parametrize("n,w,h,radius", [(50000, 800, 448, 20.0), (3000, 70, 42, 6.0),
+                                          (200000, 320, 192, 16.0)])
+def test_sorted_buffer_matches_oracle_order(mode, n, w, h, radius):
+    """What the blend consumes -- the device-sorted (key, value) list and the range
+    table -- must equal the reference's (key, value) order bit for bit, in both
+    sort modes.  The 200K / 320x192 case has buckets far
+    above 4096 pairs (the tile sort's global-stride path)."""
+    act = fgs.activate(fgs.gen_synthetic("mixed", n, 12))
+    cam = fgs.orbit_cameras(1, radius, w, h)[0]
+    pipe = fgs.Pipeline(act, sort_mode=mode)
     ob = orc.preprocess_and_bin(act, cam)
     ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, act.count)
     ostarts = orc.tile_range_table(ok, ob.grid_w, ob.grid_h)
-    fb, st = pipe.render(cam)
-    ws = pipe._free[(800, 448)][0]
-    lay, M = ws.lay, st.pairs_emitted
-    assert M == ok.shape[0]
-    si = int(lay.sorted_in)
-    keys = ws.view(torch, lay.off_keys[si], M * 8, torch.int64).cpu().numpy().view(np.uint64)
-    vals = ws.view(torch, lay.off_vals[si], M * 4, torch.int32).cpu().numpy().view(np.uint32)
-    starts = ws.view(torch, lay.off_starts, (lay.tiles + 1) * 4, torch.int32).cpu().numpy()
+    keys, vals, starts = fgs.sorted_pairs(pipe, cam)
     assert np.array_equal(keys, ok)
     assert np.array_equal(vals, ov)
-    assert np.array_equal(starts.astype(np.int64), ostarts)
+    assert np.array_equal(starts, ostarts)
+    fb, st = pipe.render(cam, exact=True)
+    oimg, ost = orc.render(act, cam)
+    assert np.array_equal(fb.image.view(np.uint32), oimg.view(np.uint32))
+    assert (st.pairs_emitted, st.tiles_nonempty, st.pairs_contributing) == \
+        (ost["pairs_emitted"], ost["tiles_nonempty"], ost["pairs_contributing"])
+
+
+def test_both_sort_modes_give_identical_frames():
+    act = fgs.activate(fgs.gen_synthetic("elongated", 40000, 3))
+    for cam in fgs.orbit_cameras(2, 14.0, 640, 360):
+        a, sa = fgs.Pipeline(act, sort_mode="tile-bucket").render(cam)
+        b, sb = fgs.Pipeline(act, sort_mode="onesweep").render(cam)
+        assert np.array_equal(a.image, b.image)
+        assert (sa.pairs_emitted, sa.tiles_nonempty, sa.pairs_contributing) == \
+            (sb.pairs_emitted, sb.tiles_nonempty, sb.pairs_contributing)
 
 
 # ---------------------------------------------------------------------------

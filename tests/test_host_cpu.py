@@ -52,9 +52,14 @@ def test_struct_layouts_match_the_c_compiler():
 def test_workspace_layout_is_host_only_and_consistent(lib):
     lay = _capi.layout(1_000_000, 1920, 1080, 8_000_000)
     assert (lay.grid_w, lay.grid_h, lay.tiles, lay.tile_bits) == (120, 68, 8160, 13)
-    assert lay.sort_passes == 6 and lay.sorted_in == 0
+    assert lay.sort_passes == 6 and lay.sort_mode == _capi.SORT_TILE_BUCKET
+    assert (lay.sorted_keys_in, lay.sorted_vals_in) == (1, 0)
+    one = _capi.layout(1_000_000, 1920, 1080, 8_000_000, _capi.SORT_ONESWEEP)
+    assert (one.sort_mode, one.sorted_keys_in, one.sorted_vals_in) == (0, 0, 0)
+    assert one.total_bytes == lay.total_bytes
     assert lay.preprocess_blocks == 3907
-    offs = [lay.off_stats, lay.off_splat, lay.off_depth, lay.off_rects, lay.off_flags,
+    assert lay.off_tilecount == lay.off_stats + 256        # one memset clears stats + histogram
+    offs = [lay.off_stats, lay.off_tilecount, lay.off_cursor, lay.off_splat, lay.off_depth, lay.off_rects, lay.off_flags,
             lay.off_counts, lay.off_blocksums, lay.off_keys[0], lay.off_keys[1],
             lay.off_vals[0], lay.off_vals[1], lay.off_sortstate, lay.off_hist,
             lay.off_starts, lay.off_contrib]
