@@ -116,8 +116,9 @@ typedef struct fgs_layout {
     uint64_t off_starts;       /* int32  [tiles + 1]  sorting.py:139-152      */
     uint64_t off_contrib;      /* uint8  [capacity]                           */
     uint64_t off_stats;        /* fgs_stats                                   */
-    uint64_t off_tilecount;    /* uint32 [tiles]  pairs per tile (TILE_BUCKET) */
-    uint64_t off_cursor;       /* uint32 [tiles]  scatter cursors (TILE_BUCKET)*/
+    uint64_t off_tilecount;    /* uint32 [tiles][8], word 0 used: pairs per tile
+                                  (TILE_BUCKET; one 32-byte sector per counter) */
+    uint64_t off_cursor;       /* uint32 [tiles][8], word 0 used: scatter cursors */
     int64_t  gaussians, capacity;
     int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
     int32_t  preprocess_blocks, sort_passes;
@@ -177,7 +178,8 @@ int fgs_workspace_init(void *workspace, const fgs_layout *layout_host, void *str
 /* binning.py:197-257 preprocess_and_bin, phase A + the count half of phase B:
  * cull, project, conic, cutoff, extent rectangle, SH colour, and the number of
  * candidate tiles that pass the strategy's test (intersect.py:63-94 for
- * `precise`).  Writes splat rows, depth, rects, flags, counts, block sums.
+ * `precise`).  Writes splat rows, depth, rects, flags, counts, and block sums
+ * (ONESWEEP) or the per-tile histogram (TILE_BUCKET).
  * Tile rows outside [band_ty0, band_ty1] are not counted (row-band mode;
  * pass 0 and grid_h-1 for a whole frame). */
 int fgs_preprocess(const void *packed_scene, const float *k_cut, int64_t gaussians,
@@ -189,9 +191,13 @@ int fgs_preprocess(const void *packed_scene, const float *k_cut, int64_t gaussia
  * per-block pair counts; fixes M, the overflow flag, and resets sort counters. */
 int fgs_scan(void *workspace, const fgs_layout *layout_host, void *stream);
 
-/* binning.py:264-354 phase B emit: key = tile << 32 | depth bits
- * (binning.py:47-54), value = Gaussian index, written at the scanned offsets,
- * i.e. in ascending Gaussian order (deterministic, unlike an atomic cursor). */
+/* binning.py:264-354 phase B emit.
+ * ONESWEEP: key = tile << 32 | depth bits (binning.py:47-54), value = Gaussian
+ *   index, written at the scanned offsets, i.e. in ascending Gaussian order
+ *   (deterministic, unlike an atomic cursor) into keys[0] / vals[0].
+ * TILE_BUCKET: every pair is written once, as a (depth bits << 32 | index)
+ *   record at its tile's cursor in keys[0] (cursors start at the scanned
+ *   histogram); order inside a bucket is arbitrary until fgs_sort. */
 int fgs_emit(const fgs_camera *camera_host, int32_t strategy, int32_t band_ty0,
              int32_t band_ty1, void *workspace, const fgs_layout *layout_host,
              void *stream);

@@ -94,6 +94,7 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
 {
     __shared__ BlendSmem S;
+    if (stats != nullptr && stats->overflow) return;   // frame is re-run with a larger buffer
     const int tid = threadIdx.x;
     const int tx = blockIdx.x, ty = ty_first + blockIdx.y;
     const int tile = ty * grid_w + tx;
@@ -106,13 +107,19 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
     const float wx_lo = (float)bx + 0.5f, wx_hi = (float)bx + 7.5f;
     const float wy_lo = (float)by + 0.5f, wy_hi = (float)by + 3.5f;
     const bool inside = px < width && py < height;
-    const float fx = (float)px + 0.5f, fy = (float)py + 0.5f;
+    // A finished pixel (outside the image, or T < 1e-4) parks its x centre at +inf: every
+    // later extent test then rejects it (render.py:203-204) without a separate flag.
+    const float kInf = __int_as_float(0x7f800000);
+    float fx = inside ? (float)px + 0.5f : kInf;
+    const float fy = (float)py + 0.5f;
+    // alpha within 1e-5 (relative) of tau <=> its bit pattern within [band_lo, band_lo+band_span]
+    const uint32_t band_lo = __float_as_uint(tau * (1.0f - 1e-5f));
+    const uint32_t band_span = __float_as_uint(tau * (1.0f + 1e-5f)) - band_lo;
 
     const int start = starts[tile], n = starts[tile + 1] - start;
     if (tid < 32) S.tab[tid] = c_exp2_tab[tid];
 
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, dz = 0.0f;
-    bool done = !inside;
     uint32_t ncontrib = 0;
 
     const int nb = (n + FGS_BLEND_BATCH - 1) / FGS_BLEND_BATCH;
@@ -151,7 +158,7 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         const int cnt = n - b * FGS_BLEND_BATCH < FGS_BLEND_BATCH ? n - b * FGS_BLEND_BATCH
                                                                   : FGS_BLEND_BATCH;
         for (int c0 = 0; c0 < cnt; c0 += 32) {
-            if (__all_sync(FGS_FULL, done)) break;
+            if (__all_sync(FGS_FULL, fx == kInf)) break;
             // warp-level cull, one pair per lane: a pair whose extent rectangle misses the
             // whole 8x4 block is rejected by every pixel's render.py:211 test (float32
             // subtraction is monotone, so testing the block's extreme centres is exact)
@@ -171,7 +178,7 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                 const float4 r2 = S.row[cur][j][2];
                 const float dx = fs(fx, r0.x), dy = fs(fy, r0.y);
                 // render.py:211 extent rectangle, exact float32 compares
-                if (done || fabsf(dx) > r2.z || fabsf(dy) > r2.w) continue;
+                if (fabsf(dx) > r2.z || fabsf(dy) > r2.w) continue;
                 const float4 r1 = S.row[cur][j][1];
                 // render.py:213  s = 0.5*(a dx dx + c dy dy) + b dx dy, unfused
                 const float s = fa(fm(0.5f, fa(fm(fm(r0.z, dx), dx), fm(fm(r1.x, dy), dy))),
@@ -182,7 +189,8 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                     al = fm(r1.y, expf_exact(-s, S.tab));
                 } else {
                     al = r1.y * ex2_approx(-s * 1.4426950408889634f);
-                    if (fabsf(al - tau) <= tau * 1e-5f) al = fm(r1.y, expf_exact(-s, S.tab));
+                    if (__float_as_uint(al) - band_lo <= band_span)
+                        al = fm(r1.y, expf_exact(-s, S.tab));
                 }
                 al = al > FGS_ALPHA_CAP ? FGS_ALPHA_CAP : al;     // render.py:217-218
                 if (al < tau) continue;                           // render.py:219
@@ -202,10 +210,10 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                     T = T * (1.0f - al);
                 }
                 if (CONTRIB) S.touched[cur][j] = 1u;
-                done = T < FGS_T_STOP;                            // render.py:228
+                if (T < FGS_T_STOP) fx = kInf;                    // render.py:228
             }
         }
-        const bool all_done = __syncthreads_and(done);
+        const bool all_done = __syncthreads_and(fx == kInf);
         if (CONTRIB) {
             if (tid < cnt) {
                 const uint32_t t = S.touched[cur][tid];

@@ -139,8 +139,8 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     const uint64_t cap = (uint64_t)capacity, p = (uint64_t)P;
     const uint64_t sort_tiles = (cap + FGS_SORT_TILE - 1) / FGS_SORT_TILE;
     L->off_stats = take(sizeof(fgs_stats));          // stats and tilecount are contiguous:
-    L->off_tilecount = take((uint64_t)L->tiles * 4); // one memset clears both
-    L->off_cursor = take((uint64_t)L->tiles * 4);
+    L->off_tilecount = take((uint64_t)L->tiles * 4 * FGS_CTR_STRIDE); // one memset clears both
+    L->off_cursor = take((uint64_t)L->tiles * 4 * FGS_CTR_STRIDE);
     L->off_splat = take(p * 48);
     L->off_depth = take(p * 4);
     L->off_rects = take(p * 8);

@@ -24,6 +24,9 @@
 #define FGS_SORT_TILE     (FGS_SORT_THREADS * FGS_SORT_IPT)   // 4096 pairs per CTA pass
 #define FGS_SORT_MAXPASS  16
 #define FGS_BLEND_BATCH   256
+// per-tile atomic counters sit FGS_CTR_STRIDE words apart (one 32-byte sector each):
+// thousands of L2 atomics on neighbouring words of one line serialise
+#define FGS_CTR_STRIDE    8
 
 // Camera as the kernels see it (passed by value: lives in the constant bank).
 struct CamDev {

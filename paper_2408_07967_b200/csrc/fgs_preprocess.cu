@@ -131,10 +131,14 @@ struct TileJob {
 
 // Walk the warp's candidate tiles 32 at a time.  Returns this lane's number of
 // passing tiles.  MODE selects what happens to a passing (tile, Gaussian):
-//   WALK_COUNT   nothing (count only)
-//   WALK_HIST    also bump the per-tile histogram (TILE_BUCKET counting pass)
-//   WALK_EMIT    write (key, value) at out_base(owner) + rank      (ONESWEEP)
-//   WALK_SCATTER write (depth bits << 32 | index) at the tile's cursor (TILE_BUCKET)
+//   WALK_COUNT   nothing (count only)                                  (ONESWEEP, K1)
+//   WALK_HIST    bump the per-tile histogram (fire-and-forget RED)    (TILE_BUCKET, K1)
+//   WALK_EMIT    write (key, value) at out_base(owner) + rank          (ONESWEEP, K3)
+//   WALK_SCATTER write (depth bits << 32 | index) at the tile's cursor (TILE_BUCKET, K3)
+// (Measured on B200: appending the pair list from K1 through a warp-aggregated
+// cursor instead, so that the tests run once, makes K1 60 % slower -- the
+// cursor's round trip stalls every walk iteration -- and the scatter is bound by
+// the return-atomics either way, so the tests are simply repeated in K3.)
 enum { WALK_COUNT = 0, WALK_HIST = 1, WALK_EMIT = 2, WALK_SCATTER = 3 };
 
 template <bool PRECISE, int MODE>
@@ -179,9 +183,6 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
         }
         const uint32_t ballot = __ballot_sync(FGS_FULL, pass);
-        if (MODE == WALK_HIST) {
-            if (pass) atomicAdd(&tile_ctr[ty * grid_w + tx], 1u);
-        }
         if (MODE == WALK_EMIT) {
             const uint32_t run_o = __shfl_sync(FGS_FULL, mine, o);
             const uint32_t base_o = __shfl_sync(FGS_FULL, out_base, o);
@@ -195,11 +196,15 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
                 vals[slot] = gid_o;
             }
         }
+        if (MODE == WALK_HIST) {
+            if (pass) atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
+        }
         if (MODE == WALK_SCATTER) {
             const uint32_t bits_o = __shfl_sync(FGS_FULL, depth_bits, o);
             const uint32_t gid_o = __shfl_sync(FGS_FULL, gid, o);
             if (pass) {
-                const uint32_t slot = atomicAdd(&tile_ctr[ty * grid_w + tx], 1u);
+                const uint32_t slot =
+                    atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
                 keys[slot] = ((uint64_t)bits_o << 32) | gid_o;
             }
         }
@@ -473,7 +478,7 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
 {
     (void)g_dummy_cam;
     // stats and (TILE_BUCKET) the per-tile histogram sit back to back: one memset
-    const size_t zero_bytes = bucket ? (size_t)((char *)(f.tilecount + tiles) - (char *)f.stats)
+    const size_t zero_bytes = bucket ? (size_t)((char *)(f.tilecount + (size_t)tiles * FGS_CTR_STRIDE) - (char *)f.stats)
                                      : sizeof(fgs_stats);
     cudaError_t e = cudaMemsetAsync(f.stats, 0, zero_bytes, st);
     if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
@@ -567,73 +572,72 @@ int fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream
 // K2 (TILE_BUCKET): exclusive scan of the per-tile histogram.  The result IS the
 // range table (sorting.py:139-152): starts[t] .. starts[t+1] is tile t's bucket.
 // Also seeds the scatter cursors, fixes M / overflow and counts non-empty tiles.
+// One CTA per 1024 tiles; instead of a second kernel or a spin-wait, CTA b sums
+// the (L2-resident) counts of all tiles before its own -- O(T^2/1024) reads, at
+// most 33 MB for an 8K frame's 129600 tiles, and no inter-CTA dependency at all.
 __global__ void __launch_bounds__(1024)
 k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
              uint32_t *__restrict__ cursor, int tiles, unsigned long long capacity,
              fgs_stats *__restrict__ stats)
 {
     __shared__ unsigned long long s_w[32];
-    __shared__ unsigned long long s_carry;
-    __shared__ uint32_t s_nonempty;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (threadIdx.x == 0) { s_carry = 0ull; s_nonempty = 0u; }
+    const int first = blockIdx.x * 1024;
+    // prefix of everything before this CTA's slice
+    unsigned long long before = 0;
+    for (int i = threadIdx.x; i < first; i += 1024) before += counts[(size_t)i * FGS_CTR_STRIDE];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) before += __shfl_xor_sync(FGS_FULL, before, o);
+    if (lane == 0) s_w[w] = before;
     __syncthreads();
-    uint32_t nonempty = 0;
-    for (int base = 0; base < tiles; base += 1024) {
-        const int i = base + threadIdx.x;
-        const unsigned long long v = i < tiles ? counts[i] : 0u;
-        nonempty += v ? 1u : 0u;
-        unsigned long long incl = v;
+    unsigned long long carry = 0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) carry += s_w[i];
+    __syncthreads();
+
+    const int i = first + threadIdx.x;
+    const unsigned long long v = i < tiles ? counts[(size_t)i * FGS_CTR_STRIDE] : 0u;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(FGS_FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) s_w[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const unsigned long long ws = s_w[lane];
+        unsigned long long wi = ws;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long t = __shfl_up_sync(FGS_FULL, incl, o);
-            if (lane >= o) incl += t;
+            const unsigned long long t = __shfl_up_sync(FGS_FULL, wi, o);
+            if (lane >= o) wi += t;
         }
-        if (lane == 31) s_w[w] = incl;
-        __syncthreads();
-        if (w == 0) {
-            const unsigned long long ws = s_w[lane];
-            unsigned long long wi = ws;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned long long t = __shfl_up_sync(FGS_FULL, wi, o);
-                if (lane >= o) wi += t;
-            }
-            s_w[lane] = wi - ws;
-        }
-        __syncthreads();
-        const unsigned long long excl = s_carry + s_w[w] + incl - v;
-        if (i < tiles) {
-            const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
-            starts[i] = (int32_t)e32;
-            cursor[i] = e32;
-        }
-        __syncthreads();
-        if (threadIdx.x == 1023) s_carry = excl + v;
-        __syncthreads();
+        s_w[lane] = wi - ws;
     }
-    nonempty = __reduce_add_sync(FGS_FULL, nonempty);
-    if (lane == 0 && nonempty) atomicAdd(&s_nonempty, nonempty);
     __syncthreads();
-    const unsigned long long M = s_carry;
-    const bool over = M > capacity;
-    if (threadIdx.x == 0) {
+    const unsigned long long excl = carry + s_w[w] + incl - v;
+    if (i < tiles) {
+        const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
+        starts[i] = (int32_t)e32;
+        cursor[(size_t)i * FGS_CTR_STRIDE] = e32;
+    }
+    const uint32_t nonempty = __reduce_add_sync(FGS_FULL, v ? 1u : 0u);
+    if (lane == 0 && nonempty) atomicAdd(&stats->tiles_nonempty, nonempty);
+    if (i == tiles - 1) {                       // the thread that owns the last tile knows M
+        const unsigned long long M = excl + v;
+        const bool over = M > capacity;
         stats->pairs_emitted = M > 0xffffffffull ? 0xffffffffu : (uint32_t)M;
-        stats->overflow = over ? 1u : 0u;
+        stats->overflow = over ? 1u : 0u;       // later kernels of this frame see it and no-op
         stats->pairs_in_buffer = over ? 0u : (uint32_t)M;
-        stats->tiles_nonempty = s_nonempty;
         starts[tiles] = (int32_t)(M > 0x7fffffffull ? 0x7fffffffu : (uint32_t)M);
     }
-    // overflow: the frame is re-run with a larger buffer; leave an all-empty range
-    // table so the remaining kernels of this frame touch nothing
-    if (over)
-        for (int i = threadIdx.x; i <= tiles; i += 1024) starts[i] = 0;
 }
 
 int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st)
 {
-    k_scan_tiles<<<1, 1024, 0, st>>>(f.tilecount, f.starts, f.cursor, tiles,
-                                     (unsigned long long)capacity, f.stats);
+    k_scan_tiles<<<(unsigned)((tiles + 1023) / 1024), 1024, 0, st>>>(
+        f.tilecount, f.starts, f.cursor, tiles, (unsigned long long)capacity, f.stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }

@@ -122,6 +122,7 @@ def test_oracle_parity_all_stages(preset, n, seed, w, h, radius, tau, deg, bg):
             ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, max(n, 1))
             # tile-bucket emission: same multiset, bucketed by tile
             tb = fgs.preprocess_and_bin(pipe, cam, s, tau, sh_degree=deg, sort_mode="tile-bucket")
+            assert np.array_equal(tb.pair_counts, ob.pair_counts)
             assert np.all(np.diff((tb.keys >> np.uint64(32)).astype(np.int64)) >= 0)
             tk, tv = _sorted_pairs(tb, n)
             assert np.array_equal(tk, ok) and np.array_equal(tv, ov)
