@@ -49,11 +49,12 @@ class FgsStats(C.Structure):
                 ("overflow", C.c_uint32), ("bad_depth", C.c_uint32),
                 ("unsorted", C.c_uint32), ("tile_out_of_grid", C.c_uint32),
                 ("candidate_tiles_lo", C.c_uint32), ("candidate_tiles_hi", C.c_uint32),
-                ("reserved", C.c_uint32 * 4)]
+                ("dense_tiles", C.c_uint32), ("medium_tiles", C.c_uint32),
+                ("hard_tiles", C.c_uint32), ("reserved", C.c_uint32 * 1)]
 
 
 STATS_DTYPE = np.dtype([(n, np.uint32) for n, _ in FgsStats._fields_[:-1]]
-                       + [("reserved", np.uint32, (4,))])
+                       + [("reserved", np.uint32, (1,))])
 assert STATS_DTYPE.itemsize == C.sizeof(FgsStats) == 64
 
 

@@ -27,6 +27,11 @@
 // per-tile atomic counters sit FGS_CTR_STRIDE words apart (one 32-byte sector each):
 // thousands of L2 atomics on neighbouring words of one line serialise
 #define FGS_CTR_STRIDE    8
+// tile-sort size classes: <= SMALL one CTA per tile; <= DENSE the medium list; beyond,
+// the dense list.  The lists live in spare words of the cursor slots: dense entry i
+// at cursor[i*FGS_CTR_STRIDE + 1], medium entry i at cursor[i*FGS_CTR_STRIDE + 2]
+#define FGS_SMALL_TILE    1024
+#define FGS_DENSE_TILE    4096
 
 // Camera as the kernels see it (passed by value: lives in the constant bank).
 struct CamDev {

@@ -621,6 +621,10 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
         const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
         starts[i] = (int32_t)e32;
         cursor[(size_t)i * FGS_CTR_STRIDE] = e32;
+        if (v > FGS_DENSE_TILE)     // queue the bucket for its tile-sort size class
+            cursor[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE + 1] = (uint32_t)i;
+        else if (v > FGS_SMALL_TILE)
+            cursor[(size_t)atomicAdd(&stats->medium_tiles, 1u) * FGS_CTR_STRIDE + 2] = (uint32_t)i;
     }
     const uint32_t nonempty = __reduce_add_sync(FGS_FULL, v ? 1u : 0u);
     if (lane == 0 && nonempty) atomicAdd(&stats->tiles_nonempty, nonempty);

@@ -247,29 +247,52 @@ k_tile_ranges(const uint64_t *__restrict__ keys, const uint32_t *__restrict__ n_
 // that 64-bit word, which is exactly the reference's (depth, then index) order
 // inside a tile (sorting.py:3-5).  Records are unique.
 //
-// Buckets of up to 4096 records: LSD radix sort on the four depth bytes, entirely
-// in shared memory (same stable warp-match ranking as k_sort_pass, local digit
-// offsets instead of a look-back), then equal-depth neighbours -- rare: two
-// Gaussians with the same float32 depth in one tile -- are put in index order by
-// an odd-even pass.  Larger buckets (very dense scenes) use a bitonic network in
-// its all-ascending form, long strides through L2 and the rest chunk-wise in
-// shared memory; every comparator moves the larger element up, so comparators
-// touching an index >= n are simply skipped and any n works without padding.
-constexpr int TS_THREADS = 256;
-constexpr int TS_CAP = 4096;
-constexpr int TS_E = TS_CAP / TS_THREADS;       // max records per thread
-
+// The sort is an LSD radix sort on the four depth bytes, entirely in shared
+// memory (same stable warp-match ranking as k_sort_pass, local digit offsets
+// instead of a look-back); equal-depth neighbours -- rare: two Gaussians with the
+// same float32 depth in one tile -- are then put in index order by an odd-even
+// pass.  This radix sort serves the dense buckets (> 4096 records, persistent CTAs
+// over the list k_scan_tiles collected) and the rare buckets the faster
+// bucket-rank sort below gives up on.  Buckets beyond 8192 first go through one counting
+// pass on their top 8 varying depth bits (through L2); consecutive bins are then
+// grouped into chunks of at most 8192 records, each sorted in shared memory.  A bitonic network (all-ascending form, so
+// comparators touching an index >= n are simply skipped) is the last resort for
+// pathological depth distributions.
+template <int NT, int EMAX>
 struct TileSortSmem {
-    uint64_t s[TS_CAP];
-    uint32_t whist[NW][BINS];
+    static constexpr int CAP = NT * EMAX;
+    static constexpr int WARPS = NT / 32;
+    uint64_t s[CAP];
+    uint32_t whist[WARPS][BINS];
     uint32_t texcl[256];
-    uint32_t scan[8];
+    uint32_t scan[32];
+    uint32_t sub[257];
+    uint32_t grp[258];
+    uint32_t mm[2];
+    uint32_t ngroups;
 };
 
+// Exclusive scan of one value per thread over the first 256 threads of an NT-thread
+// CTA (the other threads pass 0).  Two barriers.
+template <int NT>
+__device__ __forceinline__ uint32_t ts_scan256(uint32_t v, uint32_t *scratch)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t incl = warp_incl_scan(v, lane);
+    if (lane == 31 && w < 8) scratch[w] = incl;
+    __syncthreads();
+    uint32_t wsum = lane < 8 ? scratch[lane] : 0u;
+    uint32_t wincl = warp_incl_scan(wsum, lane);
+    uint32_t wbase = __shfl_sync(FGS_FULL, wincl - wsum, w & 7);
+    __syncthreads();
+    return wbase + incl - v;
+}
+
+template <int NT>
 __device__ __forceinline__ void ts_step_smem(uint64_t *s, int count, int mask, int hb)
 {
     // compare-exchange (i, i ^ mask) for every i < count with bit `hb` clear
-    for (int t = threadIdx.x; t < count / 2; t += TS_THREADS) {
+    for (int t = threadIdx.x; t < count / 2; t += NT) {
         const int i = ((t & ~(hb - 1)) << 1) | (t & (hb - 1));
         const int p = i ^ mask;
         const uint64_t a = s[i], b = s[p];
@@ -278,9 +301,10 @@ __device__ __forceinline__ void ts_step_smem(uint64_t *s, int count, int mask, i
     __syncthreads();
 }
 
+template <int NT>
 __device__ __forceinline__ void ts_step_global(uint64_t *g, int n, int npad, int mask, int hb)
 {
-    for (int t = threadIdx.x; t < npad / 2; t += TS_THREADS) {
+    for (int t = threadIdx.x; t < npad / 2; t += NT) {
         const int i = ((t & ~(hb - 1)) << 1) | (t & (hb - 1));
         const int p = i ^ mask;
         if (p < n) {
@@ -291,152 +315,429 @@ __device__ __forceinline__ void ts_step_global(uint64_t *g, int n, int npad, int
     __syncthreads();
 }
 
+template <int NT>
 __device__ __forceinline__ void ts_bitonic_smem(uint64_t *s, int npad)
 {
     for (int k = 2; k <= npad; k <<= 1) {
-        ts_step_smem(s, npad, k - 1, k >> 1);
-        for (int j = k >> 2; j > 0; j >>= 1) ts_step_smem(s, npad, j, j);
+        ts_step_smem<NT>(s, npad, k - 1, k >> 1);
+        for (int j = k >> 2; j > 0; j >>= 1) ts_step_smem<NT>(s, npad, j, j);
     }
 }
 
-__global__ void __launch_bounds__(TS_THREADS, 4)
-k_tile_sort(uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
-            uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts, int write_keys,
-            const fgs_stats *__restrict__ stats)
+// Sort m <= CAP records (src, global) ascending on (depth bits, index) into
+// S.s[0..m): `npass` LSD byte passes starting at record bit 32, then the
+// equal-depth fix-up.  Every thread of the CTA calls it with the same arguments.
+template <int NT, int EMAX>
+__device__ __forceinline__ void ts_sort_small(TileSortSmem<NT, EMAX> &S,
+                                              const uint64_t *__restrict__ src, int m, int npass)
 {
-    __shared__ TileSortSmem S;
-    if (stats->overflow) return;
-    const int tile = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int start = starts[tile], n = starts[tile + 1] - start;
-    if (n <= 0) return;
-    uint64_t *g = rec + start;
+    constexpr int TS_E = EMAX;
+    constexpr int WARPS = NT / 32;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint64_t *s = S.s;
-    const uint64_t tile_hi = (uint64_t)(uint32_t)tile << 32;
-
-    if (n <= TS_CAP) {
-        if (n > 1) {
-            // records spread evenly over the warps: E per thread, warp-striped
-            const int E = (n + TS_THREADS - 1) / TS_THREADS;
-            const int wbase = w * 32 * E;
-            uint64_t key[TS_E];
-            uint16_t rank[TS_E];
+    if (m <= 1) {
+        if (tid == 0 && m == 1) s[0] = src[0];
+        __syncthreads();
+        return;
+    }
+    // records spread evenly over the warps: E per thread, warp-striped
+    const int E = (m + NT - 1) / NT;
+    const int wbase = w * 32 * E;
+    uint64_t key[TS_E];
+    uint16_t rank[TS_E];
+#pragma unroll
+    for (int i = 0; i < TS_E; ++i) {
+        const int loc = wbase + i * 32 + lane;
+        key[i] = (i < E && loc < m) ? src[loc] : ~0ull;
+    }
+    if (npass == 0) {                      // nothing to sort on: just stage the records
+#pragma unroll
+        for (int i = 0; i < TS_E; ++i) {
+            const int loc = wbase + i * 32 + lane;
+            if (i < E && loc < m) s[loc] = key[i];
+        }
+        __syncthreads();
+    }
+    uint32_t *wh = S.whist[w];
+    for (int pass = 0; pass < npass; ++pass) {
+        const int shift = 32 + 8 * pass;
+        for (int i = tid; i < WARPS * BINS; i += NT) (&S.whist[0][0])[i] = 0u;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < TS_E; ++i) {
+            if (i < E) {                                  // uniform
+                const bool ok = wbase + i * 32 + lane < m;
+                const uint32_t d = ok ? (uint32_t)(key[i] >> shift) & 0xffu : 256u;
+                const uint32_t prev = wh[d];
+                __syncwarp();
+                const uint32_t peers = __match_any_sync(FGS_FULL, d);
+                const uint32_t before = __popc(peers & lanemask_lt());
+                if (before == 0) wh[d] = prev + __popc(peers);
+                __syncwarp();
+                rank[i] = (uint16_t)(prev + before);
+            }
+        }
+        __syncthreads();
+        uint32_t cnt = 0;
+        if (tid < 256) {
+#pragma unroll 8
+            for (int ww = 0; ww < WARPS; ++ww) {
+                const uint32_t c = S.whist[ww][tid];
+                S.whist[ww][tid] = cnt;
+                cnt += c;
+            }
+        }
+        const uint32_t ex = ts_scan256<NT>(cnt, S.scan);
+        if (tid < 256) S.texcl[tid] = ex;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < TS_E; ++i) {
+            if (i < E && wbase + i * 32 + lane < m) {
+                const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
+                s[S.texcl[d] + wh[d] + rank[i]] = key[i];
+            }
+        }
+        __syncthreads();
+        if (pass + 1 < npass) {
 #pragma unroll
             for (int i = 0; i < TS_E; ++i) {
                 const int loc = wbase + i * 32 + lane;
-                key[i] = (i < E && loc < n) ? g[loc] : ~0ull;
+                key[i] = (i < E && loc < m) ? s[loc] : ~0ull;
             }
-            uint32_t *wh = S.whist[w];
-            for (int pass = 0; pass < 4; ++pass) {
-                const int shift = 32 + 8 * pass;
-                for (int i = tid; i < NW * BINS; i += TS_THREADS) (&S.whist[0][0])[i] = 0u;
-                __syncthreads();
-#pragma unroll
-                for (int i = 0; i < TS_E; ++i) {
-                    if (i < E) {                                  // uniform
-                        const bool ok = wbase + i * 32 + lane < n;
-                        const uint32_t d = ok ? (uint32_t)(key[i] >> shift) & 0xffu : 256u;
-                        const uint32_t prev = wh[d];
-                        __syncwarp();
-                        const uint32_t peers = __match_any_sync(FGS_FULL, d);
-                        const uint32_t before = __popc(peers & lanemask_lt());
-                        if (before == 0) wh[d] = prev + __popc(peers);
-                        __syncwarp();
-                        rank[i] = (uint16_t)(prev + before);
-                    }
-                }
-                __syncthreads();
-                uint32_t cnt = 0;
-#pragma unroll
-                for (int ww = 0; ww < NW; ++ww) {
-                    const uint32_t c = S.whist[ww][tid];
-                    S.whist[ww][tid] = cnt;
-                    cnt += c;
-                }
-                uint32_t ttotal;
-                S.texcl[tid] = block_excl_scan_256(cnt, S.scan, ttotal);
-                __syncthreads();
-#pragma unroll
-                for (int i = 0; i < TS_E; ++i) {
-                    if (i < E && wbase + i * 32 + lane < n) {
-                        const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
-                        s[S.texcl[d] + wh[d] + rank[i]] = key[i];
-                    }
-                }
-                __syncthreads();
-                if (pass < 3) {
-#pragma unroll
-                    for (int i = 0; i < TS_E; ++i) {
-                        const int loc = wbase + i * 32 + lane;
-                        key[i] = (i < E && loc < n) ? s[loc] : ~0ull;
-                    }
-                }
-            }
-            // equal depths: order by index (low word).  Odd-even transposition over
-            // equal-depth neighbours; almost always zero or one round.
-            for (int round = 0;; ++round) {
-                bool swapped = false;
-                for (int t = tid; 2 * t + 1 < n; t += TS_THREADS) {
-                    const uint64_t a = s[2 * t], b = s[2 * t + 1];
-                    if ((a >> 32) == (b >> 32) && a > b) { s[2 * t] = b; s[2 * t + 1] = a; swapped = true; }
-                }
-                __syncthreads();
-                for (int t = tid; 2 * t + 2 < n; t += TS_THREADS) {
-                    const uint64_t a = s[2 * t + 1], b = s[2 * t + 2];
-                    if ((a >> 32) == (b >> 32) && a > b) { s[2 * t + 1] = b; s[2 * t + 2] = a; swapped = true; }
-                }
-                if (!__syncthreads_or(swapped)) break;
-                if (round == 6) {           // long runs of one depth: finish with the network
-                    int npad = 2;
-                    while (npad < n) npad <<= 1;
-                    for (int i = n + tid; i < npad; i += TS_THREADS) s[i] = ~0ull;
-                    __syncthreads();
-                    ts_bitonic_smem(s, npad);
-                    break;
-                }
-            }
-        } else {
-            if (tid == 0) s[0] = g[0];
-            __syncthreads();
         }
-        for (int i = tid; i < n; i += TS_THREADS) {
-            const uint64_t r = s[i];
-            vals_out[start + i] = (uint32_t)r;
-            if (write_keys) keys_out[start + i] = tile_hi | (r >> 32);
-        }
-        return;
     }
-
-    // large bucket: chunk-wise in shared memory, long strides through L2
-    int npad = TS_CAP;
-    while (npad < n) npad <<= 1;
-    const int nchunks = (n + TS_CAP - 1) / TS_CAP;
-    for (int c = 0; c < nchunks; ++c) {
-        const int cb = c * TS_CAP;
-        for (int i = tid; i < TS_CAP; i += TS_THREADS) s[i] = cb + i < n ? g[cb + i] : ~0ull;
+    // equal depths: order by index (low word).  Odd-even transposition over
+    // equal-depth neighbours; almost always zero or one round.
+    for (int round = 0;; ++round) {
+        bool swapped = false;
+        for (int t = tid; 2 * t + 1 < m; t += NT) {
+            const uint64_t a = s[2 * t], b = s[2 * t + 1];
+            if ((a >> 32) == (b >> 32) && a > b) { s[2 * t] = b; s[2 * t + 1] = a; swapped = true; }
+        }
         __syncthreads();
-        ts_bitonic_smem(s, TS_CAP);
-        for (int i = tid; i < TS_CAP; i += TS_THREADS)
+        for (int t = tid; 2 * t + 2 < m; t += NT) {
+            const uint64_t a = s[2 * t + 1], b = s[2 * t + 2];
+            if ((a >> 32) == (b >> 32) && a > b) { s[2 * t + 1] = b; s[2 * t + 2] = a; swapped = true; }
+        }
+        if (!__syncthreads_or(swapped)) break;
+        if (round == 6) {           // long runs of one depth: finish with the network
+            int npad = 2;
+            while (npad < m) npad <<= 1;
+            for (int i = m + tid; i < npad; i += NT) s[i] = ~0ull;
+            __syncthreads();
+            ts_bitonic_smem<NT>(s, npad);
+            break;
+        }
+    }
+}
+
+// Bitonic sort of an arbitrarily large segment in global memory (strides >= CAP
+// through L2, the rest chunk-wise in shared memory).  Last resort only.
+template <int NT, int EMAX>
+__device__ __noinline__ void ts_bitonic_global(TileSortSmem<NT, EMAX> &S, uint64_t *g, int n)
+{
+    constexpr int CAP = TileSortSmem<NT, EMAX>::CAP;
+    const int tid = threadIdx.x;
+    uint64_t *s = S.s;
+    int npad = CAP;
+    while (npad < n) npad <<= 1;
+    const int nchunks = (n + CAP - 1) / CAP;
+    for (int c = 0; c < nchunks; ++c) {
+        const int cb = c * CAP;
+        for (int i = tid; i < CAP; i += NT) s[i] = cb + i < n ? g[cb + i] : ~0ull;
+        __syncthreads();
+        ts_bitonic_smem<NT>(s, CAP);
+        for (int i = tid; i < CAP; i += NT)
             if (cb + i < n) g[cb + i] = s[i];
         __syncthreads();
     }
-    for (int k = 2 * TS_CAP; k <= npad; k <<= 1) {
-        ts_step_global(g, n, npad, k - 1, k >> 1);
+    for (int k = 2 * CAP; k <= npad; k <<= 1) {
+        ts_step_global<NT>(g, n, npad, k - 1, k >> 1);
         int j = k >> 2;
-        for (; j >= TS_CAP; j >>= 1) ts_step_global(g, n, npad, j, j);
+        for (; j >= CAP; j >>= 1) ts_step_global<NT>(g, n, npad, j, j);
         for (int c = 0; c < nchunks; ++c) {
-            const int cb = c * TS_CAP;
-            for (int i = tid; i < TS_CAP; i += TS_THREADS) s[i] = cb + i < n ? g[cb + i] : ~0ull;
+            const int cb = c * CAP;
+            for (int i = tid; i < CAP; i += NT) s[i] = cb + i < n ? g[cb + i] : ~0ull;
             __syncthreads();
-            for (int jj = TS_CAP >> 1; jj > 0; jj >>= 1) ts_step_smem(s, TS_CAP, jj, jj);
-            for (int i = tid; i < TS_CAP; i += TS_THREADS)
+            for (int jj = CAP >> 1; jj > 0; jj >>= 1) ts_step_smem<NT>(s, CAP, jj, jj);
+            for (int i = tid; i < CAP; i += NT)
                 if (cb + i < n) g[cb + i] = s[i];
             __syncthreads();
         }
     }
-    for (int i = tid; i < n; i += TS_THREADS) {
+}
+
+// One bucket.  Every thread of the CTA calls it with the same arguments.  With
+// SPLIT = false the caller guarantees n <= CAP (and the split code is not compiled
+// in, which keeps the hot kernel inside the instruction cache).
+template <int NT, int EMAX, bool SPLIT>
+__device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile,
+                                             uint64_t *__restrict__ rec,
+                                             uint64_t *__restrict__ alt, uint32_t *__restrict__ vals_out,
+                                             uint64_t *__restrict__ keys_out,
+                                             const int32_t *__restrict__ starts, int write_keys)
+{
+    constexpr int CAP = TileSortSmem<NT, EMAX>::CAP;
+    const int tid = threadIdx.x;
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    if (n <= 0) return;
+    uint64_t *g = rec + start;
+    uint64_t *a = alt + start;
+    uint64_t *s = S.s;
+    const uint64_t tile_hi = (uint64_t)(uint32_t)tile << 32;
+    const bool split = SPLIT && n > CAP;
+
+    if (split) {
+        // ---- bucket beyond the shared-memory capacity: one counting pass on the top 8
+        // varying depth bits into `alt` (through L2).  Bins are in depth order, so runs
+        // of consecutive bins are then grouped greedily into chunks of at most CAP
+        // records and each chunk is sorted in shared memory on all four depth bytes.
+        // keys_out may alias alt: a chunk is consumed before its slice is overwritten.
+        if (tid == 0) { S.mm[0] = 0xffffffffu; S.mm[1] = 0u; }
+        for (int i = tid; i < 257; i += NT) S.sub[i] = 0u;
+        __syncthreads();
+        uint32_t lo = 0xffffffffu, hi = 0u;
+        for (int i = tid; i < n; i += NT) {
+            const uint32_t d = (uint32_t)(g[i] >> 32);
+            lo = d < lo ? d : lo;
+            hi = d > hi ? d : hi;
+        }
+        lo = __reduce_min_sync(FGS_FULL, lo);
+        hi = __reduce_max_sync(FGS_FULL, hi);
+        if ((tid & 31) == 0) { atomicMin(&S.mm[0], lo); atomicMax(&S.mm[1], hi); }
+        __syncthreads();
+        const uint32_t diff = S.mm[0] ^ S.mm[1];
+        const int top = diff ? 31 - __clz((int)diff) : 0;   // highest varying depth bit
+        const int sh = top > 7 ? top - 7 : 0;                // bin = depth bits [sh, sh+8)
+        for (int i = tid; i < n; i += NT)
+            atomicAdd(&S.sub[1 + (((uint32_t)(g[i] >> 32) >> sh) & 0xffu)], 1u);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int d = 0; d <= 256; ++d) { run += S.sub[d]; S.sub[d] = run; }
+            uint32_t k = 0;
+            S.grp[0] = 0;
+            for (uint32_t d = 0; d < 256; ++d)
+                if (S.sub[d + 1] - S.sub[S.grp[k]] > (uint32_t)CAP && d > S.grp[k]) S.grp[++k] = d;
+            S.grp[++k] = 256;
+            S.ngroups = k;
+        }
+        __syncthreads();
+        if (tid < 256) S.texcl[tid] = S.sub[tid];            // scatter cursors
+        __syncthreads();
+        for (int i = tid; i < n; i += NT) {
+            const uint64_t r = g[i];
+            a[atomicAdd(&S.texcl[((uint32_t)(r >> 32) >> sh) & 0xffu], 1u)] = r;
+        }
+        __syncthreads();
+    }
+    const int ngroups = split ? (int)S.ngroups : 1;
+    const uint64_t *src = split ? a : g;
+    for (int k = 0; k < ngroups; ++k) {
+        const int b0 = split ? (int)S.sub[S.grp[k]] : 0;
+        const int m = split ? (int)S.sub[S.grp[k + 1]] - b0 : n;
+        if (m == 0) continue;                                 // uniform
+        if (!SPLIT || m <= CAP) {
+            ts_sort_small<NT, EMAX>(S, src + b0, m, 4);
+            for (int i = tid; i < m; i += NT) {
+                const uint64_t r = s[i];
+                vals_out[start + b0 + i] = (uint32_t)r;
+                if (write_keys) keys_out[start + b0 + i] = tile_hi | (r >> 32);
+            }
+        } else {                                              // one bin alone exceeds CAP
+            ts_bitonic_global<NT, EMAX>(S, a + b0, m);
+            for (int i = tid; i < m; i += NT) {
+                const uint64_t r = a[b0 + i];
+                vals_out[start + b0 + i] = (uint32_t)r;
+                if (write_keys) keys_out[start + b0 + i] = tile_hi | (r >> 32);
+            }
+        }
+        if (split) __syncthreads();
+    }
+}
+
+// ---- bucket-rank sort: the fast path for buckets of up to 4096 records -------------
+// Depths inside a tile are spread fairly evenly between the tile's nearest and
+// farthest splat, so a monotone linear map of the depth bits onto NB = CAP/4 bins
+// leaves a handful of records per bin.  One shared-memory atomic per record builds
+// the bin histogram (its return value is the record's slot inside the bin), a scan
+// turns it into bin offsets, the records are scattered bin-contiguously, and each
+// record then ranks itself inside its bin by comparing the full 64-bit word with
+// the bin's few other members -- which also settles equal depths by index.  Six
+// barriers per tile instead of twenty, no serial LDS -> match -> STS chains.
+// A tile where some bin holds more than TB_MAXBIN records (many equal or tightly
+// clustered depths) is pushed on the "hard" list and sorted by the radix kernel.
+constexpr int TB_MAXBIN = 64;
+
+template <int NT, int EMAX>
+struct BucketSmem {
+    static constexpr int CAP = NT * EMAX;
+    static constexpr int NB = CAP / 4;
+    uint64_t a[CAP];
+    uint64_t b[CAP];
+    uint32_t bin[NB + 1];
+    uint32_t red[64];
+};
+
+// Returns false (tile untouched) when the tile has to go to the radix fallback.
+template <int NT, int EMAX>
+__device__ __forceinline__ bool tb_sort_tile(BucketSmem<NT, EMAX> &S, int tile,
+                                             const uint64_t *__restrict__ rec,
+                                             uint32_t *__restrict__ vals_out,
+                                             uint64_t *__restrict__ keys_out,
+                                             const int32_t *__restrict__ starts, int write_keys)
+{
+    constexpr int NB = BucketSmem<NT, EMAX>::NB;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    const uint64_t *g = rec + start;
+    const uint64_t tile_hi = (uint64_t)(uint32_t)tile << 32;
+
+    // 1. stage the records, depth range of the tile
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = tid; i < n; i += NT) {
         const uint64_t r = g[i];
-        vals_out[start + i] = (uint32_t)r;
-        if (write_keys) keys_out[start + i] = tile_hi | (r >> 32);
+        S.a[i] = r;
+        const uint32_t d = (uint32_t)(r >> 32);
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+    }
+    for (int i = tid; i <= NB; i += NT) S.bin[i] = 0u;
+    lo = __reduce_min_sync(FGS_FULL, lo);
+    hi = __reduce_max_sync(FGS_FULL, hi);
+    if (lane == 0) { S.red[w] = lo; S.red[32 + w] = hi; }
+    __syncthreads();
+    lo = 0xffffffffu; hi = 0u;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+        lo = S.red[i] < lo ? S.red[i] : lo;
+        hi = S.red[32 + i] > hi ? S.red[32 + i] : hi;
+    }
+    const uint32_t range = hi - lo;
+    const bool direct = range < (uint32_t)NB;                 // one depth value per bin
+    const uint64_t inv = direct ? 0ull : ((uint64_t)NB << 32) / ((uint64_t)range + 1ull);
+#define TB_BIN(d) (direct ? (d) - lo : (uint32_t)(((uint64_t)((d) - lo) * inv) >> 32))
+
+    // 2. histogram; the atomic's return value is the record's slot inside its bin
+    uint16_t slot[EMAX];
+    bool too_big = false;
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const int i = tid + k * NT;
+        if (i < n) {
+            const uint32_t d = (uint32_t)(S.a[i] >> 32);
+            const uint32_t sl = atomicAdd(&S.bin[1 + TB_BIN(d)], 1u);
+            slot[k] = (uint16_t)sl;
+            too_big |= sl >= (uint32_t)TB_MAXBIN;
+        }
+    }
+    if (__syncthreads_or(too_big)) return false;
+
+    // 3. bin offsets: inclusive scan of bin[1..NB] in place (bin[0] = 0)
+    {
+        constexpr int PER = (NB + NT - 1) / NT;               // consecutive bins per thread
+        uint32_t v[PER], sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = 1 + tid * PER + k;
+            v[k] = idx <= NB ? S.bin[idx] : 0u;
+            sum += v[k];
+        }
+        uint32_t incl = warp_incl_scan(sum, lane);
+        if (lane == 31) S.red[w] = incl;
+        __syncthreads();
+        uint32_t wsum = lane < NT / 32 ? S.red[lane] : 0u;
+        uint32_t wincl = warp_incl_scan(wsum, lane);
+        uint32_t run = __shfl_sync(FGS_FULL, wincl - wsum, w) + incl - sum;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = 1 + tid * PER + k;
+            run += v[k];
+            if (idx <= NB) S.bin[idx] = run;
+        }
+    }
+    __syncthreads();
+
+    // 4. scatter bin-contiguously
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const int i = tid + k * NT;
+        if (i < n) {
+            const uint64_t r = S.a[i];
+            S.b[S.bin[TB_BIN((uint32_t)(r >> 32))] + slot[k]] = r;
+        }
+    }
+    __syncthreads();
+
+    // 5. rank inside the bin by full-word comparison; write straight to the output
+    for (int i = tid; i < n; i += NT) {
+        const uint64_t r = S.b[i];
+        const uint32_t bn = TB_BIN((uint32_t)(r >> 32));
+        const int b0 = (int)S.bin[bn], b1 = (int)S.bin[bn + 1];
+        int rank = 0;
+        for (int j = b0; j < b1; ++j) rank += S.b[j] < r ? 1 : 0;
+        vals_out[start + b0 + rank] = (uint32_t)r;
+        if (write_keys) keys_out[start + b0 + rank] = tile_hi | (r >> 32);
+    }
+#undef TB_BIN
+    return true;
+}
+
+// Size classes (k_scan_tiles sorts the tiles into them):
+//   small   n <= 1024   one CTA per tile, bucket-rank sort
+//   medium  n <= 4096   persistent CTAs over the medium list, bucket-rank sort
+//   hard    n <= 4096   tiles the bucket-rank sort gave up on: radix sort
+//   dense   n >  4096   512 threads, radix sort with 8192-record capacity, split beyond
+__global__ void __launch_bounds__(256, 6)
+k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
+            uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
+            uint32_t *__restrict__ hard_list, int write_keys, fgs_stats *__restrict__ stats)
+{
+    __shared__ BucketSmem<256, 4> S;
+    if (stats->overflow) return;
+    const int tile = blockIdx.x;
+    const int n = starts[tile + 1] - starts[tile];
+    if (n <= 0 || n > FGS_SMALL_TILE) return;
+    if (!tb_sort_tile<256, 4>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+        threadIdx.x == 0)
+        hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+}
+
+__global__ void __launch_bounds__(256, 3)
+k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
+                   uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
+                   const uint32_t *__restrict__ list, uint32_t *__restrict__ hard_list,
+                   int write_keys, fgs_stats *__restrict__ stats)
+{
+    extern __shared__ __align__(16) unsigned char ts_raw[];
+    BucketSmem<256, 16> &S = *reinterpret_cast<BucketSmem<256, 16> *>(ts_raw);
+    if (stats->overflow) return;
+    const uint32_t count = stats->medium_tiles;
+    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
+        if (!tb_sort_tile<256, 16>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+            threadIdx.x == 0)
+            hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+        __syncthreads();
+    }
+}
+
+template <int NT, int EMAX, bool SPLIT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+k_tile_sort_list(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
+                 uint32_t *__restrict__ vals_out, uint64_t *__restrict__ keys_out,
+                 const int32_t *__restrict__ starts, const uint32_t *__restrict__ list,
+                 const uint32_t *__restrict__ list_len, int write_keys,
+                 const fgs_stats *__restrict__ stats)
+{
+    extern __shared__ __align__(16) unsigned char ts_raw[];
+    TileSortSmem<NT, EMAX> &S = *reinterpret_cast<TileSortSmem<NT, EMAX> *>(ts_raw);
+    if (stats->overflow) return;
+    const uint32_t count = *list_len;
+    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+        ts_sort_tile<NT, EMAX, SPLIT>(S, (int)list[(size_t)i * FGS_CTR_STRIDE], rec, alt, vals_out,
+                                      keys_out, starts, write_keys);
+        __syncthreads();
     }
 }
 
@@ -445,8 +746,53 @@ k_tile_sort(uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
 int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st)
 {
     if (tiles <= 0) return FGS_OK;
-    k_tile_sort<<<(unsigned)tiles, TS_THREADS, 0, st>>>(f.keys[0], f.vals[0], f.keys[1], f.starts,
-                                                        write_keys, f.stats);
+    auto hard = k_tile_sort_list<256, 16, false, 3>;
+    auto dense = k_tile_sort_list<512, 16, true, 2>;
+    using MediumSmem = BucketSmem<256, 16>;
+    using HardSmem = TileSortSmem<256, 16>;
+    using DenseSmem = TileSortSmem<512, 16>;
+    static_assert(BucketSmem<256, 4>::CAP == FGS_SMALL_TILE, "small class = small capacity");
+    static_assert(MediumSmem::CAP == FGS_DENSE_TILE && HardSmem::CAP == FGS_DENSE_TILE,
+                  "dense threshold = medium capacity");
+    static bool attr_set = false;
+    static int sms = 148;
+    if (!attr_set) {
+        cudaError_t e = cudaSuccess;
+        auto prep = [&](const void *fn, size_t smem) {
+            if (e == cudaSuccess && smem)
+                e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            // largest shared-memory carve-out, or the occupancy the launch bounds assume
+            // (6 x 17 KB, 3 x 69 KB, 3 x 43 KB, 2 x 83 KB per SM) is not reached
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         cudaSharedmemCarveoutMaxShared);
+        };
+        prep((const void *)k_tile_sort, 0);
+        prep((const void *)k_tile_sort_medium, sizeof(MediumSmem));
+        prep((const void *)hard, sizeof(HardSmem));
+        prep((const void *)dense, sizeof(DenseSmem));
+        if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        attr_set = true;
+    }
+    // lists in the spare words of the cursor slots: +1 dense, +2 medium, +3 hard
+    uint32_t *dense_list = f.cursor + 1, *medium_list = f.cursor + 2, *hard_list = f.cursor + 3;
+    k_tile_sort<<<(unsigned)tiles, 256, 0, st>>>(f.keys[0], f.vals[0], f.keys[1], f.starts,
+                                                 hard_list, write_keys, f.stats);
+    FGS_AFTER_LAUNCH(st);
+    const unsigned mgrid = (unsigned)(tiles < 3 * sms ? tiles : 3 * sms);
+    k_tile_sort_medium<<<mgrid, 256, sizeof(MediumSmem), st>>>(
+        f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
+    FGS_AFTER_LAUNCH(st);
+    const unsigned dgrid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);
+    dense<<<dgrid, 512, sizeof(DenseSmem), st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
+                                                 f.starts, dense_list, &f.stats->dense_tiles,
+                                                 write_keys, f.stats);
+    FGS_AFTER_LAUNCH(st);
+    hard<<<mgrid, 256, sizeof(HardSmem), st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1], f.starts,
+                                               hard_list, &f.stats->hard_tiles, write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
@@ -482,6 +828,9 @@ int fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev,
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sizeof(SortSmem));
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                     cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         attr_set = true;
     }

@@ -176,6 +176,29 @@ def test_sorted_buffer_matches_oracle_order(mode, n, w, h, radius):
         (ost["pairs_emitted"], ost["tiles_nonempty"], ost["pairs_contributing"])
 
 
+@pytest.mark.parametrize("n", [3000, 30000])
+def test_equal_depth_ties_order_by_index(n):
+    """Every Gaussian at the same camera depth: inside a tile the order is decided by
+    the index tie-break alone (sorting.py:3-5, test_sorting.py:55-60).  3000 exercises
+    the shared-memory tie fix-up, 30000 (buckets > 4096 with a single depth value)
+    the large-bucket fallback."""
+    rng = np.random.default_rng(n)
+    cam = identity_camera(32, 32, focal=16)
+    z = 10.0
+    xy = rng.uniform(-0.95, 0.95, size=(n, 2)) * z
+    scene = make_raw_scene(np.concatenate([xy, np.full((n, 1), z)], axis=1),
+                           rng.uniform(0.05, 0.4, size=(n, 3)), rng.uniform(0.1, 0.9, size=n),
+                           dc=rng.uniform(-1, 1, size=(n, 3)))
+    act = fgs.activate(scene)
+    ob = orc.preprocess_and_bin(act, cam)
+    assert np.unique(ob.depth[ob.retained]).size == 1
+    ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, n)
+    for mode in ("tile-bucket", "onesweep"):
+        keys, vals, starts = fgs.sorted_pairs(fgs.Pipeline(act, sort_mode=mode), cam)
+        assert np.array_equal(keys, ok) and np.array_equal(vals, ov), mode
+        assert np.array_equal(starts, orc.tile_range_table(ok, ob.grid_w, ob.grid_h))
+
+
 def test_both_sort_modes_give_identical_frames():
     act = fgs.activate(fgs.gen_synthetic("elongated", 40000, 3))
     for cam in fgs.orbit_cameras(2, 14.0, 640, 360):
