@@ -111,6 +111,9 @@ typedef struct fgs_layout {
     uint64_t off_rects;        /* uint16 [P][4]   inclusive tx0,ty0,tx1,ty1   */
     uint64_t off_flags;        /* uint8  [P]      bit0 retained, bit1 degen.  */
     uint64_t off_counts;       /* uint32 [P]      emitted pairs per Gaussian  */
+    uint64_t off_passmask;     /* uint64 [P]      bit j = candidate tile j (row-major in
+                                  the banded rect) passed; valid when the
+                                  Gaussian has <= 64 candidates              */
     uint64_t off_blocksums;    /* uint32 [2][nblocks]  sums, exclusive bases  */
     uint64_t off_keys[2];      /* uint64 [capacity]   ping / pong             */
     uint64_t off_vals[2];      /* uint32 [capacity]                           */

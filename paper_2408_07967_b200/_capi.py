@@ -62,6 +62,7 @@ class FgsLayout(C.Structure):
     _fields_ = [("total_bytes", C.c_uint64), ("off_splat", C.c_uint64),
                 ("off_depth", C.c_uint64), ("off_rects", C.c_uint64),
                 ("off_flags", C.c_uint64), ("off_counts", C.c_uint64),
+                ("off_passmask", C.c_uint64),
                 ("off_blocksums", C.c_uint64), ("off_keys", C.c_uint64 * 2),
                 ("off_vals", C.c_uint64 * 2), ("off_sortstate", C.c_uint64),
                 ("off_hist", C.c_uint64), ("off_starts", C.c_uint64),

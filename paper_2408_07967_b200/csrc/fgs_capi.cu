@@ -146,6 +146,7 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     L->off_rects = take(p * 8);
     L->off_flags = take(p);
     L->off_counts = take(p * 4);
+    L->off_passmask = take(p * 8);
     L->off_blocksums = take((uint64_t)L->preprocess_blocks * 8 + 8);
     L->off_keys[0] = take(cap * 8);
     L->off_keys[1] = take(cap * 8);

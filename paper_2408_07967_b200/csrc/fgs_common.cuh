@@ -73,6 +73,7 @@ struct FrameDev {
     ushort4  *rects;
     uint8_t  *flags;
     uint32_t *counts;
+    uint64_t *passmask;     // [P]
     uint32_t *blocksums;    // [nblocks]
     uint32_t *blockbase;    // [nblocks]
     uint64_t *keys[2];
@@ -96,6 +97,7 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.rects = (ushort4 *)(b + L->off_rects);
     f.flags = (uint8_t *)(b + L->off_flags);
     f.counts = (uint32_t *)(b + L->off_counts);
+    f.passmask = (uint64_t *)(b + L->off_passmask);
     f.blocksums = (uint32_t *)(b + L->off_blocksums);
     f.blockbase = f.blocksums + L->preprocess_blocks;
     f.keys[0] = (uint64_t *)(b + L->off_keys[0]);

@@ -127,7 +127,9 @@ struct TileJob {
     uint32_t cand;              // candidate tiles (0 = lane idle)
     float cx, cy, a, b, c, keff;
     int tx0, ty0, nx;
+    uint64_t mask;              // K3: pass bits recorded by K1 (cand <= FGS_MASK_CAND)
 };
+#define FGS_MASK_CAND 64
 
 // Walk the warp's candidate tiles 32 at a time.  Returns this lane's number of
 // passing tiles.  MODE selects what happens to a passing (tile, Gaussian):
@@ -141,19 +143,27 @@ struct TileJob {
 // the return-atomics either way, so the tests are simply repeated in K3.)
 enum { WALK_COUNT = 0, WALK_HIST = 1, WALK_EMIT = 2, WALK_SCATTER = 3 };
 
+// The count walks (K1) also return, in `mask_out`, the pass bits of this lane's first 64
+// candidates; the emit walks (K3) take them back through job.mask and only re-run the
+// exact test for the rare Gaussian with more candidates than that.
 template <bool PRECISE, int MODE>
 __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int width, int height,
                                                     int grid_w, uint32_t out_base,
                                                     uint32_t depth_bits, uint32_t gid,
                                                     uint64_t *__restrict__ keys,
                                                     uint32_t *__restrict__ vals,
-                                                    uint32_t *__restrict__ tile_ctr)
+                                                    uint32_t *__restrict__ tile_ctr,
+                                                    uint64_t *mask_out = nullptr)
 {
+    constexpr bool COUNTING = (MODE == WALK_COUNT || MODE == WALK_HIST);
     const int lane = threadIdx.x & 31;
     const uint32_t incl = warp_incl_scan(job.cand, lane);
     const uint32_t total = __shfl_sync(FGS_FULL, incl, 31);
     const uint32_t excl = incl - job.cand;
     uint32_t mine = 0;
+    uint64_t mymask = 0;
+    // K3: does any lane of this warp need the exact test again?
+    const bool any_big = !COUNTING && PRECISE && __any_sync(FGS_FULL, job.cand > FGS_MASK_CAND);
     for (uint32_t base = 0; base < total; base += 32) {
         const uint32_t j = base + lane;
         // owner = first lane whose inclusive prefix exceeds j
@@ -173,14 +183,27 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
         const int ry = (int)(local / (uint32_t)(nx > 0 ? nx : 1));
         const int tx = tx0 + (int)local - ry * nx, ty = ty0 + ry;
         bool pass = act;
-        if (PRECISE) {
+        if (PRECISE && !COUNTING) {
+            // recorded bits of the owner (valid when it has <= 64 candidates)
+            const uint32_t mlo = __shfl_sync(FGS_FULL, (uint32_t)job.mask, o);
+            const uint32_t mhi = __shfl_sync(FGS_FULL, (uint32_t)(job.mask >> 32), o);
+            const uint32_t word = local < 32u ? mlo : mhi;
+            pass = act && ((word >> (local & 31u)) & 1u);
+        }
+        if (PRECISE && (COUNTING || any_big)) {
             const float cx = __shfl_sync(FGS_FULL, job.cx, o);
             const float cy = __shfl_sync(FGS_FULL, job.cy, o);
             const float a = __shfl_sync(FGS_FULL, job.a, o);
             const float b = __shfl_sync(FGS_FULL, job.b, o);
             const float c = __shfl_sync(FGS_FULL, job.c, o);
             const float ke = __shfl_sync(FGS_FULL, job.keff, o);
-            pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
+            if (COUNTING) {
+                pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
+            } else {
+                const uint32_t cand_o = __shfl_sync(FGS_FULL, job.cand, o);
+                if (cand_o > FGS_MASK_CAND)
+                    pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
+            }
         }
         const uint32_t ballot = __ballot_sync(FGS_FULL, pass);
         if (MODE == WALK_EMIT) {
@@ -214,8 +237,14 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
         if (job.cand && incl > base && lo < hi) {
             const uint32_t m = (hi - lo == 32) ? FGS_FULL : (((1u << (hi - lo)) - 1u) << lo);
             mine += __popc(ballot & m);
+            if (COUNTING) {
+                // my candidates in this window start at my local index base + lo - excl
+                const uint32_t first = base + (uint32_t)lo - excl;
+                if (first < 64u) mymask |= (uint64_t)((ballot & m) >> lo) << first;
+            }
         }
     }
+    if (COUNTING && mask_out) *mask_out = mymask;
     return mine;
 }
 
@@ -268,6 +297,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     job.cx = job.cy = job.a = job.b = job.c = job.keff = 0.f;
     job.tx0 = job.ty0 = 0;
     job.nx = 1;
+    job.mask = 0;
     bool retained = false, degenerate = false;
     uint32_t full_cand = 0;
 
@@ -436,15 +466,20 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     }
 
     uint32_t npairs;
+    uint64_t passmask = 0;
     if (BUCKET)
         npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_HIST>(
-            job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, f.tilecount);
+            job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, f.tilecount,
+            &passmask);
     else if (STRAT == FGS_PRECISE)
         npairs = warp_walk_tiles<true, WALK_COUNT>(job, cam.width, cam.height, cam.grid_w, 0, 0, 0,
-                                                   nullptr, nullptr, nullptr);
+                                                   nullptr, nullptr, nullptr, &passmask);
     else
         npairs = job.cand;
-    if (live) f.counts[g] = npairs;
+    if (live) {
+        f.counts[g] = npairs;
+        if (STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
+    }
 
     // block totals: pairs (-> blocksums), retained / degenerate / candidates (-> stats)
     uint32_t v0 = npairs, v1 = (retained ? 1u : 0u) | ((degenerate ? 1u : 0u) << 16), v2 = full_cand;
@@ -671,22 +706,29 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
     job.cx = job.cy = job.a = job.b = job.c = job.keff = 0.f;
     job.tx0 = job.ty0 = 0;
     job.nx = 1;
+    job.mask = 0;
     uint32_t bits = 0;
     if (cnt) {
         const ushort4 r = f.rects[g];
-        const float4 *row = (const float4 *)(f.splat + (size_t)g * 12);
-        const float4 r0 = row[0], r1 = row[1], r2 = row[2];
-        const float k = r1.z, hx = r2.z, hy = r2.w;
-        // binning.py:187-193 conservative cutoff for the exact test
-        const float ex = fa(hx, 16.0f), ey = fa(hy, 16.0f);
-        const float term = fa(fa(fm(fm(r0.z, ex), ex), fm(fm(fm(2.0f, fabsf(r0.w)), ex), ey)),
-                              fm(fm(r1.x, ey), ey));
-        job.keff = fa(k, fm(FGS_CUTOFF_SLACK, term));
-        job.cx = r0.x; job.cy = r0.y; job.a = r0.z; job.b = r0.w; job.c = r1.x;
         const int by0 = (int)r.y > band0 ? (int)r.y : band0;
         const int by1 = (int)r.w < band1 ? (int)r.w : band1;
         job.tx0 = r.x; job.ty0 = by0; job.nx = (int)r.z - (int)r.x + 1;
         job.cand = (uint32_t)job.nx * (uint32_t)(by1 - by0 + 1);
+        if (STRAT == FGS_PRECISE) {
+            if (job.cand <= FGS_MASK_CAND) {
+                job.mask = f.passmask[g];                 // K1's verdicts, no test needed
+            } else {
+                const float4 *row = (const float4 *)(f.splat + (size_t)g * 12);
+                const float4 r0 = row[0], r1 = row[1], r2 = row[2];
+                const float k = r1.z, hx = r2.z, hy = r2.w;
+                // binning.py:187-193 conservative cutoff for the exact test
+                const float ex = fa(hx, 16.0f), ey = fa(hy, 16.0f);
+                const float term = fa(fa(fm(fm(r0.z, ex), ex), fm(fm(fm(2.0f, fabsf(r0.w)), ex), ey)),
+                                      fm(fm(r1.x, ey), ey));
+                job.keff = fa(k, fm(FGS_CUTOFF_SLACK, term));
+                job.cx = r0.x; job.cy = r0.y; job.a = r0.z; job.b = r0.w; job.c = r1.x;
+            }
+        }
         const float d = f.depth[g];
         bits = __float_as_uint(d);
         // binning.py:50-51: depths must be positive and finite

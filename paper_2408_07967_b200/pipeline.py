@@ -108,6 +108,17 @@ def _stream_ptr(torch, device):
     return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
+def _fill_counters(stats, s):
+    """Device fgs_stats record -> the reference's FrameStats counters (pipeline.py:103-110)."""
+    stats.pairs_emitted = int(s["pairs_emitted"])
+    stats.pairs_contributing = int(s["pairs_contributing"])
+    stats.gaussians_retained = int(s["gaussians_retained"])
+    stats.gaussians_degenerate = int(s["gaussians_degenerate"])
+    stats.tiles_nonempty = int(s["tiles_nonempty"])
+    stats.pair_buffer_bytes = 12 * stats.pairs_emitted
+    stats.candidate_tiles = int(s["candidate_tiles_lo"]) | (int(s["candidate_tiles_hi"]) << 32)
+
+
 class _PinnedPool:
     """Recycles pinned host frames: a frame handed to the caller returns to the
     pool when the caller's ndarray is garbage-collected."""
@@ -353,13 +364,7 @@ class Pipeline:
                 stats.sort_ns = int(ev[1].elapsed_time(ev[2]) * 1e6)
                 stats.render_ns = int(ev[2].elapsed_time(ev[3]) * 1e6)
                 stats.total_ns = int(ev[0].elapsed_time(ev[3]) * 1e6)
-            stats.pairs_emitted = int(s["pairs_emitted"])
-            stats.pairs_contributing = int(s["pairs_contributing"])
-            stats.gaussians_retained = int(s["gaussians_retained"])
-            stats.gaussians_degenerate = int(s["gaussians_degenerate"])
-            stats.tiles_nonempty = int(s["tiles_nonempty"])
-            stats.pair_buffer_bytes = 12 * stats.pairs_emitted
-            stats.candidate_tiles = int(s["candidate_tiles_lo"]) | (int(s["candidate_tiles_hi"]) << 32)
+            _fill_counters(stats, s)
             self._last_pairs = max(self._last_pairs, stats.pairs_emitted)
             if as_numpy:
                 fb = Framebuffer(_pinned.as_numpy(h_rgb), bg)
@@ -372,6 +377,79 @@ class Pipeline:
             self._give_ws(ws)
         stats.e2e_ns = time.perf_counter_ns() - t_host0
         return fb, stats
+
+    def render_many(self, cameras, strategy="precise", tau=TAU_DEFAULT,
+                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=2):
+        """``list(render_iter(...))``: every view's ``(Framebuffer, FrameStats)``."""
+        return list(self.render_iter(cameras, strategy, tau, background, exact=exact,
+                                     contrib=contrib, depth=depth))
+
+    def render_iter(self, cameras, strategy="precise", tau=TAU_DEFAULT,
+                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=2):
+        """Throughput path for a batch of views (BASELINE config 5; the reference's
+        ``bench_frames`` loop, ``pipeline.py:212-233``): same frames and stats as calling
+        ``render`` per camera, but frame i's device->host copy runs on a copy stream
+        while the kernels of frame i+1 execute, and each frame is one C-ABI call
+        (``fgs_render``).  ``depth`` frames are in flight at most.  Yields
+        ``(Framebuffer, FrameStats)`` in camera order; host frames are pinned buffers
+        that return to a pool when the caller drops them."""
+        torch = _torch()
+        from collections import deque
+        sid = _strategy_id(strategy)
+        deg = _check_sh_degree(self.sh_degree)
+        L = _capi.lib()
+        bg = np.asarray(background, dtype=np.float32).reshape(3)
+        bg_c = (C.c_float * 3)(*bg.tolist())
+        flags = (_capi.BLEND_EXACT if exact else 0) | (_capi.BLEND_CONTRIB if contrib else 0)
+        inflight = deque()
+
+        def finish(job):
+            cam_obj, ws, h_rgb, done, t0 = job
+            done.synchronize()
+            s = np.frombuffer(ws.h_stats.numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+            self._give_ws(ws)
+            if int(s["overflow"]) or int(s["bad_depth"]):
+                _pinned.give(h_rgb)          # grow-and-rerun / raise through the plain path
+                return self.render(cam_obj, strategy, tau, background, exact=exact,
+                                   contrib=contrib, timing=False)
+            st = FrameStats(strategy=strategy, tau=float(tau), workers=1)
+            _fill_counters(st, s)
+            self._last_pairs = max(self._last_pairs, st.pairs_emitted)
+            st.e2e_ns = time.perf_counter_ns() - t0
+            return Framebuffer(_pinned.as_numpy(h_rgb), bg), st
+
+        with torch.cuda.device(self.device):
+            compute = torch.cuda.current_stream(self.device)
+            if getattr(self, "_copy_stream", None) is None:
+                self._copy_stream = torch.cuda.Stream(device=self.device)
+            copy = self._copy_stream
+            kcut = self._cutoffs(torch, tau)
+            for cam_obj in cameras:
+                while len(inflight) >= max(1, int(depth)):
+                    yield finish(inflight.popleft())
+                t0 = time.perf_counter_ns()
+                cam = _capi.camera_struct(cam_obj)
+                W, H = int(cam_obj.width), int(cam_obj.height)
+                gh = -(-H // TILE_SIZE)
+                ws = self._take_ws(torch, W, H, self._default_capacity())
+                ws.set_mode(_capi.SORT_MODES[self.sort_mode])
+                _capi.check(L.fgs_render(self.packed.data_ptr(), kcut.data_ptr(), self.count,
+                                         C.byref(cam), float(tau), deg, sid, bg_c, flags, 0, gh - 1,
+                                         ws.next_epoch(), ws.rgb.data_ptr(), None, None,
+                                         C.c_void_p(ws.base), C.byref(ws.lay),
+                                         C.c_void_p(compute.cuda_stream)))
+                ready = torch.cuda.Event()
+                ready.record(compute)
+                copy.wait_event(ready)
+                h_rgb = _pinned.take(torch, (H, W, 3), torch.float32)
+                with torch.cuda.stream(copy):
+                    h_rgb.copy_(ws.rgb, non_blocking=True)
+                    ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
+                    done = torch.cuda.Event()
+                    done.record(copy)
+                inflight.append((cam_obj, ws, h_rgb, done, t0))
+            while inflight:
+                yield finish(inflight.popleft())
 
 
 def sorted_pairs(pipe, camera, strategy="precise", tau=TAU_DEFAULT, band=None):
