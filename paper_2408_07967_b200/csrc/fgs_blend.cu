@@ -174,26 +174,30 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
             while (live) {
                 const int j = c0 + __ffs(live) - 1;
                 live &= live - 1;
+                // Straight-line body: a lane the reference would skip (render.py:211, 214,
+                // 219) carries alpha = 0 through the blend, which leaves C and T bit-for-bit
+                // unchanged.  With 18-28 of 32 lanes live per surviving pair, early-out
+                // branches almost never skip work but cost reconvergence bookkeeping.
                 const float4 r0 = S.row[cur][j][0];
+                const float4 r1 = S.row[cur][j][1];
                 const float4 r2 = S.row[cur][j][2];
                 const float dx = fs(fx, r0.x), dy = fs(fy, r0.y);
-                // render.py:211 extent rectangle, exact float32 compares
-                if (fabsf(dx) > r2.z || fabsf(dy) > r2.w) continue;
-                const float4 r1 = S.row[cur][j][1];
                 // render.py:213  s = 0.5*(a dx dx + c dy dy) + b dx dy, unfused
                 const float s = fa(fm(0.5f, fa(fm(fm(r0.z, dx), dx), fm(fm(r1.x, dy), dy))),
                                    fm(fm(r0.w, dx), dy));
-                if (s > fm(0.5f, r1.z)) continue;                 // render.py:214
+                // render.py:211 extent rectangle (exact float32 compares), :214 cutoff
+                bool on = !(fabsf(dx) > r2.z) && !(fabsf(dy) > r2.w) && !(s > fm(0.5f, r1.z));
                 float al;
                 if (EXACT) {
-                    al = fm(r1.y, expf_exact(-s, S.tab));
+                    al = on ? fm(r1.y, expf_exact(-s, S.tab)) : 0.0f;
                 } else {
                     al = r1.y * ex2_approx(-s * 1.4426950408889634f);
-                    if (__float_as_uint(al) - band_lo <= band_span)
+                    if (on && __float_as_uint(al) - band_lo <= band_span)
                         al = fm(r1.y, expf_exact(-s, S.tab));
                 }
                 al = al > FGS_ALPHA_CAP ? FGS_ALPHA_CAP : al;     // render.py:217-218
-                if (al < tau) continue;                           // render.py:219
+                on = on && !(al < tau);                           // render.py:219
+                al = on ? al : 0.0f;
                 if (EXACT) {
                     const float wgt = fm(al, T);
                     cr = fa(cr, fm(r1.w, wgt));
@@ -209,7 +213,7 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                     if (EXTRAS) dz = fmaf(S.z[cur][j], wgt, dz);
                     T = T * (1.0f - al);
                 }
-                if (CONTRIB) S.touched[cur][j] = 1u;
+                if (CONTRIB && on) S.touched[cur][j] = 1u;
                 if (T < FGS_T_STOP) fx = kInf;                    // render.py:228
             }
         }
