@@ -11,13 +11,15 @@ from .pipeline import (BinOutput, Framebuffer, FrameStats, Pipeline, STRATEGIES,
                        TAU_DEFAULT, TILE_SIZE, UnsortedPairsError, max_abs_diff,
                        power_cutoffs, preprocess_and_bin, psnr, render_frame,
                        run_frame, sort_pairs, sorted_pairs, tile_range_table)
+from .reports import REPORT_SCHEMA_VERSION, CompareReport, bench_frames, compare_modes
 from .scene import (ActivatedScene, Camera, CameraValidationError, Scene, activate,
                     gen_synthetic, look_at_camera, make_camera, orbit_cameras)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ActivatedScene", "BinOutput", "Camera", "CameraValidationError", "Framebuffer",
+    "ActivatedScene", "BinOutput", "Camera", "CameraValidationError", "CompareReport",
+    "Framebuffer", "REPORT_SCHEMA_VERSION", "bench_frames", "compare_modes",
     "FrameStats", "Pipeline", "STRATEGIES", "Scene", "TAU_DEFAULT", "TILE_SIZE",
     "UnsortedPairsError", "activate", "gen_synthetic", "look_at_camera", "make_camera",
     "max_abs_diff", "orbit_cameras", "power_cutoffs", "preprocess_and_bin", "psnr",

@@ -375,3 +375,56 @@ def test_row_bands_equal_full_frame():
         total += s.pairs_emitted
     assert np.array_equal(out, full.image)
     assert total == st.pairs_emitted
+
+
+# ---------------------------------------------------------------------------
+# report emitters (reference pipeline.py:171-269, docs/report-schema.md)
+# ---------------------------------------------------------------------------
+def test_compare_modes_report_matches_oracle_counters():
+    act = fgs.activate(fgs.gen_synthetic("elongated", 4000, 5))
+    cams = fgs.orbit_cameras(2, 14.0, 256, 192)
+    rep = fgs.compare_modes(act, cams).to_dict()
+    assert rep["schema_version"] == 1 and rep["kind"] == "compare"
+    assert rep["strategies"] == list(STRATS) and len(rep["frames"]) == 2
+    for fr, cam in zip(rep["frames"], cams):
+        assert fr["frame_id"] == cam.cam_id
+        for s in STRATS:
+            _, ost = orc.render(act, cam, s)
+            got = fr["stats"][s]
+            for k in ("pairs_emitted", "pairs_contributing", "gaussians_retained",
+                      "gaussians_degenerate", "tiles_nonempty"):
+                assert got[k] == ost[k], (s, k)
+            assert got["pair_buffer_bytes"] == 12 * got["pairs_emitted"]
+            assert set(got) == {"strategy", "tau", "workers", "preprocess_bin_ns", "sort_ns",
+                                "render_ns", "total_ns", "pairs_emitted", "pairs_contributing",
+                                "gaussians_retained", "gaussians_degenerate", "tiles_nonempty",
+                                "pair_buffer_bytes", "buffer_regrows"}
+        # the shared tau rule makes every strategy render the same frame (render.py:17-22)
+        for a in STRATS:
+            for b in STRATS:
+                assert fr["psnr"][f"{a}|{b}"] == "identical"
+                assert fr["max_abs_diff"][f"{a}|{b}"] == 0.0
+        r = fr["pairs_emitted_ratio_vs_first"]
+        assert r["precise"] == 1.0 and r["precise"] <= r["tight-aabb"] <= r["baseline-circle-aabb"]
+    agg = rep["aggregate"]
+    assert agg["precise"]["frames"] == 2
+    assert agg["precise"]["pairs_emitted_total"] == sum(
+        f["stats"]["precise"]["pairs_emitted"] for f in rep["frames"])
+    with pytest.raises(ValueError):
+        fgs.compare_modes(act, cams, strategies=["precise"])
+
+
+def test_bench_frames_report_shape_and_determinism():
+    act = fgs.activate(fgs.gen_synthetic("mixed", 3000, 7))
+    cams = fgs.orbit_cameras(3, 20.0, 320, 200)
+    rep = fgs.bench_frames(act, cams, repeat=2)
+    assert rep["kind"] == "bench" and rep["repeat"] == 2 and rep["frames_per_repeat"] == 3
+    assert set(rep["frame_ms"]) == {"0", "1", "2"}
+    assert rep["min_ms"] <= rep["avg_ms"] <= rep["max_ms"]
+    assert abs(sum(rep["stage_percent"].values()) - 100.0) < 1e-6
+    assert rep["stage_coverage_percent"] >= 95.0          # SPEC acceptance: stages cover the frame
+    for cam, m, c in zip(cams, rep["pairs_emitted"], rep["pairs_contributing"]):
+        _, ost = orc.render(act, cam)
+        assert (m, c) == (ost["pairs_emitted"], ost["pairs_contributing"])
+    with pytest.raises(ValueError):
+        fgs.bench_frames(act, cams, repeat=0)
