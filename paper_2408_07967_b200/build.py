@@ -53,16 +53,21 @@ def is_stale() -> bool:
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not is_stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build the library.  ``variant`` / ``defines`` are for tuning experiments only:
+    a variant is built with extra -D flags into _lib/variants/<variant>/ and is
+    picked up when FGS_LIB points at it (see _capi.LIB_PATH)."""
+    out_dir = os.path.join(OUT_DIR, "variants", variant) if variant else OUT_DIR
+    lib = os.path.join(out_dir, "libflashgs_b200.so")
+    if not variant and not force and not is_stale():
         return LIB
     nvcc = _nvcc()
-    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(out_dir, exist_ok=True)
     objs = []
     procs = []
     for unit, extra in UNITS:
-        obj = os.path.join(OUT_DIR, unit.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *COMMON, *extra,
+        obj = os.path.join(out_dir, unit.replace(".cu", ".o"))
+        cmd = [nvcc, *ARCH, *COMMON, *extra, *[f"-D{d}" for d in defines],
                "-c", os.path.join(CSRC, unit), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
@@ -75,12 +80,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(out.decode())
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {unit}:\n{out.decode()}")
-    cmd = [nvcc, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static"]
     r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + r.stdout.decode())
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python -m paper_2408_07967_b200.build [--force] [-v] [--variant NAME -DX=1 -DY=2]
+    var = sys.argv[sys.argv.index("--variant") + 1] if "--variant" in sys.argv else ""
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, variant=var, defines=defs))

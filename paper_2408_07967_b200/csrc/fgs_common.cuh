@@ -19,6 +19,9 @@
 
 // ---- launch shapes ---------------------------------------------------------
 #define FGS_PRE_THREADS   256      // K1 / K3: one Gaussian per thread
+#ifndef FGS_PRE_MINBLOCKS
+#define FGS_PRE_MINBLOCKS 3        // K1 resident CTAs per SM the register budget targets
+#endif
 #define FGS_SORT_THREADS  256
 #define FGS_SORT_IPT      16
 #define FGS_SORT_TILE     (FGS_SORT_THREADS * FGS_SORT_IPT)   // 4096 pairs per CTA pass
@@ -26,7 +29,9 @@
 #define FGS_BLEND_BATCH   256
 // per-tile atomic counters sit FGS_CTR_STRIDE words apart (one 32-byte sector each):
 // thousands of L2 atomics on neighbouring words of one line serialise
+#ifndef FGS_CTR_STRIDE
 #define FGS_CTR_STRIDE    8
+#endif
 // tile-sort size classes: <= SMALL one CTA per tile; <= DENSE the medium list; beyond,
 // the dense list.  The lists live in spare words of the cursor slots: dense entry i
 // at cursor[i*FGS_CTR_STRIDE + 1], medium entry i at cursor[i*FGS_CTR_STRIDE + 2]

@@ -164,6 +164,12 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
     uint64_t mymask = 0;
     // K3: does any lane of this warp need the exact test again?
     const bool any_big = !COUNTING && PRECISE && __any_sync(FGS_FULL, job.cand > FGS_MASK_CAND);
+    bool pend = false;                  // WALK_SCATTER: record waiting for its slot
+    uint32_t pend_slot = 0;
+    uint64_t pend_rec = 0;
+    // unrolled by two so the in-flight slot needs no register move right behind its atomic
+    // (a move would wait for the return trip on the spot)
+#pragma unroll 2
     for (uint32_t base = 0; base < total; base += 32) {
         const uint32_t j = base + lane;
         // owner = first lane whose inclusive prefix exceeds j
@@ -223,13 +229,20 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             if (pass) atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
         }
         if (MODE == WALK_SCATTER) {
+            // The cursor's return trip (~320 cycles) is the whole cost of this kernel, so the
+            // record of window i is stored only after window i+1's atomics are in flight.
             const uint32_t bits_o = __shfl_sync(FGS_FULL, depth_bits, o);
             const uint32_t gid_o = __shfl_sync(FGS_FULL, gid, o);
-            if (pass) {
-                const uint32_t slot =
-                    atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
-                keys[slot] = ((uint64_t)bits_o << 32) | gid_o;
-            }
+            uint32_t slot = 0;
+#ifdef FGS_DIAG_RED_ONLY    // timing diagnostic only (wrong output): no return trip
+            if (pass) { atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u); slot = j; }
+#else
+            if (pass) slot = atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
+#endif
+            if (pend) keys[pend_slot] = pend_rec;
+            pend = pass;
+            pend_slot = slot;
+            pend_rec = ((uint64_t)bits_o << 32) | gid_o;
         }
         // owner side: how many of my candidates in this window passed
         const int lo = excl > base ? (int)(excl - base) : 0;
@@ -244,6 +257,7 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             }
         }
     }
+    if (MODE == WALK_SCATTER && pend) keys[pend_slot] = pend_rec;
     if (COUNTING && mask_out) *mask_out = mymask;
     return mine;
 }
@@ -282,7 +296,7 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
 // K1: preprocess + count
 // ---------------------------------------------------------------------------
 template <int STRAT, bool BUCKET>
-__global__ void __launch_bounds__(FGS_PRE_THREADS)
+__global__ void __launch_bounds__(FGS_PRE_THREADS, FGS_PRE_MINBLOCKS)
 k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
              const __grid_constant__ CamDev cam, float tau32, float frustum_thresh,
              int sh_degree, int band0, int band1, FrameDev f)
