@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FGS_ABI_VERSION 2
+#define FGS_ABI_VERSION 3
 #define FGS_TILE 16              /* constants.py:4  TILE_SIZE */
 
 enum {
@@ -50,9 +50,11 @@ enum { FGS_PRECISE = 0, FGS_TIGHT_AABB = 1, FGS_BASELINE_CIRCLE_AABB = 2 };
 /* How the frame's pairs get into (tile, depth, index) order (fgs_layout.sort_mode).
  * Both produce the bit-identical sorted list and range table.
  *   TILE_BUCKET (default): MSD counting pass on the tile field fused into the
- *     count/emit kernels (per-tile histogram -> scan -> scatter), then each
- *     tile's bucket is sorted on (depth bits, index) in shared memory; the
- *     range table is the scan itself.  ~20 B of HBM traffic per pair.
+ *     preprocess kernel: the per-tile counter's old value is the pair's rank
+ *     in its bucket, the pair is parked in a stage, the scan of the counters
+ *     is the range table, and fgs_emit places every staged pair at
+ *     starts[tile] + rank.  Each bucket is then sorted on (depth bits, index)
+ *     in shared memory.  ~52 B of (mostly L2-resident) traffic per pair.
  *   ONESWEEP: pairs emitted in Gaussian order, then a stable LSD radix sort
  *     (8-bit digits, one-sweep passes with decoupled look-back) over the packed
  *     tile|depth key, then a range-identification kernel.  ~172 B per pair. */
@@ -99,7 +101,8 @@ typedef struct fgs_stats {
     uint32_t dense_tiles;          /* TILE_BUCKET: tiles with > 4096 pairs       */
     uint32_t medium_tiles;         /* TILE_BUCKET: tiles with 1025..4096 pairs   */
     uint32_t hard_tiles;           /* TILE_BUCKET: tiles sent to the radix fallback */
-    uint32_t reserved[1];
+    uint32_t stage_used;           /* TILE_BUCKET: stage records reserved = candidate
+                                      tiles inside the band; must fit `capacity`    */
 } fgs_stats;
 
 /* Byte offsets of every per-frame buffer inside the caller's workspace.
@@ -116,7 +119,10 @@ typedef struct fgs_layout {
                                   Gaussian has <= 64 candidates              */
     uint64_t off_blocksums;    /* uint32 [2][nblocks]  sums, exclusive bases  */
     uint64_t off_keys[2];      /* uint64 [capacity]   ping / pong             */
-    uint64_t off_vals[2];      /* uint32 [capacity]                           */
+    uint64_t off_vals[2];      /* uint32 [capacity]
+                                  TILE_BUCKET: keys[1], vals[0], vals[1] are contiguous
+                                  and double as the pair stage (16 B x capacity)
+                                  between fgs_preprocess and fgs_emit             */
     uint64_t off_sortstate;    /* uint64 [sort tiles][256] look-back table    */
     uint64_t off_hist;         /* uint32 [16][256] + tickets                  */
     uint64_t off_starts;       /* int32  [tiles + 1]  sorting.py:139-152      */
@@ -124,8 +130,8 @@ typedef struct fgs_layout {
     uint64_t off_stats;        /* fgs_stats                                   */
     uint64_t off_tilecount;    /* uint32 [tiles][8], word 0 used: pairs per tile
                                   (TILE_BUCKET; one 32-byte sector per counter) */
-    uint64_t off_cursor;       /* uint32 [tiles][8], word 0 used: scatter cursors */
-    int64_t  gaussians, capacity;
+    uint64_t off_cursor;       /* uint32 [tiles][8]: size-class tile lists (words 1..3) */
+    int64_t  gaussians, capacity;   /* capacity = the request rounded up to 64 pairs */
     int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
     int32_t  preprocess_blocks, sort_passes;
     int32_t  sort_mode;        /* FGS_SORT_*; change only via fgs_layout_set_sort_mode */
@@ -185,7 +191,9 @@ int fgs_workspace_init(void *workspace, const fgs_layout *layout_host, void *str
  * cull, project, conic, cutoff, extent rectangle, SH colour, and the number of
  * candidate tiles that pass the strategy's test (intersect.py:63-94 for
  * `precise`).  Writes splat rows, depth, rects, flags, counts, and block sums
- * (ONESWEEP) or the per-tile histogram (TILE_BUCKET).
+ * (ONESWEEP) or the per-tile histogram plus the staged pairs (TILE_BUCKET).
+ * TILE_BUCKET needs room for one stage record per candidate tile: when
+ * stats.stage_used > capacity the overflow flag is raised like for M.
  * Tile rows outside [band_ty0, band_ty1] are not counted (row-band mode;
  * pass 0 and grid_h-1 for a whole frame). */
 int fgs_preprocess(const void *packed_scene, const float *k_cut, int64_t gaussians,
@@ -201,9 +209,9 @@ int fgs_scan(void *workspace, const fgs_layout *layout_host, void *stream);
  * ONESWEEP: key = tile << 32 | depth bits (binning.py:47-54), value = Gaussian
  *   index, written at the scanned offsets, i.e. in ascending Gaussian order
  *   (deterministic, unlike an atomic cursor) into keys[0] / vals[0].
- * TILE_BUCKET: every pair is written once, as a (depth bits << 32 | index)
- *   record at its tile's cursor in keys[0] (cursors start at the scanned
- *   histogram); order inside a bucket is arbitrary until fgs_sort. */
+ * TILE_BUCKET: every staged pair is written once, as a (depth bits << 32 |
+ *   index) record at starts[tile] + rank in keys[0]; order inside a bucket is
+ *   arbitrary (it is the order the counters were hit in) until fgs_sort. */
 int fgs_emit(const fgs_camera *camera_host, int32_t strategy, int32_t band_ty0,
              int32_t band_ty1, void *workspace, const fgs_layout *layout_host,
              void *stream);

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # FGS_LIB selects another build of the same library (tuning variants, see build.py)
 LIB_PATH = os.environ.get("FGS_LIB") or os.path.join(HERE, "_lib", "libflashgs_b200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 STRATEGIES = ("baseline-circle-aabb", "tight-aabb", "precise")   # binning.py:38 order
 STRATEGY_ID = {"precise": 0, "tight-aabb": 1, "baseline-circle-aabb": 2}
 BLEND_EXACT, BLEND_CONTRIB = 1, 2
@@ -51,11 +51,10 @@ class FgsStats(C.Structure):
                 ("unsorted", C.c_uint32), ("tile_out_of_grid", C.c_uint32),
                 ("candidate_tiles_lo", C.c_uint32), ("candidate_tiles_hi", C.c_uint32),
                 ("dense_tiles", C.c_uint32), ("medium_tiles", C.c_uint32),
-                ("hard_tiles", C.c_uint32), ("reserved", C.c_uint32 * 1)]
+                ("hard_tiles", C.c_uint32), ("stage_used", C.c_uint32)]
 
 
-STATS_DTYPE = np.dtype([(n, np.uint32) for n, _ in FgsStats._fields_[:-1]]
-                       + [("reserved", np.uint32, (1,))])
+STATS_DTYPE = np.dtype([(n, np.uint32) for n, _ in FgsStats._fields_])
 assert STATS_DTYPE.itemsize == C.sizeof(FgsStats) == 64
 
 

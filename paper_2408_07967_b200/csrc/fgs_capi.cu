@@ -114,11 +114,12 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
 {
     if (!L || P < 0 || width < 1 || height < 1 || capacity < 0) return FGS_E_ARG;
     // 30-bit pair counts in the sort look-back words; 31-bit Gaussian indices
-    if (P > 0x7fffff00ll || capacity > 0x3fffffffll) return FGS_E_SIZE;
+    if (P > 0x7fffff00ll || capacity > 0x3fffffc0ll) return FGS_E_SIZE;
     memset(L, 0, sizeof(*L));
     const int64_t gw = (width + FGS_TILE - 1) / FGS_TILE, gh = (height + FGS_TILE - 1) / FGS_TILE;
     if (gw > 65535 || gh > 65535 || gw * gh > 0x7ffffff0ll) return FGS_E_SIZE;
     L->gaussians = P;
+    capacity = (capacity + 63) & ~(int64_t)63;        // keys[1] | vals[0] | vals[1] contiguous
     L->capacity = capacity;
     L->width = width;
     L->height = height;

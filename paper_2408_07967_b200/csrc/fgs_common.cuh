@@ -91,6 +91,8 @@ struct FrameDev {
     fgs_stats *stats;
     uint32_t *tilecount;    // [tiles]
     uint32_t *cursor;       // [tiles]
+    uint4    *stage;        // TILE_BUCKET: staged pairs, aliases keys[1] + vals[0] + vals[1]
+    uint32_t stage_capacity;
 };
 
 static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
@@ -117,6 +119,8 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.stats = (fgs_stats *)(b + L->off_stats);
     f.tilecount = (uint32_t *)(b + L->off_tilecount);
     f.cursor = (uint32_t *)(b + L->off_cursor);
+    f.stage = (uint4 *)(b + L->off_keys[1]);
+    f.stage_capacity = (uint32_t)L->capacity;
     return f;
 }
 

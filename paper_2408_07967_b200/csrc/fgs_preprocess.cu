@@ -134,14 +134,24 @@ struct TileJob {
 // Walk the warp's candidate tiles 32 at a time.  Returns this lane's number of
 // passing tiles.  MODE selects what happens to a passing (tile, Gaussian):
 //   WALK_COUNT   nothing (count only)                                  (ONESWEEP, K1)
-//   WALK_HIST    bump the per-tile histogram (fire-and-forget RED)    (TILE_BUCKET, K1)
+//   WALK_STAGE   take the pair's rank inside its tile from the tile's counter and
+//                park (tile, rank, depth bits, index) in the stage     (TILE_BUCKET, K1)
 //   WALK_EMIT    write (key, value) at out_base(owner) + rank          (ONESWEEP, K3)
-//   WALK_SCATTER write (depth bits << 32 | index) at the tile's cursor (TILE_BUCKET, K3)
-// (Measured on B200: appending the pair list from K1 through a warp-aggregated
-// cursor instead, so that the tests run once, makes K1 60 % slower -- the
-// cursor's round trip stalls every walk iteration -- and the scatter is bound by
-// the return-atomics either way, so the tests are simply repeated in K3.)
-enum { WALK_COUNT = 0, WALK_HIST = 1, WALK_EMIT = 2, WALK_SCATTER = 3 };
+// TILE_BUCKET: the counter's old value IS the pair's slot inside its bucket, so the
+// histogram pass hands every pair its final position relative to the bucket start and K3
+// is a plain placement (no second walk, no second round of atomics).  The atomic's return
+// trip is hidden by parking each window's records in registers until the next window's
+// tests are done.
+enum { WALK_COUNT = 0, WALK_STAGE = 1, WALK_EMIT = 2 };
+
+// Where WALK_STAGE parks its records: a chunk of `total candidates` records per warp,
+// reserved with one atomic on stats->stage_used (passing pairs are packed at its front).
+struct StageOut {
+    uint4 *stage;               // (tile, rank in tile, depth bits, Gaussian index)
+    uint32_t *tile_ctr;         // per-tile counters, FGS_CTR_STRIDE words apart
+    fgs_stats *stats;
+    uint32_t capacity;          // records the stage can hold
+};
 
 // The count walks (K1) also return, in `mask_out`, the pass bits of this lane's first 64
 // candidates; the emit walks (K3) take them back through job.mask and only re-run the
@@ -152,10 +162,10 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
                                                     uint32_t depth_bits, uint32_t gid,
                                                     uint64_t *__restrict__ keys,
                                                     uint32_t *__restrict__ vals,
-                                                    uint32_t *__restrict__ tile_ctr,
+                                                    const StageOut *so = nullptr,
                                                     uint64_t *mask_out = nullptr)
 {
-    constexpr bool COUNTING = (MODE == WALK_COUNT || MODE == WALK_HIST);
+    constexpr bool COUNTING = (MODE == WALK_COUNT || MODE == WALK_STAGE);
     const int lane = threadIdx.x & 31;
     const uint32_t incl = warp_incl_scan(job.cand, lane);
     const uint32_t total = __shfl_sync(FGS_FULL, incl, 31);
@@ -164,10 +174,14 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
     uint64_t mymask = 0;
     // K3: does any lane of this warp need the exact test again?
     const bool any_big = !COUNTING && PRECISE && __any_sync(FGS_FULL, job.cand > FGS_MASK_CAND);
-    bool pend = false;                  // WALK_SCATTER: record waiting for its slot
-    uint32_t pend_slot = 0;
-    uint64_t pend_rec = 0;
-    // unrolled by two so the in-flight slot needs no register move right behind its atomic
+    // WALK_STAGE: the warp's chunk of the stage (lane 0 holds the raw reservation; it is
+    // only broadcast when the first records are flushed, one window later)
+    uint32_t chunk_raw = 0, staged = 0;
+    bool pend = false;
+    uint32_t pend_pos = 0, pend_tile = 0, pend_rank = 0, pend_bits = 0, pend_gid = 0;
+    if (MODE == WALK_STAGE && lane == 0 && total)
+        chunk_raw = atomicAdd(&so->stats->stage_used, total);
+    // unrolled by two so a parked rank needs no register move right behind its atomic
     // (a move would wait for the return trip on the spot)
 #pragma unroll 2
     for (uint32_t base = 0; base < total; base += 32) {
@@ -225,24 +239,25 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
                 vals[slot] = gid_o;
             }
         }
-        if (MODE == WALK_HIST) {
-            if (pass) atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
-        }
-        if (MODE == WALK_SCATTER) {
-            // The cursor's return trip (~320 cycles) is the whole cost of this kernel, so the
-            // record of window i is stored only after window i+1's atomics are in flight.
+        if (MODE == WALK_STAGE) {
             const uint32_t bits_o = __shfl_sync(FGS_FULL, depth_bits, o);
             const uint32_t gid_o = __shfl_sync(FGS_FULL, gid, o);
-            uint32_t slot = 0;
-#ifdef FGS_DIAG_RED_ONLY    // timing diagnostic only (wrong output): no return trip
-            if (pass) { atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u); slot = j; }
-#else
-            if (pass) slot = atomicAdd(&tile_ctr[(size_t)(ty * grid_w + tx) * FGS_CTR_STRIDE], 1u);
-#endif
-            if (pend) keys[pend_slot] = pend_rec;
+            const uint32_t tile = (uint32_t)(ty * grid_w + tx);
+            uint32_t rank = 0;
+            if (pass) rank = atomicAdd(&so->tile_ctr[(size_t)tile * FGS_CTR_STRIDE], 1u);
+            // flush the previous window: its ranks have had a whole window to come back
+            if (__any_sync(FGS_FULL, pend)) {
+                const uint32_t cb = __shfl_sync(FGS_FULL, chunk_raw, 0);
+                if (pend && cb + total <= so->capacity)
+                    so->stage[cb + pend_pos] = make_uint4(pend_tile, pend_rank, pend_bits, pend_gid);
+            }
             pend = pass;
-            pend_slot = slot;
-            pend_rec = ((uint64_t)bits_o << 32) | gid_o;
+            pend_pos = staged + __popc(ballot & lanemask_lt());
+            pend_tile = tile;
+            pend_rank = rank;
+            pend_bits = bits_o;
+            pend_gid = gid_o;
+            staged += __popc(ballot);
         }
         // owner side: how many of my candidates in this window passed
         const int lo = excl > base ? (int)(excl - base) : 0;
@@ -250,15 +265,27 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
         if (job.cand && incl > base && lo < hi) {
             const uint32_t m = (hi - lo == 32) ? FGS_FULL : (((1u << (hi - lo)) - 1u) << lo);
             mine += __popc(ballot & m);
-            if (COUNTING) {
+            if (MODE == WALK_COUNT) {
                 // my candidates in this window start at my local index base + lo - excl
                 const uint32_t first = base + (uint32_t)lo - excl;
                 if (first < 64u) mymask |= (uint64_t)((ballot & m) >> lo) << first;
             }
         }
     }
-    if (MODE == WALK_SCATTER && pend) keys[pend_slot] = pend_rec;
-    if (COUNTING && mask_out) *mask_out = mymask;
+    if (MODE == WALK_STAGE && total) {
+        const uint32_t cb = __shfl_sync(FGS_FULL, chunk_raw, 0);
+        const bool fits = cb + total <= so->capacity;
+        if (fits) {
+            if (pend)
+                so->stage[cb + pend_pos] = make_uint4(pend_tile, pend_rank, pend_bits, pend_gid);
+            // the chunk was reserved by candidates: mark what the rejected ones left unused,
+            // so the placement kernel can run flat over [0, stage_used)
+            for (uint32_t i = staged + lane; i < total; i += 32) so->stage[cb + i].x = 0xffffffffu;
+        } else if (lane == 0) {
+            so->stats->overflow = 1u;                          // grow and re-run
+        }
+    }
+    if (MODE == WALK_COUNT && mask_out) *mask_out = mymask;
     return mine;
 }
 
@@ -314,6 +341,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     job.mask = 0;
     bool retained = false, degenerate = false;
     uint32_t full_cand = 0;
+    float zcam = 0.0f;
 
     if (live) {
         const float4 m = sc.g0[g];
@@ -323,6 +351,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         const float t1 = fa(fa(fa(fm(cam.v[4], x), fm(cam.v[5], y)), fm(cam.v[6], z)), cam.v[7]);
         const float t2 = fa(fa(fa(fm(cam.v[8], x), fm(cam.v[9], y)), fm(cam.v[10], z)), cam.v[11]);
         f.depth[g] = t2;
+        zcam = t2;
         ushort4 rect = make_ushort4(0, 0, 0, 0);
         // projection.py:39-47 frustum_mask
         if ((t2 > FGS_Z_NEAR) && (op > frustum_thresh)) {
@@ -481,18 +510,22 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
 
     uint32_t npairs;
     uint64_t passmask = 0;
-    if (BUCKET)
-        npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_HIST>(
-            job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, f.tilecount,
-            &passmask);
-    else if (STRAT == FGS_PRECISE)
+    if (BUCKET) {
+        const StageOut so{f.stage, f.tilecount, f.stats, f.stage_capacity};
+        const float d = zcam;
+        npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_STAGE>(
+            job, cam.width, cam.height, cam.grid_w, 0, __float_as_uint(d), (uint32_t)g, nullptr,
+            nullptr, &so);
+        // binning.py:50-51: depths of emitted pairs must be positive and finite
+        if (npairs && !(d < __int_as_float(0x7f800000))) f.stats->bad_depth = 1u;
+    } else if (STRAT == FGS_PRECISE)
         npairs = warp_walk_tiles<true, WALK_COUNT>(job, cam.width, cam.height, cam.grid_w, 0, 0, 0,
                                                    nullptr, nullptr, nullptr, &passmask);
     else
         npairs = job.cand;
     if (live) {
         f.counts[g] = npairs;
-        if (STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
+        if (!BUCKET && STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
     }
 
     // block totals: pairs (-> blocksums), retained / degenerate / candidates (-> stats)
@@ -620,7 +653,7 @@ int fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream
 
 // K2 (TILE_BUCKET): exclusive scan of the per-tile histogram.  The result IS the
 // range table (sorting.py:139-152): starts[t] .. starts[t+1] is tile t's bucket.
-// Also seeds the scatter cursors, fixes M / overflow and counts non-empty tiles.
+// Also queues the tiles by size class, fixes M / overflow and counts non-empty tiles.
 // One CTA per 1024 tiles; instead of a second kernel or a spin-wait, CTA b sums
 // the (L2-resident) counts of all tiles before its own -- O(T^2/1024) reads, at
 // most 33 MB for an 8K frame's 129600 tiles, and no inter-CTA dependency at all.
@@ -669,7 +702,6 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     if (i < tiles) {
         const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
         starts[i] = (int32_t)e32;
-        cursor[(size_t)i * FGS_CTR_STRIDE] = e32;
         if (v > FGS_DENSE_TILE)     // queue the bucket for its tile-sort size class
             cursor[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE + 1] = (uint32_t)i;
         else if (v > FGS_SMALL_TILE)
@@ -679,7 +711,8 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     if (lane == 0 && nonempty) atomicAdd(&stats->tiles_nonempty, nonempty);
     if (i == tiles - 1) {                       // the thread that owns the last tile knows M
         const unsigned long long M = excl + v;
-        const bool over = M > capacity;
+        // K1 has already raised the flag if some warp's chunk did not fit the stage
+        const bool over = M > capacity || stats->overflow != 0u;
         stats->pairs_emitted = M > 0xffffffffull ? 0xffffffffu : (uint32_t)M;
         stats->overflow = over ? 1u : 0u;       // later kernels of this frame see it and no-op
         stats->pairs_in_buffer = over ? 0u : (uint32_t)M;
@@ -696,9 +729,9 @@ int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaSt
 }
 
 // ---------------------------------------------------------------------------
-// K3: emit (key, value) pairs at the scanned offsets
+// K3 (ONESWEEP): emit (key, value) pairs at the scanned offsets
 // ---------------------------------------------------------------------------
-template <int STRAT, bool BUCKET>
+template <int STRAT>
 __global__ void __launch_bounds__(FGS_PRE_THREADS)
 k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev f)
 {
@@ -707,13 +740,9 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const bool live = g < P;
     const uint32_t cnt = live ? f.counts[g] : 0u;
-    uint32_t total, off = 0;
-    if (BUCKET) {
-        if (__syncthreads_or(cnt != 0u) == 0) return;    // uniform per block
-    } else {
-        off = f.blockbase[blockIdx.x] + block_excl_scan_256(cnt, s_scan, total);
-        if (total == 0) return;                          // uniform per block
-    }
+    uint32_t total;
+    const uint32_t off = f.blockbase[blockIdx.x] + block_excl_scan_256(cnt, s_scan, total);
+    if (total == 0) return;                              // uniform per block
 
     TileJob job;
     job.cand = 0;
@@ -748,12 +777,35 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
         // binning.py:50-51: depths must be positive and finite
         if (!(d > 0.0f) || !(d < __int_as_float(0x7f800000))) f.stats->bad_depth = 1u;
     }
-    if (BUCKET)
-        warp_walk_tiles<STRAT == FGS_PRECISE, WALK_SCATTER>(job, width, height, grid_w, 0, bits,
-                                                            (uint32_t)g, f.keys[0], nullptr, f.cursor);
-    else
-        warp_walk_tiles<STRAT == FGS_PRECISE, WALK_EMIT>(job, width, height, grid_w, off, bits,
-                                                         (uint32_t)g, f.keys[0], f.vals[0], nullptr);
+    warp_walk_tiles<STRAT == FGS_PRECISE, WALK_EMIT>(job, width, height, grid_w, off, bits,
+                                                     (uint32_t)g, f.keys[0], f.vals[0]);
+}
+
+// ---------------------------------------------------------------------------
+// K3 (TILE_BUCKET): place the staged pairs.  K1 parked (tile, rank, depth bits, index)
+// per pair; the scan has since fixed every bucket's start, so a record goes to
+// starts[tile] + rank.  Flat over the reserved part of the stage (unused slots carry
+// tile = ~0), coalesced 16-byte reads, four records in flight per thread.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256)
+k_place(const uint4 *__restrict__ stage, const int32_t *__restrict__ starts,
+        uint64_t *__restrict__ rec, const fgs_stats *__restrict__ stats)
+{
+    if (stats->overflow) return;                         // uniform: grow and re-run
+    const uint32_t n = stats->stage_used;
+    const uint32_t stride = gridDim.x * 256u;
+    for (uint32_t i0 = blockIdx.x * 256u + threadIdx.x; i0 < n; i0 += 4u * stride) {
+        uint4 r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = i0 + (uint32_t)k * stride;
+            r[k] = i < n ? stage[i] : make_uint4(0xffffffffu, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (r[k].x != 0xffffffffu)
+                rec[(uint32_t)starts[r[k].x] + r[k].y] = ((uint64_t)r[k].z << 32) | r[k].w;
+    }
 }
 
 int fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int band1,
@@ -761,14 +813,21 @@ int fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int b
 {
     if (P == 0) return FGS_OK;
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
-#define FGS_K3(S, B) k_emit<S, B><<<blocks, FGS_PRE_THREADS, 0, st>>>( \
-        (int)P, cam.width, cam.height, cam.grid_w, band0, band1, f)
-    if (strategy == FGS_PRECISE) {
-        if (bucket) FGS_K3(FGS_PRECISE, true); else FGS_K3(FGS_PRECISE, false);
+    if (bucket) {
+        // sized from the capacity (the record count lives on the device)
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int64_t want = (f.stage_capacity + 1023) / 1024;
+        const unsigned grid = (unsigned)(want < 1 ? 1 : (want > sms * 8 ? sms * 8 : want));
+        k_place<<<grid, 256, 0, st>>>(f.stage, f.starts, f.keys[0], f.stats);
+    } else if (strategy == FGS_PRECISE) {
+        k_emit<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, 0, st>>>(
+            (int)P, cam.width, cam.height, cam.grid_w, band0, band1, f);
     } else {
-        if (bucket) FGS_K3(FGS_TIGHT_AABB, true); else FGS_K3(FGS_TIGHT_AABB, false);
+        k_emit<FGS_TIGHT_AABB><<<blocks, FGS_PRE_THREADS, 0, st>>>(
+            (int)P, cam.width, cam.height, cam.grid_w, band0, band1, f);
     }
-#undef FGS_K3
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
