@@ -78,6 +78,37 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Second-level cull (after the extent rectangle): does the cutoff ellipse s <= k/2 of a
+// pair miss the whole block of pixel centres [u0,u1] x [v0,v1] (offsets from the splat
+// centre)?  s = (a u^2 + c v^2)/2 + b u v is convex, so over a rectangle that does not
+// contain the centre its minimum lies on an edge the centre is outside of; each such edge
+// is a 1-D parabola.  The comparison carries a margin of 1e-4 of the largest term
+// magnitude in the block -- 100x the rounding of this float32 evaluation and of the
+// per-pixel render.py:213 evaluation it stands in for -- so a pair is only dropped when
+// every pixel of the block would have failed render.py:214 anyway.  NaNs keep the pair.
+__device__ __forceinline__ bool ellipse_misses_block(float a, float b, float c, float k, float u0,
+                                                     float u1, float v0, float v1)
+{
+    const bool out_u = u0 > 0.0f || u1 < 0.0f, out_v = v0 > 0.0f || v1 < 0.0f;
+    if (!out_u && !out_v) return false;                   // centre inside the block
+    const float ue = u0 > 0.0f ? u0 : u1;                 // the edge facing the centre
+    const float ve = v0 > 0.0f ? v0 : v1;
+    float qmin = __int_as_float(0x7f800000);
+    if (out_u) {                                          // edge u = ue, v in [v0, v1]
+        const float bu = b * ue;
+        const float vs = fminf(fmaxf(__fdividef(-bu, c), v0), v1);
+        qmin = fmaf(0.5f * a * ue, ue, fmaf(0.5f * c * vs, vs, bu * vs));
+    }
+    if (out_v) {                                          // edge v = ve, u in [u0, u1]
+        const float bv = b * ve;
+        const float us = fminf(fmaxf(__fdividef(-bv, a), u0), u1);
+        qmin = fminf(qmin, fmaf(0.5f * c * ve, ve, fmaf(0.5f * a * us, us, bv * us)));
+    }
+    const float um = fmaxf(fabsf(u0), fabsf(u1)), vm = fmaxf(fabsf(v0), fabsf(v1));
+    const float mag = fmaf(fabsf(a) * um, um, fmaf(fabsf(c) * vm, vm, 2.0f * fabsf(b) * um * vm));
+    return qmin > fmaf(1e-4f, mag, 0.5f * k * 1.001f);
+}
+
 struct BlendSmem {
     float4 row[2][FGS_BLEND_BATCH][3];     // (cx,cy,a,b) (c,op,k,r) (g,b,hx,hy)
     float  z[2][FGS_BLEND_BATCH];          // camera depth of the pair's Gaussian (extras)
@@ -166,9 +197,12 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
             bool keep = false;
             if (jl < cnt) {
                 const float4 q0 = S.row[cur][jl][0];
+                const float4 q1 = S.row[cur][jl][1];
                 const float4 q2 = S.row[cur][jl][2];
-                keep = !(fs(wx_lo, q0.x) > q2.z || fs(wx_hi, q0.x) < -q2.z ||
-                         fs(wy_lo, q0.y) > q2.w || fs(wy_hi, q0.y) < -q2.w);
+                const float u0 = fs(wx_lo, q0.x), u1 = fs(wx_hi, q0.x);
+                const float v0 = fs(wy_lo, q0.y), v1 = fs(wy_hi, q0.y);
+                keep = !(u0 > q2.z || u1 < -q2.z || v0 > q2.w || v1 < -q2.w);
+                if (keep) keep = !ellipse_misses_block(q0.z, q0.w, q1.x, q1.z, u0, u1, v0, v1);
             }
             uint32_t live = __ballot_sync(FGS_FULL, keep);
             while (live) {

@@ -122,6 +122,44 @@ __device__ __forceinline__ bool tile_hits(int tx, int ty, int width, int height,
     return chord_hits(c, dm(b2, u1), ds(dm(dm(a, u1), u1), k), v0, v1);
 }
 
+// float32 screening of the same predicate.  intersect.py:63-94 is true exactly when the
+// cutoff ellipse a u^2 + 2 b u v + c v^2 <= k meets the (closed) tile rectangle, i.e. when
+// the minimum of that convex form over the rectangle is <= k.  The minimum is 0 if the
+// centre is inside; otherwise it lies on an edge the centre is outside of, where the form is
+// a 1-D parabola.  Returns 1 (hit) or 0 (miss) when the float32 minimum is clear of k by
+// more than 1e-4 of the largest term magnitude in the tile (1000x the rounding of this
+// evaluation; the float64 reference is far more accurate still), and 2 when it is not --
+// the caller then runs the float64 predicate, so the verdict is always the reference's.
+__device__ __forceinline__ int tile_hits32(int tx, int ty, int width, int height, float cx,
+                                           float cy, float a, float b, float c, float k)
+{
+    const float x0 = (float)(tx * FGS_TILE), y0 = (float)(ty * FGS_TILE);
+    const float x1 = fminf(x0 + (float)FGS_TILE, (float)width);
+    const float y1 = fminf(y0 + (float)FGS_TILE, (float)height);
+    const float u0 = x0 - cx, u1 = x1 - cx, v0 = y0 - cy, v1 = y1 - cy;   // signs are exact
+    const bool out_u = !(u0 <= 0.0f && u1 >= 0.0f), out_v = !(v0 <= 0.0f && v1 >= 0.0f);
+    if (!out_u && !out_v) return 1;                       // intersect.py:84-86 centre in tile
+    const float ue = u0 > 0.0f ? u0 : u1;                 // the edge facing the centre
+    const float ve = v0 > 0.0f ? v0 : v1;
+    float qmin = __int_as_float(0x7f800000);
+    if (out_u) {                                          // edge u = ue, v in [v0, v1]
+        const float bu = b * ue;
+        const float vs = fminf(fmaxf(__fdividef(-bu, c), v0), v1);
+        qmin = a * ue * ue + (c * vs * vs + 2.0f * bu * vs);
+    }
+    if (out_v) {                                          // edge v = ve, u in [u0, u1]
+        const float bv = b * ve;
+        const float us = fminf(fmaxf(__fdividef(-bv, a), u0), u1);
+        qmin = fminf(qmin, c * ve * ve + (a * us * us + 2.0f * bv * us));
+    }
+    const float um = fmaxf(fabsf(u0), fabsf(u1)), vm = fmaxf(fabsf(v0), fabsf(v1));
+    const float tol = 1e-4f * (fabsf(a) * um * um + fabsf(c) * vm * vm + 2.0f * fabsf(b) * um * vm
+                               + fabsf(k));
+    if (qmin < k - tol) return 1;
+    if (qmin > k + tol) return 0;
+    return 2;                                             // too close (or not finite): ask float64
+}
+
 // What a lane contributes to its warp's flattened candidate list.
 struct TileJob {
     uint32_t cand;              // candidate tiles (0 = lane idle)
@@ -218,7 +256,9 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             const float c = __shfl_sync(FGS_FULL, job.c, o);
             const float ke = __shfl_sync(FGS_FULL, job.keff, o);
             if (COUNTING) {
-                pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
+                const int h = act ? tile_hits32(tx, ty, width, height, cx, cy, a, b, c, ke) : 0;
+                pass = h == 1;
+                if (h == 2) pass = tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
             } else {
                 const uint32_t cand_o = __shfl_sync(FGS_FULL, job.cand, o);
                 if (cand_o > FGS_MASK_CAND)
