@@ -272,6 +272,12 @@ int fgs_blend_tiles(const float *splat, const float *gaussian_depth,
                     float *out_rgb, float *out_alpha, float *out_depth,
                     uint8_t *contrib, fgs_stats *stats, void *stream);
 
+/* images.py:12-15 quantize: float32 linear channels -> uint8,
+ * q = floor(clip(c, 0, 1) * 255 + 0.5) evaluated in float64 like the reference.
+ * `count` = number of channel values (H*W*3).  The step after the path: it lets a
+ * frame service read back 3 bytes per pixel instead of 12. */
+int fgs_quantize_rgb8(const float *rgb, int64_t count, uint8_t *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

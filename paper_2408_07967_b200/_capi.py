@@ -31,7 +31,7 @@ SYMBOLS = (
     "fgs_workspace_init",
     "fgs_preprocess", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
     "fgs_render", "fgs_sort_pairs_scratch_bytes", "fgs_sort_pairs", "fgs_tile_ranges",
-    "fgs_blend_tiles", "fgs_profile_begin", "fgs_profile_end",
+    "fgs_blend_tiles", "fgs_profile_begin", "fgs_profile_end", "fgs_quantize_rgb8",
 )
 
 
@@ -115,6 +115,7 @@ def _declare(L):
         "fgs_tile_ranges": (C.c_int, [vp, i64, i32, vp, vp, vp]),
         "fgs_blend_tiles": (C.c_int, [vp, vp, vp, vp, i32, i32, f3, dbl, i32, i32, i32,
                                       vp, vp, vp, vp, vp, vp]),
+        "fgs_quantize_rgb8": (C.c_int, [vp, i64, vp, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

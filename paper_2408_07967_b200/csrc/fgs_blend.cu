@@ -324,3 +324,31 @@ int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *va
     return want_contrib ? FGS_GO(false, true) : FGS_GO(false, false);
 #undef FGS_GO
 }
+
+// images.py:12-15 quantize (float64 like the reference); four values per thread
+__global__ void __launch_bounds__(256)
+k_quantize_rgb8(const float *__restrict__ rgb, int64_t count, uint8_t *__restrict__ out)
+{
+    const int64_t i0 = ((int64_t)blockIdx.x * 256 + threadIdx.x) * 4;
+    if (i0 >= count) return;
+    auto q = [](float v) -> uint32_t {
+        double c = (double)v;
+        c = c < 0.0 ? 0.0 : (c > 1.0 ? 1.0 : c);
+        return (uint32_t)floor(da(dm(c, 255.0), 0.5));
+    };
+    if (i0 + 4 <= count) {
+        const float4 v = *reinterpret_cast<const float4 *>(rgb + i0);
+        *reinterpret_cast<uint32_t *>(out + i0) = q(v.x) | (q(v.y) << 8) | (q(v.z) << 16) | (q(v.w) << 24);
+    } else {
+        for (int64_t i = i0; i < count; ++i) out[i] = (uint8_t)q(rgb[i]);
+    }
+}
+
+int fgs_launch_quantize(const float *rgb, int64_t count, uint8_t *out, cudaStream_t st)
+{
+    if (count == 0) return FGS_OK;
+    const int64_t blocks = (count + 1023) / 1024;
+    k_quantize_rgb8<<<(unsigned)blocks, 256, 0, st>>>(rgb, count, out);
+    FGS_CHECK_LAUNCH();
+    return FGS_OK;
+}

@@ -355,4 +355,11 @@ int fgs_blend_tiles(const float *splat, const float *gaussian_depth, const uint3
                             (cudaStream_t)stream);
 }
 
+int fgs_quantize_rgb8(const float *rgb, int64_t count, uint8_t *out, void *stream)
+{
+    if (count < 0 || (count && (!rgb || !out))) return FGS_E_ARG;
+    if (((uintptr_t)rgb & 15) || ((uintptr_t)out & 3)) return FGS_E_ARG;   // vector accesses
+    return fgs_launch_quantize(rgb, count, out, (cudaStream_t)stream);
+}
+
 }  // extern "C"

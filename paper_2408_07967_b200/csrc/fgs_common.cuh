@@ -156,6 +156,8 @@ int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *v
                       double tau, int flags, int band0, int band1, float *rgb, float *alpha,
                       float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st);
 
+int  fgs_launch_quantize(const float *rgb, int64_t count, uint8_t *out, cudaStream_t st);
+
 void fgs_set_cuda_error(cudaError_t e);
 // Records the next caller-supplied profiling event on `st` (no-op unless
 // fgs_profile_begin armed this thread).  Called after every kernel launch.

@@ -163,6 +163,7 @@ class _Workspace:
         self.rgb = torch.empty((height, width, 3), dtype=torch.float32, device=device)
         self.alpha = None
         self.depthmap = None
+        self.rgb8 = None               # (H, W, 3) uint8, allocated on first quantized render
         self.h_stats = torch.empty(64, dtype=torch.uint8, pin_memory=True)
         self.epoch = 1
         _capi.check(_capi.lib().fgs_workspace_init(C.c_void_p(self.base), C.byref(self.lay),
@@ -275,7 +276,7 @@ class Pipeline:
     def render(self, camera, strategy="precise", tau=TAU_DEFAULT,
                background=(0.0, 0.0, 0.0), workers=1, initial_capacity=None,
                pipelined=True, *, exact=False, extras=False, contrib=True,
-               as_numpy=True, band=None, timing=True):
+               as_numpy=True, band=None, timing=True, quantized=False):
         """bin -> sort -> render on the GPU; returns (Framebuffer, FrameStats).
 
         ``workers`` and ``pipelined`` are accepted for signature compatibility
@@ -283,7 +284,9 @@ class Pipeline:
         Keyword-only extras: ``exact`` (bit-identical frame, FP64 expf),
         ``extras`` (alpha + depth maps), ``contrib`` (pairs_contributing),
         ``as_numpy`` (False: CUDA tensors, no D2H), ``band=(ty0, ty1)`` tile-row
-        band for multi-GPU row splitting.
+        band for multi-GPU row splitting, ``quantized`` (the image comes back as
+        uint8, quantised on the device exactly like ``images.py:12-15``; a
+        quarter of the bytes to read back).
         """
         torch = _torch()
         t_host0 = time.perf_counter_ns()
@@ -335,11 +338,18 @@ class Pipeline:
                                         a_ptr, d_ptr, base, lay, st))
                 if timing:
                     ev[3].record()
+                out_img = ws.rgb
+                if quantized:
+                    if ws.rgb8 is None:
+                        ws.rgb8 = torch.empty((H, W, 3), dtype=torch.uint8, device=self.device)
+                    _capi.check(L.fgs_quantize_rgb8(ws.rgb.data_ptr(), H * W * 3,
+                                                    ws.rgb8.data_ptr(), st))
+                    out_img = ws.rgb8
                 ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
                 h_rgb = None
                 if as_numpy:
-                    h_rgb = _pinned.take(torch, (H, W, 3), torch.float32)
-                    h_rgb.copy_(ws.rgb, non_blocking=True)
+                    h_rgb = _pinned.take(torch, (H, W, 3), out_img.dtype)
+                    h_rgb.copy_(out_img, non_blocking=True)
                     if extras:
                         h_a = _pinned.take(torch, (H, W), torch.float32)
                         h_d = _pinned.take(torch, (H, W), torch.float32)
@@ -371,7 +381,7 @@ class Pipeline:
                 if extras:
                     fb.alpha, fb.depth = _pinned.as_numpy(h_a), _pinned.as_numpy(h_d)
             else:
-                fb = Framebuffer(ws.rgb.clone(), bg)
+                fb = Framebuffer(out_img.clone(), bg)
                 if extras:
                     fb.alpha, fb.depth = ws.alpha.clone(), ws.depthmap.clone()
             self._give_ws(ws)
@@ -379,10 +389,12 @@ class Pipeline:
         return fb, stats
 
     def render_many(self, cameras, strategy="precise", tau=TAU_DEFAULT,
-                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=4, streams=2):
+                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=4, streams=2,
+                    quantized=False):
         """``list(render_iter(...))``: every view's ``(Framebuffer, FrameStats)``."""
         return list(self.render_iter(cameras, strategy, tau, background, exact=exact,
-                                     contrib=contrib, depth=depth, streams=streams))
+                                     contrib=contrib, depth=depth, streams=streams,
+                                     quantized=quantized))
 
     def _side_streams(self, torch, n):
         pool = getattr(self, "_streams", None)
@@ -393,7 +405,8 @@ class Pipeline:
         return pool[:n]
 
     def render_iter(self, cameras, strategy="precise", tau=TAU_DEFAULT,
-                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=4, streams=2):
+                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=4, streams=2,
+                    quantized=False):
         """Throughput path for a batch of views (BASELINE config 5; the reference's
         ``bench_frames`` loop, ``pipeline.py:212-233``): same frames and stats as calling
         ``render`` per camera, but up to ``depth`` frames are in flight, issued round-robin
@@ -424,7 +437,7 @@ class Pipeline:
             if int(s["overflow"]) or int(s["bad_depth"]):
                 _pinned.give(h_rgb)          # grow-and-rerun / raise through the plain path
                 return self.render(cam_obj, strategy, tau, background, exact=exact,
-                                   contrib=contrib, timing=False)
+                                   contrib=contrib, timing=False, quantized=quantized)
             st = FrameStats(strategy=strategy, tau=float(tau), workers=1)
             _fill_counters(st, s)
             self._last_pairs = max(self._last_pairs, st.pairs_emitted)
@@ -457,9 +470,17 @@ class Pipeline:
                                              ws.next_epoch(), ws.rgb.data_ptr(), None, None,
                                              C.c_void_p(ws.base), C.byref(ws.lay),
                                              C.c_void_p(lane.cuda_stream)))
-                    h_rgb = _pinned.take(torch, (H, W, 3), torch.float32)
+                    out_img = ws.rgb
+                    if quantized:
+                        if ws.rgb8 is None:
+                            ws.rgb8 = torch.empty((H, W, 3), dtype=torch.uint8, device=self.device)
+                        _capi.check(L.fgs_quantize_rgb8(ws.rgb.data_ptr(), H * W * 3,
+                                                        ws.rgb8.data_ptr(),
+                                                        C.c_void_p(lane.cuda_stream)))
+                        out_img = ws.rgb8
+                    h_rgb = _pinned.take(torch, (H, W, 3), out_img.dtype)
                     with torch.cuda.stream(lane):
-                        h_rgb.copy_(ws.rgb, non_blocking=True)
+                        h_rgb.copy_(out_img, non_blocking=True)
                         ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
                         done = torch.cuda.Event()
                         done.record(lane)

@@ -429,3 +429,47 @@ def test_bench_frames_report_shape_and_determinism():
         assert (m, c) == (ost["pairs_emitted"], ost["pairs_contributing"])
     with pytest.raises(ValueError):
         fgs.bench_frames(act, cams, repeat=0)
+
+
+# ---------------------------------------------------------------------------
+# quantised output and the frame-service adapter (reference images.py:12-15, service.py:111-155)
+# ---------------------------------------------------------------------------
+def test_quantized_frames_match_reference_quantize():
+    from paper_2408_07967_b200 import service
+    act = fgs.activate(fgs.gen_synthetic("mixed", 5000, 9))
+    cams = fgs.orbit_cameras(3, 18.0, 333, 201)          # odd sizes: vector tail path
+    pipe = fgs.Pipeline(act)
+    for cam in cams:
+        for bg in ((0, 0, 0), (1.5, -0.25, 0.3)):        # out-of-range channels get clipped
+            fb, _ = pipe.render(cam, background=bg)
+            q, _ = pipe.render(cam, background=bg, quantized=True)
+            assert q.image.dtype == np.uint8 and q.image.shape == fb.image.shape
+            assert np.array_equal(q.image, service.quantize(fb.image))
+    many = pipe.render_many(cams, quantized=True)
+    for cam, (fbq, _) in zip(cams, many):
+        assert np.array_equal(fbq.image, service.quantize(pipe.render(cam)[0].image))
+
+
+def test_frame_service_render_pose():
+    from paper_2408_07967_b200 import service
+    act = fgs.activate(fgs.gen_synthetic("mixed", 3000, 4))
+    svc = service.FrameService(act, encoding="ppm", max_pixels=320 * 240)
+    req = {"width": 320, "height": 200, "position": [0.0, 0.0, -20.0], "yaw": 0.1, "pitch": -0.05}
+    body, headers = svc.render_pose(req)
+    assert body.startswith(b"P6\n320 200\n255\n") and len(body) == 15 + 320 * 200 * 3
+    cam, strat = svc.camera_for(req)
+    oimg, ost = orc.render(act, cam)
+    assert headers["X-Flash-Pairs-Emitted"] == str(ost["pairs_emitted"])
+    assert headers["X-Flash-Strategy"] == strat == "precise"
+    got = np.frombuffer(body[15:], np.uint8).reshape(200, 320, 3).astype(np.int32)
+    assert np.abs(got - service.quantize(oimg).astype(np.int32)).max() <= 1   # 1e-3 tolerance -> <= 1 level
+    # toggling the strategy gives the identical bytes (reference test_service.py:94-101)
+    body2, _ = svc.render_pose(dict(req, strategy="baseline-circle-aabb"))
+    assert body2 == body
+    with pytest.raises(service.OversizeError):
+        svc.render_pose(dict(req, width=4000, height=4000))
+    for bad in ({"width": 320}, dict(req, position=[1, 2]), dict(req, strategy="nope"),
+                dict(req, fov_y=1.0), {"width": 320, "height": 200, "position": [0, 0, 0]},
+                dict(req, width=8, height=8)):
+        with pytest.raises(service.PoseError):
+            svc.render_pose(bad)

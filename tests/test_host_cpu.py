@@ -144,3 +144,17 @@ def test_psnr_known_answers():
     assert abs(fgs.max_abs_diff(a, a + np.float32(0.25)) - 0.25) < 1e-9
     with pytest.raises(ValueError):
         fgs.psnr(a, np.zeros((2, 2, 3), np.float32))
+
+
+def test_integration_doc_structs_match_the_library():
+    """INTEGRATION.md shows the reference-side ctypes binding; its struct mirrors must
+    have the real field names and sizes."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = open(os.path.join(root, "INTEGRATION.md")).read()
+    ns = {"C": C}
+    exec(src[src.index("class Cam(C.Structure):"):src.index("class Layout(C.Structure):")], ns)
+    exec(src[src.index("class Layout(C.Structure):"):src.index("    # fill it with")], ns)
+    assert C.sizeof(ns["Cam"]) == C.sizeof(_capi.FgsCamera)
+    assert [f[0] for f in ns["Cam"]._fields_] == [f[0] for f in _capi.FgsCamera._fields_]
+    assert C.sizeof(ns["Layout"]) == C.sizeof(_capi.FgsLayout)
+    assert [f[0] for f in ns["Layout"]._fields_] == [f[0] for f in _capi.FgsLayout._fields_]
