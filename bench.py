@@ -173,6 +173,8 @@ def main():
     ap.add_argument("--exact", action="store_true", help="bit-exact blend mode")
     ap.add_argument("--sort-mode", default="tile-bucket", choices=["tile-bucket", "onesweep"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-spatial", action="store_true",
+                    help="keep the scene in the caller's order (no Morton slot order)")
     ap.add_argument("--streams", type=int, default=2,
                     help="CUDA streams the timed views are issued on round-robin (1 = back to back)")
     args = ap.parse_args()
@@ -209,7 +211,8 @@ def main():
     if args.mode == "bands" and world > 1:
         band = bands[rank]
 
-    pipe = fgs.Pipeline(act, sort_mode=args.sort_mode)
+    pipe = fgs.Pipeline(act, sort_mode=args.sort_mode,
+                        spatial_order=False if args.no_spatial else None)
     L = _capi.lib()
     hbm_peak, peak_src, sm_max = peaks()
 
@@ -368,9 +371,9 @@ def main():
         T_tiles = int(lay.tiles)
         # algorithmic bytes per launch (packed scene reads 240+4 B/Gaussian)
         alg = {
-            "preprocess": 236.0 * P + 52.0 * R + (16.0 * M if bucket else 0.0),
-            # bucket: 16 B staged record in + 8 B record out; onesweep: 12 B pair out + counts
-            "emit": 24.0 * M if bucket else 12.0 * M + 4.0 * P,
+            "preprocess": 236.0 * P + 52.0 * R,
+            # bucket: rect + mask + depth + count in, 8 B record out; onesweep: 12 B pair out
+            "emit": 8.0 * M + 24.0 * P if bucket else 12.0 * M + 4.0 * P,
             "tile_sort": 12.0 * M,          # 8 B record in, 4 B index out
             "sort_hist": 8.0 * M,
             "ranges": 8.0 * M + 4.0 * (T_tiles + 1),

@@ -49,12 +49,14 @@ enum { FGS_PRECISE = 0, FGS_TIGHT_AABB = 1, FGS_BASELINE_CIRCLE_AABB = 2 };
 
 /* How the frame's pairs get into (tile, depth, index) order (fgs_layout.sort_mode).
  * Both produce the bit-identical sorted list and range table.
- *   TILE_BUCKET (default): MSD counting pass on the tile field fused into the
- *     preprocess kernel: the per-tile counter's old value is the pair's rank
- *     in its bucket, the pair is parked in a stage, the scan of the counters
- *     is the range table, and fgs_emit places every staged pair at
- *     starts[tile] + rank.  Each bucket is then sorted on (depth bits, index)
- *     in shared memory.  ~52 B of (mostly L2-resident) traffic per pair.
+ *   TILE_BUCKET (default): counting sort on the tile index with the CTA as the
+ *     unit: fgs_preprocess counts each CTA's pairs per tile in shared memory
+ *     and reserves one range per (CTA, tile) in the tile's bucket; the scan of
+ *     the per-tile counters is the range table; fgs_emit walks again, gathers
+ *     each CTA's records by tile in shared memory and writes contiguous runs.
+ *     Each bucket is then sorted on (depth bits, index) in shared memory.
+ *     Best with a scene packed in spatial order (fgs_scene_order), where a
+ *     CTA's Gaussians share a few dozen tiles.  ~20 B of HBM traffic per pair.
  *   ONESWEEP: pairs emitted in Gaussian order, then a stable LSD radix sort
  *     (8-bit digits, one-sweep passes with decoupled look-back) over the packed
  *     tile|depth key, then a range-identification kernel.  ~172 B per pair. */
@@ -101,8 +103,8 @@ typedef struct fgs_stats {
     uint32_t dense_tiles;          /* TILE_BUCKET: tiles with > 4096 pairs       */
     uint32_t medium_tiles;         /* TILE_BUCKET: tiles with 1025..4096 pairs   */
     uint32_t hard_tiles;           /* TILE_BUCKET: tiles sent to the radix fallback */
-    uint32_t stage_used;           /* TILE_BUCKET: stage records reserved = candidate
-                                      tiles inside the band; must fit `capacity`    */
+    uint32_t list_used;            /* TILE_BUCKET: (CTA, tile) table entries of the frame;
+                                      at most M, so it fits whenever M fits          */
 } fgs_stats;
 
 /* Byte offsets of every per-frame buffer inside the caller's workspace.
@@ -121,16 +123,19 @@ typedef struct fgs_layout {
     uint64_t off_keys[2];      /* uint64 [capacity]   ping / pong             */
     uint64_t off_vals[2];      /* uint32 [capacity]
                                   TILE_BUCKET: keys[1], vals[0], vals[1] are contiguous
-                                  and double as the pair stage (16 B x capacity)
-                                  between fgs_preprocess and fgs_emit             */
+                                  and hold the frame's (CTA, tile) table list (16 B x
+                                  capacity) between fgs_preprocess and fgs_emit   */
     uint64_t off_sortstate;    /* uint64 [sort tiles][256] look-back table    */
     uint64_t off_hist;         /* uint32 [16][256] + tickets                  */
     uint64_t off_starts;       /* int32  [tiles + 1]  sorting.py:139-152      */
     uint64_t off_contrib;      /* uint8  [capacity]                           */
     uint64_t off_stats;        /* fgs_stats                                   */
-    uint64_t off_tilecount;    /* uint32 [tiles][8], word 0 used: pairs per tile
-                                  (TILE_BUCKET; one 32-byte sector per counter) */
+    uint64_t off_tilecount;    /* uint32 [tiles][8]: TILE_BUCKET per-tile counters, one 32-byte
+                                  sector each: [0] pairs reserved through the CTAs' tile
+                                  tables, [1] fallback pairs, [2] fallback cursor       */
     uint64_t off_cursor;       /* uint32 [tiles][8]: size-class tile lists (words 1..3) */
+    uint64_t off_ctainfo;      /* uint32 [preprocess blocks][4]: TILE_BUCKET, each K1 CTA's
+                                  (first table entry, entries, write-combined records, 0) */
     int64_t  gaussians, capacity;   /* capacity = the request rounded up to 64 pairs */
     int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
     int32_t  preprocess_blocks, sort_passes;
@@ -158,15 +163,31 @@ int32_t fgs_profile_end(void);
 /* ---- per-scene (model_io.py:78-118 ActivatedScene; untimed in the reference,
  *      pipeline.py:1-5) ------------------------------------------------------ */
 
-/* Bytes of the packed device scene for P Gaussians. */
+/* Bytes of the packed device scene for P Gaussians (248 B per Gaussian, P rounded
+ * up to 32). */
 size_t fgs_scene_bytes(int64_t gaussians);
+
+/* Spatial (Morton) order of a scene, computed on the device: order_out[slot] =
+ * index of the Gaussian stored in that slot, a permutation of 0..P-1 sorted by
+ * the 63-bit Morton code of the mean inside the scene's bounding box (ties by
+ * index).  Per scene, untimed like activate (pipeline.py:1-5).  `scratch` is
+ * fgs_scene_order_scratch_bytes(P) bytes of device memory. */
+size_t fgs_scene_order_scratch_bytes(int64_t gaussians);
+int fgs_scene_order(const float *means, int64_t gaussians, uint32_t *order_out,
+                    void *scratch, size_t scratch_bytes, void *stream);
 
 /* Re-lay the reference's arrays (means (P,3), opacities (P,), scales (P,3),
  * rotations (P,4) wxyz unit, sh (P,16,3)) into float4 planes so that the
- * preprocess kernel's loads are coalesced: 240 B per Gaussian. */
+ * preprocess kernel's loads are coalesced, plus the slot <-> index tables.
+ * `order` (device, may be NULL = identity) is a permutation of 0..P-1: slot i
+ * holds Gaussian order[i].  The per-Gaussian frame buffers (splat, depth,
+ * rects, flags, counts) are indexed by SLOT: buffer row `slot` belongs to
+ * Gaussian order[slot].  Pair values are Gaussian indices and the sorted list
+ * is the reference's for any packing; FGS_SORT_ONESWEEP alone requires the
+ * identity order (its pair values are slots). */
 int fgs_scene_pack(const float *means, const float *opacities, const float *scales,
-                   const float *rotations, const float *sh, int64_t gaussians,
-                   void *packed_scene, void *stream);
+                   const float *rotations, const float *sh, const uint32_t *order,
+                   int64_t gaussians, void *packed_scene, void *stream);
 
 /* extent.py:19-30 power_cutoffs: k = min(9, 2 ln(alpha0 / tau)) with the log in
  * float64, rounded once to float32.  One float per Gaussian; depends on the
@@ -191,9 +212,8 @@ int fgs_workspace_init(void *workspace, const fgs_layout *layout_host, void *str
  * cull, project, conic, cutoff, extent rectangle, SH colour, and the number of
  * candidate tiles that pass the strategy's test (intersect.py:63-94 for
  * `precise`).  Writes splat rows, depth, rects, flags, counts, and block sums
- * (ONESWEEP) or the per-tile histogram plus the staged pairs (TILE_BUCKET).
- * TILE_BUCKET needs room for one stage record per candidate tile: when
- * stats.stage_used > capacity the overflow flag is raised like for M.
+ * (ONESWEEP) or the per-tile counters plus each CTA's (tile, range) list
+ * (TILE_BUCKET).
  * Tile rows outside [band_ty0, band_ty1] are not counted (row-band mode;
  * pass 0 and grid_h-1 for a whole frame). */
 int fgs_preprocess(const void *packed_scene, const float *k_cut, int64_t gaussians,
@@ -209,18 +229,21 @@ int fgs_scan(void *workspace, const fgs_layout *layout_host, void *stream);
  * ONESWEEP: key = tile << 32 | depth bits (binning.py:47-54), value = Gaussian
  *   index, written at the scanned offsets, i.e. in ascending Gaussian order
  *   (deterministic, unlike an atomic cursor) into keys[0] / vals[0].
- * TILE_BUCKET: every staged pair is written once, as a (depth bits << 32 |
- *   index) record at starts[tile] + rank in keys[0]; order inside a bucket is
- *   arbitrary (it is the order the counters were hit in) until fgs_sort. */
-int fgs_emit(const fgs_camera *camera_host, int32_t strategy, int32_t band_ty0,
-             int32_t band_ty1, void *workspace, const fgs_layout *layout_host,
-             void *stream);
+ * TILE_BUCKET: every pair is written once, as a (depth bits << 32 | index)
+ *   record inside its (CTA, tile) range of the tile's bucket in keys[0]; order
+ *   inside a bucket is arbitrary until fgs_sort. */
+int fgs_emit(const void *packed_scene, const fgs_camera *camera_host, int32_t strategy,
+             int32_t band_ty0, int32_t band_ty1, void *workspace,
+             const fgs_layout *layout_host, void *stream);
 
 /* sorting.py:101-136 sort_pairs for the frame's pair buffer: stable LSD radix
  * sort, 8-bit digits, over key bits [0,31) and [32, 32+tile_bits); emission
  * order makes ties come out in ascending value, so the value passes of the
  * reference are not needed.  `epoch` must increase by at least 16 per call on
- * the same workspace. */
+ * the same workspace.
+ * TILE_BUCKET: each tile's bucket is sorted on (depth bits, Gaussian index) in
+ * shared memory.  vals[0] receives the Gaussian index of every sorted pair; with
+ * layout.keep_sorted_keys keys[1] = tile << 32 | depth bits as well. */
 int fgs_sort(void *workspace, const fgs_layout *layout_host, uint32_t epoch, void *stream);
 
 /* sorting.py:139-152 tile_range_table on the sorted buffer. */
@@ -228,8 +251,10 @@ int fgs_ranges(void *workspace, const fgs_layout *layout_host, void *stream);
 
 /* render.py:273-310 render_frame (+ 135-252 the pipelined compositor).
  * out_rgb (H,W,3) float32 is required; out_alpha (H,W) = 1 - T_final and
- * out_depth (H,W) = sum of blend weight * camera z are optional extras. */
-int fgs_blend(const float background[3], double tau, int32_t flags,
+ * out_depth (H,W) = sum of blend weight * camera z are optional extras.
+ * `packed_scene` supplies the index -> slot table: pair values are Gaussian
+ * indices, the splat rows are stored by slot. */
+int fgs_blend(const void *packed_scene, const float background[3], double tau, int32_t flags,
               int32_t band_ty0, int32_t band_ty1,
               float *out_rgb, float *out_alpha, float *out_depth,
               void *workspace, const fgs_layout *layout_host, void *stream);

@@ -27,7 +27,7 @@ SORT_TILE = 4096
 # every symbol include/flashgs_b200.h declares (checked by the CPU test-suite)
 SYMBOLS = (
     "fgs_abi_version", "fgs_error_string", "fgs_last_cuda_error", "fgs_scene_bytes",
-    "fgs_scene_pack", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_layout_set_sort_mode",
+    "fgs_scene_order_scratch_bytes", "fgs_scene_order", "fgs_scene_pack", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_layout_set_sort_mode",
     "fgs_workspace_init",
     "fgs_preprocess", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
     "fgs_render", "fgs_sort_pairs_scratch_bytes", "fgs_sort_pairs", "fgs_tile_ranges",
@@ -51,7 +51,7 @@ class FgsStats(C.Structure):
                 ("unsorted", C.c_uint32), ("tile_out_of_grid", C.c_uint32),
                 ("candidate_tiles_lo", C.c_uint32), ("candidate_tiles_hi", C.c_uint32),
                 ("dense_tiles", C.c_uint32), ("medium_tiles", C.c_uint32),
-                ("hard_tiles", C.c_uint32), ("stage_used", C.c_uint32)]
+                ("hard_tiles", C.c_uint32), ("list_used", C.c_uint32)]
 
 
 STATS_DTYPE = np.dtype([(n, np.uint32) for n, _ in FgsStats._fields_])
@@ -68,6 +68,7 @@ class FgsLayout(C.Structure):
                 ("off_hist", C.c_uint64), ("off_starts", C.c_uint64),
                 ("off_contrib", C.c_uint64), ("off_stats", C.c_uint64),
                 ("off_tilecount", C.c_uint64), ("off_cursor", C.c_uint64),
+                ("off_ctainfo", C.c_uint64),
                 ("gaussians", C.c_int64), ("capacity", C.c_int64),
                 ("width", C.c_int32), ("height", C.c_int32), ("grid_w", C.c_int32),
                 ("grid_h", C.c_int32), ("tiles", C.c_int32), ("tile_bits", C.c_int32),
@@ -97,17 +98,19 @@ def _declare(L):
         "fgs_error_string": (C.c_char_p, [C.c_int]),
         "fgs_last_cuda_error": (C.c_char_p, []),
         "fgs_scene_bytes": (C.c_size_t, [i64]),
-        "fgs_scene_pack": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, vp]),
+        "fgs_scene_order_scratch_bytes": (C.c_size_t, [i64]),
+        "fgs_scene_order": (C.c_int, [vp, i64, vp, vp, C.c_size_t, vp]),
+        "fgs_scene_pack": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, vp, vp]),
         "fgs_power_cutoffs": (C.c_int, [vp, i64, dbl, vp, vp]),
         "fgs_workspace_layout": (C.c_int, [i64, i32, i32, i64, lay_p]),
         "fgs_layout_set_sort_mode": (C.c_int, [lay_p, i32]),
         "fgs_workspace_init": (C.c_int, [vp, lay_p, vp]),
         "fgs_preprocess": (C.c_int, [vp, vp, i64, cam_p, dbl, i32, i32, i32, i32, vp, lay_p, vp]),
         "fgs_scan": (C.c_int, [vp, lay_p, vp]),
-        "fgs_emit": (C.c_int, [cam_p, i32, i32, i32, vp, lay_p, vp]),
+        "fgs_emit": (C.c_int, [vp, cam_p, i32, i32, i32, vp, lay_p, vp]),
         "fgs_sort": (C.c_int, [vp, lay_p, u32, vp]),
         "fgs_ranges": (C.c_int, [vp, lay_p, vp]),
-        "fgs_blend": (C.c_int, [f3, dbl, i32, i32, i32, vp, vp, vp, vp, lay_p, vp]),
+        "fgs_blend": (C.c_int, [vp, f3, dbl, i32, i32, i32, vp, vp, vp, vp, lay_p, vp]),
         "fgs_render": (C.c_int, [vp, vp, i64, cam_p, dbl, i32, i32, f3, i32, i32, i32, u32,
                                  vp, vp, vp, vp, lay_p, vp]),
         "fgs_sort_pairs_scratch_bytes": (C.c_size_t, [i64]),

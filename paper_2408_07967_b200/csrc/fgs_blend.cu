@@ -119,7 +119,8 @@ struct BlendSmem {
 template <bool EXACT, bool CONTRIB, bool EXTRAS>
 __global__ void __launch_bounds__(256)
 k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
-        const uint32_t *__restrict__ vals, const int32_t *__restrict__ starts, int width,
+        const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
+        const int32_t *__restrict__ starts, int width,
         int height, int grid_w, int ty_first, float bg0, float bg1, float bg2, float tau,
         float *__restrict__ rgb, float *__restrict__ alpha_out, float *__restrict__ depth_out,
         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
@@ -154,9 +155,13 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
     uint32_t ncontrib = 0;
 
     const int nb = (n + FGS_BLEND_BATCH - 1) / FGS_BLEND_BATCH;
-    // prologue: rows of batch 0 in flight, indices of batch 1 in flight
+    // A pair's value is the caller's Gaussian index; rows live at the Gaussian's slot
+    // (inv: index -> slot, null = identity).  Three steps in flight: values of batch b+3,
+    // their slots for batch b+2, row gathers of batch b+1.
+    const auto slot_of = [&](uint32_t v) { return inv ? inv[v] : v; };
+    // prologue: rows of batch 0 in flight, slots of batch 1, values of batch 2
     if (tid < n) {
-        const uint32_t g = vals[start + tid];
+        const uint32_t g = slot_of(vals[start + tid]);
         const float4 *src = (const float4 *)(splat + (size_t)g * 12);
         cp_async16(&S.row[0][tid][0], src);
         cp_async16(&S.row[0][tid][1], src + 1);
@@ -164,12 +169,13 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         if (EXTRAS) S.z[0][tid] = gdepth ? gdepth[g] : 0.0f;
     }
     cp_async_commit();
-    uint32_t idx_next = (FGS_BLEND_BATCH + tid < n) ? vals[start + FGS_BLEND_BATCH + tid] : 0u;
+    uint32_t idx_next = (FGS_BLEND_BATCH + tid < n) ? slot_of(vals[start + FGS_BLEND_BATCH + tid]) : 0u;
+    uint32_t val_next2 = (2 * FGS_BLEND_BATCH + tid < n) ? vals[start + 2 * FGS_BLEND_BATCH + tid] : 0u;
 
     int b = 0;
     for (; b < nb; ++b) {
         const int cur = b & 1, nxt = cur ^ 1;
-        // step 1: gather the rows of batch b+1 (their indices arrived during batch b-1)
+        // step 1: gather the rows of batch b+1 (their slots arrived during batch b-1)
         if ((b + 1) * FGS_BLEND_BATCH + tid < n) {
             const float4 *src = (const float4 *)(splat + (size_t)idx_next * 12);
             cp_async16(&S.row[nxt][tid][0], src);
@@ -178,9 +184,10 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
             if (EXTRAS) S.z[nxt][tid] = gdepth ? gdepth[idx_next] : 0.0f;
         }
         cp_async_commit();
-        // step 2: indices of batch b+2
-        const int i2 = (b + 2) * FGS_BLEND_BATCH + tid;
-        const uint32_t idx_next2 = i2 < n ? vals[start + i2] : 0u;
+        // step 2: slots of batch b+2 (values arrived during batch b-1), values of batch b+3
+        const uint32_t idx_next2 = ((b + 2) * FGS_BLEND_BATCH + tid < n) ? slot_of(val_next2) : 0u;
+        const int i3 = (b + 3) * FGS_BLEND_BATCH + tid;
+        val_next2 = i3 < n ? vals[start + i3] : 0u;
         if (CONTRIB) S.touched[cur][tid] = 0u;
         cp_async_wait<1>();
         __syncthreads();
@@ -290,15 +297,16 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
 
 template <bool EXACT, bool CONTRIB>
 int launch(bool extras, dim3 grid, cudaStream_t st, const float *splat, const float *gdepth,
-           const uint32_t *vals, const int32_t *starts, int width, int height, int grid_w,
+           const uint32_t *vals, const uint32_t *inv, const int32_t *starts, int width, int height,
+           int grid_w,
            int ty_first, const float bg[3], float tau, float *rgb, float *alpha, float *depth,
            uint8_t *contrib, fgs_stats *stats)
 {
     if (extras)
-        k_blend<EXACT, CONTRIB, true><<<grid, 256, 0, st>>>(splat, gdepth, vals, starts, width,
+        k_blend<EXACT, CONTRIB, true><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, width,
             height, grid_w, ty_first, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
     else
-        k_blend<EXACT, CONTRIB, false><<<grid, 256, 0, st>>>(splat, gdepth, vals, starts, width,
+        k_blend<EXACT, CONTRIB, false><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, width,
             height, grid_w, ty_first, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
@@ -307,7 +315,8 @@ int launch(bool extras, dim3 grid, cudaStream_t st, const float *splat, const fl
 }  // namespace
 
 int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
-                     const int32_t *starts, int width, int height, const float bg[3], double tau,
+                     const uint32_t *inv, const int32_t *starts, int width, int height,
+                     const float bg[3], double tau,
                      int flags, int band0, int band1, float *rgb, float *alpha, float *depth,
                      uint8_t *contrib, fgs_stats *stats, cudaStream_t st)
 {
@@ -318,7 +327,7 @@ int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *va
     const bool extras = (alpha != nullptr) || (depth != nullptr && gdepth != nullptr);
     if (depth != nullptr && gdepth == nullptr) return FGS_E_ARG;
     const float tau32 = (float)tau;
-#define FGS_GO(E, C) launch<E, C>(extras, grid, st, splat, gdepth, vals, starts, width, height, \
+#define FGS_GO(E, C) launch<E, C>(extras, grid, st, splat, gdepth, vals, inv, starts, width, height, \
                                   grid_w, band0, bg, tau32, rgb, alpha, depth, contrib, stats)
     if (exact) return want_contrib ? FGS_GO(true, true) : FGS_GO(true, false);
     return want_contrib ? FGS_GO(false, true) : FGS_GO(false, false);

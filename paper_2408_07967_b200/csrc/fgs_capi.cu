@@ -91,15 +91,50 @@ int32_t fgs_profile_end(void)
 size_t fgs_scene_bytes(int64_t P)
 {
     if (P < 0) return 0;
-    return (size_t)fgs_pad32(P) * 15 * sizeof(float4);
+    return (size_t)fgs_pad32(P) * (15 * sizeof(float4) + 2 * sizeof(uint32_t));
+}
+
+// scratch of fgs_scene_order: [bbox 256 B][codes u64][indices u32][sorted codes u64][sort scratch]
+static inline uint64_t al256(uint64_t b) { return (b + 255) & ~(uint64_t)255; }
+
+size_t fgs_scene_order_scratch_bytes(int64_t P)
+{
+    if (P < 0) return 0;
+    const uint64_t p = (uint64_t)P;
+    return (size_t)(256 + 2 * al256(p * 8) + al256(p * 4) + al256(fgs_sort_pairs_scratch_bytes(P)));
+}
+
+int fgs_scene_order(const float *means, int64_t P, uint32_t *order_out, void *scratch,
+                    size_t scratch_bytes, void *stream)
+{
+    if (P < 0 || P > 0x3fffff00ll) return P < 0 ? FGS_E_ARG : FGS_E_SIZE;
+    if (P == 0) return FGS_OK;
+    if (!means || !order_out || !scratch) return FGS_E_ARG;
+    if (scratch_bytes < fgs_scene_order_scratch_bytes(P)) return FGS_E_WORKSPACE;
+    cudaStream_t st = (cudaStream_t)stream;
+    const uint64_t p = (uint64_t)P;
+    char *b = (char *)scratch;
+    float *bbox = (float *)b;            b += 256;
+    uint64_t *codes = (uint64_t *)b;     b += al256(p * 8);
+    uint32_t *idx = (uint32_t *)b;       b += al256(p * 4);
+    uint64_t *codes_out = (uint64_t *)b; b += al256(p * 8);
+    const size_t sort_bytes = fgs_sort_pairs_scratch_bytes(P);
+    cudaError_t e = cudaMemsetAsync(b, 0, sort_bytes, st);     // look-back table starts clean
+    if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+    int rc = fgs_launch_morton_keys(means, P, bbox, codes, idx, st);
+    if (rc) return rc;
+    // stable LSD sort over code bits [0, 63): ties keep ascending index
+    return fgs_sort_pairs(codes, idx, P, 31, 0, codes_out, order_out, b, sort_bytes, 1u, stream);
 }
 
 int fgs_scene_pack(const float *means, const float *opacities, const float *scales,
-                   const float *rotations, const float *sh, int64_t P, void *packed, void *stream)
+                   const float *rotations, const float *sh, const uint32_t *order, int64_t P,
+                   void *packed, void *stream)
 {
     if (P < 0 || P > 0x7fffff00ll) return P < 0 ? FGS_E_ARG : FGS_E_SIZE;
     if (P && (!means || !opacities || !scales || !rotations || !sh || !packed)) return FGS_E_ARG;
-    return fgs_launch_pack(means, opacities, scales, rotations, sh, P, packed, (cudaStream_t)stream);
+    return fgs_launch_pack(means, opacities, scales, rotations, sh, order, P, packed,
+                           (cudaStream_t)stream);
 }
 
 int fgs_power_cutoffs(const void *packed, int64_t P, double tau, float *k_out, void *stream)
@@ -142,6 +177,7 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     L->off_stats = take(sizeof(fgs_stats));          // stats and tilecount are contiguous:
     L->off_tilecount = take((uint64_t)L->tiles * 4 * FGS_CTR_STRIDE); // one memset clears both
     L->off_cursor = take((uint64_t)L->tiles * 4 * FGS_CTR_STRIDE);
+    L->off_ctainfo = take((uint64_t)L->preprocess_blocks * 16 + 16);
     L->off_splat = take(p * 48);
     L->off_depth = take(p * 4);
     L->off_rects = take(p * 8);
@@ -212,14 +248,16 @@ int fgs_scan(void *ws, const fgs_layout *L, void *stream)
                            (cudaStream_t)stream);
 }
 
-int fgs_emit(const fgs_camera *cam, int32_t strategy, int32_t band0, int32_t band1, void *ws,
-             const fgs_layout *L, void *stream)
+int fgs_emit(const void *packed, const fgs_camera *cam, int32_t strategy, int32_t band0,
+             int32_t band1, void *ws, const fgs_layout *L, void *stream)
 {
     if (!cam || !ws) return FGS_E_ARG;
     int rc = check_frame(L, cam);
     if (rc) return rc;
+    if (L->gaussians && !packed) return FGS_E_ARG;
     if (strategy < 0 || strategy > 2) return FGS_E_STRATEGY;
-    return fgs_launch_emit(L->gaussians, make_cam(cam), strategy, band0, band1,
+    return fgs_launch_emit(fgs_scene_view(packed, L->gaussians), L->gaussians, make_cam(cam),
+                           strategy, band0, band1,
                            L->sort_mode == FGS_SORT_TILE_BUCKET, fgs_frame_view(ws, L),
                            (cudaStream_t)stream);
 }
@@ -245,14 +283,16 @@ int fgs_ranges(void *ws, const fgs_layout *L, void *stream)
                              L->tiles, f.starts, f.stats, (cudaStream_t)stream);
 }
 
-int fgs_blend(const float bg[3], double tau, int32_t flags, int32_t band0, int32_t band1,
-              float *out_rgb, float *out_alpha, float *out_depth, void *ws, const fgs_layout *L,
-              void *stream)
+int fgs_blend(const void *packed, const float bg[3], double tau, int32_t flags, int32_t band0,
+              int32_t band1, float *out_rgb, float *out_alpha, float *out_depth, void *ws,
+              const fgs_layout *L, void *stream)
 {
     if (!bg || !out_rgb || !ws || !L) return FGS_E_ARG;
     if (band0 < 0 || band1 >= L->grid_h) return FGS_E_ARG;
+    if (L->gaussians && !packed) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
-    return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in], f.starts, L->width, L->height,
+    return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in],
+                            fgs_scene_view(packed, L->gaussians).inv, f.starts, L->width, L->height,
                             bg, tau, flags, band0, band1, out_rgb, out_alpha, out_depth, f.contrib,
                             f.stats, (cudaStream_t)stream);
 }
@@ -265,10 +305,11 @@ int fgs_render(const void *packed, const float *k_cut, int64_t P, const fgs_came
     int rc = fgs_preprocess(packed, k_cut, P, cam, tau, sh_degree, strategy, band0, band1, ws, L, stream);
     if (rc) return rc;
     if ((rc = fgs_scan(ws, L, stream))) return rc;
-    if ((rc = fgs_emit(cam, strategy, band0, band1, ws, L, stream))) return rc;
+    if ((rc = fgs_emit(packed, cam, strategy, band0, band1, ws, L, stream))) return rc;
     if ((rc = fgs_sort(ws, L, epoch, stream))) return rc;
     if ((rc = fgs_ranges(ws, L, stream))) return rc;
-    return fgs_blend(bg, tau, blend_flags, band0, band1, out_rgb, out_alpha, out_depth, ws, L, stream);
+    return fgs_blend(packed, bg, tau, blend_flags, band0, band1, out_rgb, out_alpha, out_depth, ws, L,
+                     stream);
 }
 
 // ---- stand-alone stages ------------------------------------------------------
@@ -350,7 +391,7 @@ int fgs_blend_tiles(const float *splat, const float *gaussian_depth, const uint3
     if ((flags & FGS_BLEND_CONTRIB) && (!contrib || !stats)) return FGS_E_ARG;
     const int gh = (height + FGS_TILE - 1) / FGS_TILE;
     if (band0 < 0 || band1 >= gh) return FGS_E_ARG;
-    return fgs_launch_blend(splat, gaussian_depth, sorted_values, starts, width, height, bg, tau,
+    return fgs_launch_blend(splat, gaussian_depth, sorted_values, nullptr, starts, width, height, bg, tau,
                             flags, band0, band1, out_rgb, out_alpha, out_depth, contrib, stats,
                             (cudaStream_t)stream);
 }

@@ -49,11 +49,18 @@ struct CamDev {
     int   width, height, grid_w, grid_h;
 };
 
-// Packed device scene: float4 planes of stride `n` (P rounded up to 32).
+// Packed device scene: float4 planes of stride `n` (P rounded up to 32), in SLOT order.
 //   g0[i] = (mean.xyz, opacity)   g1[i] = (scale.xyz, 0)   g2[i] = quat wxyz
-//   sh[j*n + i] = floats 4j..4j+3 of Gaussian i's 48 SH coefficients
+//   sh[j*n + i] = floats 4j..4j+3 of slot i's 48 SH coefficients
+//   orig[i] = index the caller knows the Gaussian in slot i by;  inv[orig[i]] = i
+// Slot order is the caller's order unless fgs_scene_pack was given a permutation (the
+// Morton order of fgs_scene_order): neighbouring slots are then neighbours in space, so a
+// CTA's Gaussians land on the same few tiles.  Every per-Gaussian frame buffer is indexed
+// by slot; pair records carry `orig` (the reference's value and its tie-break), and the
+// blend maps them back to slots through `inv` in its index prefetch.
 struct SceneDev {
     const float4 *g0, *g1, *g2, *sh;
+    const uint32_t *orig, *inv;
     int64_t n;
 };
 
@@ -68,6 +75,8 @@ static inline SceneDev fgs_scene_view(const void *packed, int64_t P)
     s.g1 = b + s.n;
     s.g2 = b + 2 * s.n;
     s.sh = b + 3 * s.n;
+    s.orig = (const uint32_t *)(b + 15 * s.n);
+    s.inv = s.orig + s.n;
     return s;
 }
 
@@ -91,8 +100,10 @@ struct FrameDev {
     fgs_stats *stats;
     uint32_t *tilecount;    // [tiles]
     uint32_t *cursor;       // [tiles]
-    uint4    *stage;        // TILE_BUCKET: staged pairs, aliases keys[1] + vals[0] + vals[1]
-    uint32_t stage_capacity;
+    uint4    *tablelist;    // TILE_BUCKET: (tile, range base, pairs, slot | wc offset) per
+                            // (CTA, tile); aliases keys[1] + vals[0] + vals[1]
+    uint4    *ctainfo;      // [preprocess blocks] (list base, entries, staged records, 0)
+    uint32_t list_capacity;
 };
 
 static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
@@ -119,23 +130,26 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.stats = (fgs_stats *)(b + L->off_stats);
     f.tilecount = (uint32_t *)(b + L->off_tilecount);
     f.cursor = (uint32_t *)(b + L->off_cursor);
-    f.stage = (uint4 *)(b + L->off_keys[1]);
-    f.stage_capacity = (uint32_t)L->capacity;
+    f.tablelist = (uint4 *)(b + L->off_keys[1]);
+    f.ctainfo = (uint4 *)(b + L->off_ctainfo);
+    f.list_capacity = (uint32_t)L->capacity;
     return f;
 }
 
 // Internal launchers (one translation unit per stage).
 int  fgs_launch_pack(const float *means, const float *opac, const float *scales,
-                     const float *rots, const float *sh, int64_t P, void *packed,
-                     cudaStream_t st);
+                     const float *rots, const float *sh, const uint32_t *order, int64_t P,
+                     void *packed, cudaStream_t st);
+int  fgs_launch_morton_keys(const float *means, int64_t P, float *bbox6, uint64_t *keys,
+                            uint32_t *vals, cudaStream_t st);
 int  fgs_launch_cutoffs(const SceneDev &sc, int64_t P, double tau, float *k, cudaStream_t st);
 int  fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, const CamDev &cam,
                            double tau, int sh_degree, int strategy, int band0, int band1,
                            int bucket, int tiles, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream_t st);
 int  fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st);
-int  fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int band1,
-                     int bucket, const FrameDev &f, cudaStream_t st);
+int  fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
+                     int band1, int bucket, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st);
 
 struct SortPlan {
@@ -152,7 +166,8 @@ int  fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev
 int  fgs_launch_ranges(const uint64_t *keys, const uint32_t *n_dev, int64_t n_max, int tiles,
                        int32_t *starts, fgs_stats *stats, cudaStream_t st);
 int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
-                      const int32_t *starts, int width, int height, const float bg[3],
+                      const uint32_t *inv, const int32_t *starts, int width, int height,
+                      const float bg[3],
                       double tau, int flags, int band0, int band1, float *rgb, float *alpha,
                       float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st);
 

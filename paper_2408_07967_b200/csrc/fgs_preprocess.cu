@@ -27,28 +27,39 @@
 __global__ void __launch_bounds__(128)
 k_scene_pack(const float *__restrict__ means, const float *__restrict__ opac,
              const float *__restrict__ scales, const float *__restrict__ rots,
-             const float *__restrict__ sh, int64_t P, int64_t n, float4 *__restrict__ out)
+             const float *__restrict__ sh, const uint32_t *__restrict__ order, int64_t P,
+             int64_t n, float4 *__restrict__ out)
 {
     // One warp stages 32 Gaussians' 48 SH floats through shared memory so both
-    // the AoS read and the plane-major write are coalesced.
+    // the AoS read and the plane-major write are coalesced.  Slot g holds the
+    // caller's Gaussian order[g] (identity without an order).
     __shared__ float s_sh[4][32 * 48];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int64_t g0 = ((int64_t)blockIdx.x * 4 + w) * 32;
     if (g0 >= n) return;
     const int64_t g = g0 + lane;
     const bool live = g < P;
+    const int64_t src = live ? (order ? (int64_t)order[g] : g) : 0;
     float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = make_float4(1.f, 0.f, 0.f, 0.f);
     if (live) {
-        a = make_float4(means[3 * g], means[3 * g + 1], means[3 * g + 2], opac[g]);
-        b = make_float4(scales[3 * g], scales[3 * g + 1], scales[3 * g + 2], 0.f);
-        c = make_float4(rots[4 * g], rots[4 * g + 1], rots[4 * g + 2], rots[4 * g + 3]);
+        a = make_float4(means[3 * src], means[3 * src + 1], means[3 * src + 2], opac[src]);
+        b = make_float4(scales[3 * src], scales[3 * src + 1], scales[3 * src + 2], 0.f);
+        c = make_float4(rots[4 * src], rots[4 * src + 1], rots[4 * src + 2], rots[4 * src + 3]);
     }
     out[g] = a;
     out[n + g] = b;
     out[2 * n + g] = c;
-    const int64_t nlive = P - g0 < 32 ? P - g0 : 32;       // may be <= 0
-    for (int i = lane; i < 32 * 48; i += 32)
-        s_sh[w][i] = (i < nlive * 48) ? sh[g0 * 48 + i] : 0.f;
+    uint32_t *orig = (uint32_t *)(out + 15 * n), *inv = orig + n;
+    orig[g] = live ? (uint32_t)src : 0xffffffffu;
+    if (live) inv[src] = (uint32_t)g;     // `order` is a permutation: every index written once
+    else inv[g] = 0xffffffffu;            // pad entries (g >= P is never a caller index)
+    const int nlive = P - g0 < 32 ? (int)(P - g0) : 32;       // may be <= 0
+    for (int k = 0; k < 32; ++k) {
+        const int64_t srck = __shfl_sync(FGS_FULL, src, k);
+        const bool lk = k < nlive;
+        s_sh[w][k * 48 + lane] = lk ? sh[srck * 48 + lane] : 0.f;
+        if (lane < 16) s_sh[w][k * 48 + 32 + lane] = lk ? sh[srck * 48 + 32 + lane] : 0.f;
+    }
     __syncwarp();
     float4 *plane = out + 3 * n;
 #pragma unroll
@@ -59,13 +70,100 @@ k_scene_pack(const float *__restrict__ means, const float *__restrict__ opac,
 }
 
 int fgs_launch_pack(const float *means, const float *opac, const float *scales,
-                    const float *rots, const float *sh, int64_t P, void *packed, cudaStream_t st)
+                    const float *rots, const float *sh, const uint32_t *order, int64_t P,
+                    void *packed, cudaStream_t st)
 {
     const int64_t n = fgs_pad32(P);
     if (n == 0) return FGS_OK;
     const int64_t blocks = (n / 32 + 3) / 4;
-    k_scene_pack<<<(unsigned)blocks, 128, 0, st>>>(means, opac, scales, rots, sh, P, n,
+    k_scene_pack<<<(unsigned)blocks, 128, 0, st>>>(means, opac, scales, rots, sh, order, P, n,
                                                    (float4 *)packed);
+    FGS_CHECK_LAUNCH();
+    return FGS_OK;
+}
+
+// ---- spatial order of a scene (per scene, untimed): 63-bit Morton codes of the means over
+// their bounding box; the caller sorts (code, index) with the library's own radix sort.
+__device__ __forceinline__ uint32_t f2ord(float f)
+{
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);      // order-preserving float -> uint
+}
+__device__ __forceinline__ float ord2f(uint32_t u)
+{
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+
+__global__ void __launch_bounds__(256)
+k_bbox(const float *__restrict__ means, int64_t P, uint32_t *__restrict__ box)
+{
+    uint32_t lo[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, hi[3] = {0u, 0u, 0u};
+    for (int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x; g < P; g += (int64_t)gridDim.x * 256)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const float v = means[3 * g + a];
+            if (fabsf(v) <= 3.0e38f) {                       // skip NaN / inf
+                const uint32_t o = f2ord(v);
+                lo[a] = o < lo[a] ? o : lo[a];
+                hi[a] = o > hi[a] ? o : hi[a];
+            }
+        }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = __reduce_min_sync(FGS_FULL, lo[a]);
+        hi[a] = __reduce_max_sync(FGS_FULL, hi[a]);
+    }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            atomicMin(&box[a], lo[a]);
+            atomicMax(&box[3 + a], hi[a]);
+        }
+}
+
+__device__ __forceinline__ uint64_t spread21(uint32_t v)
+{
+    uint64_t x = v & 0x1fffffu;
+    x = (x | x << 32) & 0x1f00000000ffffull;
+    x = (x | x << 16) & 0x1f0000ff0000ffull;
+    x = (x | x << 8) & 0x100f00f00f00f00full;
+    x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+    x = (x | x << 2) & 0x1249249249249249ull;
+    return x;
+}
+
+__global__ void __launch_bounds__(256)
+k_morton_keys(const float *__restrict__ means, int64_t P, const uint32_t *__restrict__ box,
+              uint64_t *__restrict__ keys, uint32_t *__restrict__ vals)
+{
+    const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (g >= P) return;
+    uint32_t q[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const float lo = ord2f(box[a]), hi = ord2f(box[3 + a]);
+        const float v = means[3 * g + a];
+        float t = (hi > lo) ? fd(fs(v, lo), fs(hi, lo)) : 0.0f;
+        t = (t >= 0.0f) ? t : 0.0f;                          // NaN -> 0
+        t = t > 1.0f ? 1.0f : t;
+        q[a] = (uint32_t)fm(t, 2097151.0f);
+    }
+    keys[g] = spread21(q[0]) | (spread21(q[1]) << 1) | (spread21(q[2]) << 2);
+    vals[g] = (uint32_t)g;
+}
+
+int fgs_launch_morton_keys(const float *means, int64_t P, float *bbox6, uint64_t *keys,
+                           uint32_t *vals, cudaStream_t st)
+{
+    if (P == 0) return FGS_OK;
+    uint32_t *box = (uint32_t *)bbox6;
+    cudaError_t e = cudaMemsetAsync(box, 0xff, 3 * sizeof(uint32_t), st);      // minima
+    if (e == cudaSuccess) e = cudaMemsetAsync(box + 3, 0, 3 * sizeof(uint32_t), st);   // maxima
+    if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+    const int64_t want = (P + 255) / 256;
+    k_bbox<<<(unsigned)(want > 1184 ? 1184 : want), 256, 0, st>>>(means, P, box);
+    FGS_CHECK_LAUNCH();
+    k_morton_keys<<<(unsigned)want, 256, 0, st>>>(means, P, box, keys, vals);
     FGS_CHECK_LAUNCH();
     return FGS_OK;
 }
@@ -171,24 +269,76 @@ struct TileJob {
 
 // Walk the warp's candidate tiles 32 at a time.  Returns this lane's number of
 // passing tiles.  MODE selects what happens to a passing (tile, Gaussian):
-//   WALK_COUNT   nothing (count only)                                  (ONESWEEP, K1)
-//   WALK_STAGE   take the pair's rank inside its tile from the tile's counter and
-//                park (tile, rank, depth bits, index) in the stage     (TILE_BUCKET, K1)
+//   WALK_COUNT   nothing (count + pass mask)                           (ONESWEEP, K1)
+//   WALK_BIN     count + pass mask + the CTA's tile table              (TILE_BUCKET, K1)
 //   WALK_EMIT    write (key, value) at out_base(owner) + rank          (ONESWEEP, K3)
-// TILE_BUCKET: the counter's old value IS the pair's slot inside its bucket, so the
-// histogram pass hands every pair its final position relative to the bucket start and K3
-// is a plain placement (no second walk, no second round of atomics).  The atomic's return
-// trip is hidden by parking each window's records in registers until the next window's
-// tests are done.
-enum { WALK_COUNT = 0, WALK_STAGE = 1, WALK_EMIT = 2 };
+//   WALK_PLACE   slot from the CTA's tile table, record into the CTA's
+//                write-combining buffer (or straight to its bucket)    (TILE_BUCKET, K3)
+//
+// TILE_BUCKET binning is a counting sort on the tile index whose unit of work is the CTA,
+// not the pair.  With the scene packed in spatial order a CTA's 256 Gaussians hit a few
+// dozen tiles, so K1 counts pairs per tile in a shared-memory table and reserves ONE
+// range per (CTA, tile) in the tile's bucket (one global atomic per table entry instead
+// of one per pair; L2 serialises atomics per address).  After the scan has fixed the
+// bucket starts, K3 walks again (K1's pass masks make that cheap), ranks each pair inside
+// its (CTA, tile) range with a shared-memory atomic, gathers the CTA's records by tile in
+// shared memory and writes them out as contiguous runs.  Tiles that do not fit the table
+// (caller-order scenes, huge splats) fall back to per-pair global atomics.
+enum { WALK_COUNT = 0, WALK_BIN = 1, WALK_EMIT = 2, WALK_PLACE = 3 };
 
-// Where WALK_STAGE parks its records: a chunk of `total candidates` records per warp,
-// reserved with one atomic on stats->stage_used (passing pairs are packed at its front).
-struct StageOut {
-    uint4 *stage;               // (tile, rank in tile, depth bits, Gaussian index)
-    uint32_t *tile_ctr;         // per-tile counters, FGS_CTR_STRIDE words apart
-    fgs_stats *stats;
-    uint32_t capacity;          // records the stage can hold
+// The CTA's tile table: open addressing, at most FGS_HT_PROBES probes.
+#define FGS_HT_SIZE   1024
+#define FGS_HT_PROBES 16
+#define FGS_HT_EMPTY  0xffffffffu
+#define FGS_WC_CAP    3072          // records the CTA's write-combining buffer holds
+#define FGS_WC_NONE   0xffffu       // table entry whose range is written directly
+struct TileTable {
+    uint32_t key[FGS_HT_SIZE];      // tile index, FGS_HT_EMPTY = free
+    uint32_t val[FGS_HT_SIZE];      // K1: pairs of this CTA on the tile; K3: rank cursor
+};
+
+__device__ __forceinline__ uint32_t ht_hash(uint32_t tile)
+{
+    return (tile * 2654435761u) >> 22;                    // 10 bits
+}
+// slot of `tile`, inserting it if absent; -1 when FGS_HT_PROBES slots are taken by others
+__device__ __forceinline__ int ht_insert(TileTable &T, uint32_t tile)
+{
+    uint32_t h = ht_hash(tile);
+#pragma unroll 1
+    for (int p = 0; p < FGS_HT_PROBES; ++p) {
+        uint32_t k = T.key[h];
+        if (k == FGS_HT_EMPTY) k = atomicCAS(&T.key[h], FGS_HT_EMPTY, tile);
+        if (k == tile || k == FGS_HT_EMPTY) return (int)h;
+        h = (h + 1) & (FGS_HT_SIZE - 1);
+    }
+    return -1;
+}
+// slot of `tile` in a finished table (same probe sequence), -1 if it never got one
+__device__ __forceinline__ int ht_find(const TileTable &T, uint32_t tile)
+{
+    uint32_t h = ht_hash(tile);
+#pragma unroll 1
+    for (int p = 0; p < FGS_HT_PROBES; ++p) {
+        const uint32_t k = T.key[h];
+        if (k == tile) return (int)h;
+        if (k == FGS_HT_EMPTY) return -1;
+        h = (h + 1) & (FGS_HT_SIZE - 1);
+    }
+    return -1;
+}
+
+// What WALK_BIN / WALK_PLACE work on.
+struct BinCtx {
+    TileTable *table;
+    uint32_t *tile_ctr;             // per tile, FGS_CTR_STRIDE words apart: [0] pairs reserved
+                                    // through tables, [1] fallback pairs, [2] fallback cursor
+    // WALK_PLACE only
+    const uint32_t *gbase;          // [FGS_HT_SIZE] bucket position of the entry's range
+    const uint16_t *wcoff;          // [FGS_HT_SIZE] offset in the write-combining buffer
+    uint64_t *wcrec;                // [FGS_WC_CAP]
+    uint32_t *wcdst;                // [FGS_WC_CAP]
+    const int32_t *starts;
 };
 
 // The count walks (K1) also return, in `mask_out`, the pass bits of this lane's first 64
@@ -200,10 +350,10 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
                                                     uint32_t depth_bits, uint32_t gid,
                                                     uint64_t *__restrict__ keys,
                                                     uint32_t *__restrict__ vals,
-                                                    const StageOut *so = nullptr,
+                                                    const BinCtx *bc = nullptr,
                                                     uint64_t *mask_out = nullptr)
 {
-    constexpr bool COUNTING = (MODE == WALK_COUNT || MODE == WALK_STAGE);
+    constexpr bool COUNTING = (MODE == WALK_COUNT || MODE == WALK_BIN);
     const int lane = threadIdx.x & 31;
     const uint32_t incl = warp_incl_scan(job.cand, lane);
     const uint32_t total = __shfl_sync(FGS_FULL, incl, 31);
@@ -212,16 +362,6 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
     uint64_t mymask = 0;
     // K3: does any lane of this warp need the exact test again?
     const bool any_big = !COUNTING && PRECISE && __any_sync(FGS_FULL, job.cand > FGS_MASK_CAND);
-    // WALK_STAGE: the warp's chunk of the stage (lane 0 holds the raw reservation; it is
-    // only broadcast when the first records are flushed, one window later)
-    uint32_t chunk_raw = 0, staged = 0;
-    bool pend = false;
-    uint32_t pend_pos = 0, pend_tile = 0, pend_rank = 0, pend_bits = 0, pend_gid = 0;
-    if (MODE == WALK_STAGE && lane == 0 && total)
-        chunk_raw = atomicAdd(&so->stats->stage_used, total);
-    // unrolled by two so a parked rank needs no register move right behind its atomic
-    // (a move would wait for the return trip on the spot)
-#pragma unroll 2
     for (uint32_t base = 0; base < total; base += 32) {
         const uint32_t j = base + lane;
         // owner = first lane whose inclusive prefix exceeds j
@@ -255,14 +395,11 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             const float b = __shfl_sync(FGS_FULL, job.b, o);
             const float c = __shfl_sync(FGS_FULL, job.c, o);
             const float ke = __shfl_sync(FGS_FULL, job.keff, o);
-            if (COUNTING) {
+            const uint32_t cand_o = COUNTING ? 0u : __shfl_sync(FGS_FULL, job.cand, o);
+            if (COUNTING || cand_o > FGS_MASK_CAND) {
                 const int h = act ? tile_hits32(tx, ty, width, height, cx, cy, a, b, c, ke) : 0;
                 pass = h == 1;
                 if (h == 2) pass = tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
-            } else {
-                const uint32_t cand_o = __shfl_sync(FGS_FULL, job.cand, o);
-                if (cand_o > FGS_MASK_CAND)
-                    pass = act && tile_hits(tx, ty, width, height, cx, cy, a, b, c, ke);
             }
         }
         const uint32_t ballot = __ballot_sync(FGS_FULL, pass);
@@ -279,25 +416,36 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
                 vals[slot] = gid_o;
             }
         }
-        if (MODE == WALK_STAGE) {
+        if (MODE == WALK_BIN) {
+            if (pass) {
+                const uint32_t tile = (uint32_t)(ty * grid_w + tx);
+                const int e = ht_insert(*bc->table, tile);
+                if (e >= 0) atomicAdd(&bc->table->val[e], 1u);
+                else atomicAdd(&bc->tile_ctr[(size_t)tile * FGS_CTR_STRIDE + 1], 1u);
+            }
+        }
+        if (MODE == WALK_PLACE) {
             const uint32_t bits_o = __shfl_sync(FGS_FULL, depth_bits, o);
             const uint32_t gid_o = __shfl_sync(FGS_FULL, gid, o);
-            const uint32_t tile = (uint32_t)(ty * grid_w + tx);
-            uint32_t rank = 0;
-            if (pass) rank = atomicAdd(&so->tile_ctr[(size_t)tile * FGS_CTR_STRIDE], 1u);
-            // flush the previous window: its ranks have had a whole window to come back
-            if (__any_sync(FGS_FULL, pend)) {
-                const uint32_t cb = __shfl_sync(FGS_FULL, chunk_raw, 0);
-                if (pend && cb + total <= so->capacity)
-                    so->stage[cb + pend_pos] = make_uint4(pend_tile, pend_rank, pend_bits, pend_gid);
+            if (pass) {
+                const uint32_t tile = (uint32_t)(ty * grid_w + tx);
+                const uint64_t rec = ((uint64_t)bits_o << 32) | gid_o;
+                const int e = ht_find(*bc->table, tile);
+                if (e >= 0) {
+                    const uint32_t r = atomicAdd(&bc->table->val[e], 1u);
+                    const uint32_t dst = bc->gbase[e] + r;
+                    const uint32_t off = bc->wcoff[e];
+                    if (off != FGS_WC_NONE) {
+                        bc->wcrec[off + r] = rec;
+                        bc->wcdst[off + r] = dst;
+                    } else {
+                        keys[dst] = rec;
+                    }
+                } else {
+                    uint32_t *ctr = bc->tile_ctr + (size_t)tile * FGS_CTR_STRIDE;
+                    keys[(uint32_t)bc->starts[tile] + ctr[0] + atomicAdd(&ctr[2], 1u)] = rec;
+                }
             }
-            pend = pass;
-            pend_pos = staged + __popc(ballot & lanemask_lt());
-            pend_tile = tile;
-            pend_rank = rank;
-            pend_bits = bits_o;
-            pend_gid = gid_o;
-            staged += __popc(ballot);
         }
         // owner side: how many of my candidates in this window passed
         const int lo = excl > base ? (int)(excl - base) : 0;
@@ -305,27 +453,14 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
         if (job.cand && incl > base && lo < hi) {
             const uint32_t m = (hi - lo == 32) ? FGS_FULL : (((1u << (hi - lo)) - 1u) << lo);
             mine += __popc(ballot & m);
-            if (MODE == WALK_COUNT) {
+            if (COUNTING) {
                 // my candidates in this window start at my local index base + lo - excl
                 const uint32_t first = base + (uint32_t)lo - excl;
                 if (first < 64u) mymask |= (uint64_t)((ballot & m) >> lo) << first;
             }
         }
     }
-    if (MODE == WALK_STAGE && total) {
-        const uint32_t cb = __shfl_sync(FGS_FULL, chunk_raw, 0);
-        const bool fits = cb + total <= so->capacity;
-        if (fits) {
-            if (pend)
-                so->stage[cb + pend_pos] = make_uint4(pend_tile, pend_rank, pend_bits, pend_gid);
-            // the chunk was reserved by candidates: mark what the rejected ones left unused,
-            // so the placement kernel can run flat over [0, stage_used)
-            for (uint32_t i = staged + lane; i < total; i += 32) so->stage[cb + i].x = 0xffffffffu;
-        } else if (lane == 0) {
-            so->stats->overflow = 1u;                          // grow and re-run
-        }
-    }
-    if (MODE == WALK_COUNT && mask_out) *mask_out = mymask;
+    if (COUNTING && mask_out) *mask_out = mymask;
     return mine;
 }
 
@@ -369,9 +504,19 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
              int sh_degree, int band0, int band1, FrameDev f)
 {
     __shared__ uint32_t s_red[8];
+    __shared__ TileTable s_tab;           // TILE_BUCKET: this CTA's pairs per tile
+    __shared__ uint32_t s_bin[4], s_scan[8];
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = g < P;
+    if (BUCKET) {
+        for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) {
+            s_tab.key[i] = FGS_HT_EMPTY;
+            s_tab.val[i] = 0u;
+        }
+        if (threadIdx.x == 0) s_bin[2] = 0u;
+        __syncthreads();
+    }
 
     TileJob job;
     job.cand = 0;
@@ -551,13 +696,11 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     uint32_t npairs;
     uint64_t passmask = 0;
     if (BUCKET) {
-        const StageOut so{f.stage, f.tilecount, f.stats, f.stage_capacity};
-        const float d = zcam;
-        npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_STAGE>(
-            job, cam.width, cam.height, cam.grid_w, 0, __float_as_uint(d), (uint32_t)g, nullptr,
-            nullptr, &so);
+        const BinCtx bc{&s_tab, f.tilecount, nullptr, nullptr, nullptr, nullptr, nullptr};
+        npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_BIN>(
+            job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, &bc, &passmask);
         // binning.py:50-51: depths of emitted pairs must be positive and finite
-        if (npairs && !(d < __int_as_float(0x7f800000))) f.stats->bad_depth = 1u;
+        if (npairs && !(zcam < __int_as_float(0x7f800000))) f.stats->bad_depth = 1u;
     } else if (STRAT == FGS_PRECISE)
         npairs = warp_walk_tiles<true, WALK_COUNT>(job, cam.width, cam.height, cam.grid_w, 0, 0, 0,
                                                    nullptr, nullptr, nullptr, &passmask);
@@ -565,7 +708,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         npairs = job.cand;
     if (live) {
         f.counts[g] = npairs;
-        if (!BUCKET && STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
+        if (STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
     }
 
     // block totals: pairs (-> blocksums), retained / degenerate / candidates (-> stats)
@@ -582,13 +725,59 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         if (v1 >> 16) atomicAdd(&f.stats->gaussians_degenerate, v1 >> 16);
         if (v2) atomicAdd((unsigned long long *)&f.stats->candidate_tiles_lo, (unsigned long long)v2);
     }
-    __syncthreads();
+    __syncthreads();                      // also: every warp's walk is done, the table is final
     if (threadIdx.x == 0) {
         uint32_t t = 0;
 #pragma unroll
         for (int i = 0; i < 8; ++i) t += s_red[i];
         f.blocksums[blockIdx.x] = t;
     }
+    if (!BUCKET) return;
+
+    // ---- TILE_BUCKET epilogue: one range per (CTA, tile) in the tile's bucket.  Thread t
+    // owns table slots 4t .. 4t+3; entries go to the frame's table list in slot order, each
+    // with its offset in K3's write-combining buffer (a prefix of the entries fits).
+    uint32_t cnt[4], nent = 0, npr = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int e = threadIdx.x * 4 + k;
+        const bool used = s_tab.key[e] != FGS_HT_EMPTY;
+        cnt[k] = used ? s_tab.val[e] : 0u;
+        nent += used ? 1u : 0u;
+        npr += cnt[k];
+    }
+    uint32_t tot_ent, tot_pr;
+    const uint32_t ent_off = block_excl_scan_256(nent, s_scan, tot_ent);
+    uint32_t pr_off = block_excl_scan_256(npr, s_scan, tot_pr);
+    if (threadIdx.x == 0) {
+        const uint32_t lb = tot_ent ? atomicAdd(&f.stats->list_used, tot_ent) : 0u;
+        s_bin[0] = lb;
+        s_bin[1] = (lb + tot_ent <= f.list_capacity) ? 1u : 0u;
+        if (tot_ent && lb + tot_ent > f.list_capacity) f.stats->overflow = 1u;   // grow and re-run
+    }
+    __syncthreads();
+    const uint32_t list_base = s_bin[0];
+    const bool fits = s_bin[1] != 0u;
+    uint32_t idx = list_base + ent_off, staged_end = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int e = threadIdx.x * 4 + k;
+        const uint32_t tile = s_tab.key[e];
+        if (tile != FGS_HT_EMPTY) {
+            // the counters always get the pairs, so M stays exact when the frame overflows
+            const uint32_t gb = atomicAdd(&f.tilecount[(size_t)tile * FGS_CTR_STRIDE], cnt[k]);
+            const bool wc = pr_off + cnt[k] <= FGS_WC_CAP;
+            if (wc) staged_end = pr_off + cnt[k];
+            if (fits)
+                f.tablelist[idx++] = make_uint4(tile, gb, cnt[k],
+                                                ((uint32_t)e << 16) | (wc ? pr_off : FGS_WC_NONE));
+        }
+        pr_off += cnt[k];
+    }
+    if (staged_end) atomicMax(&s_bin[2], staged_end);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        f.ctainfo[blockIdx.x] = make_uint4(list_base, fits ? tot_ent : 0u, s_bin[2], 0u);
 }
 
 static CamDev g_dummy_cam;   // keeps CamDev's layout in one place for sizeof checks
@@ -707,7 +896,8 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     const int first = blockIdx.x * 1024;
     // prefix of everything before this CTA's slice
     unsigned long long before = 0;
-    for (int i = threadIdx.x; i < first; i += 1024) before += counts[(size_t)i * FGS_CTR_STRIDE];
+    for (int i = threadIdx.x; i < first; i += 1024)
+        before += counts[(size_t)i * FGS_CTR_STRIDE] + counts[(size_t)i * FGS_CTR_STRIDE + 1];
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) before += __shfl_xor_sync(FGS_FULL, before, o);
     if (lane == 0) s_w[w] = before;
@@ -718,7 +908,9 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     __syncthreads();
 
     const int i = first + threadIdx.x;
-    const unsigned long long v = i < tiles ? counts[(size_t)i * FGS_CTR_STRIDE] : 0u;
+    // word 0: pairs reserved through the CTAs' tile tables, word 1: fallback pairs
+    const unsigned long long v = i < tiles ? (unsigned long long)counts[(size_t)i * FGS_CTR_STRIDE] +
+                                                 counts[(size_t)i * FGS_CTR_STRIDE + 1] : 0u;
     unsigned long long incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -751,7 +943,7 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     if (lane == 0 && nonempty) atomicAdd(&stats->tiles_nonempty, nonempty);
     if (i == tiles - 1) {                       // the thread that owns the last tile knows M
         const unsigned long long M = excl + v;
-        // K1 has already raised the flag if some warp's chunk did not fit the stage
+        // K1 has already raised the flag if a CTA's table entries did not fit the list
         const bool over = M > capacity || stats->overflow != 0u;
         stats->pairs_emitted = M > 0xffffffffull ? 0xffffffffu : (uint32_t)M;
         stats->overflow = over ? 1u : 0u;       // later kernels of this frame see it and no-op
@@ -822,45 +1014,106 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
 }
 
 // ---------------------------------------------------------------------------
-// K3 (TILE_BUCKET): place the staged pairs.  K1 parked (tile, rank, depth bits, index)
-// per pair; the scan has since fixed every bucket's start, so a record goes to
-// starts[tile] + rank.  Flat over the reserved part of the stage (unused slots carry
-// tile = ~0), coalesced 16-byte reads, four records in flight per thread.
+// K3 (TILE_BUCKET): second walk.  The CTA reloads its tile table from the frame's list
+// (same slots, so lookups probe exactly as K1's inserts did), ranks every pair inside its
+// (CTA, tile) range with a shared-memory atomic, gathers the records by tile in the
+// write-combining buffer and writes them out as contiguous runs.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256)
-k_place(const uint4 *__restrict__ stage, const int32_t *__restrict__ starts,
-        uint64_t *__restrict__ rec, const fgs_stats *__restrict__ stats)
+struct PlaceSmem {
+    TileTable tab;
+    uint32_t gbase[FGS_HT_SIZE];
+    uint16_t wcoff[FGS_HT_SIZE];
+    uint32_t wcdst[FGS_WC_CAP];
+    uint64_t wcrec[FGS_WC_CAP];
+};
+
+template <int STRAT>
+__global__ void __launch_bounds__(FGS_PRE_THREADS)
+k_place(int P, int width, int height, int grid_w, int band0, int band1,
+        const uint32_t *__restrict__ orig, FrameDev f)
 {
-    if (stats->overflow) return;                         // uniform: grow and re-run
-    const uint32_t n = stats->stage_used;
-    const uint32_t stride = gridDim.x * 256u;
-    for (uint32_t i0 = blockIdx.x * 256u + threadIdx.x; i0 < n; i0 += 4u * stride) {
-        uint4 r[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const uint32_t i = i0 + (uint32_t)k * stride;
-            r[k] = i < n ? stage[i] : make_uint4(0xffffffffu, 0u, 0u, 0u);
-        }
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            if (r[k].x != 0xffffffffu)
-                rec[(uint32_t)starts[r[k].x] + r[k].y] = ((uint64_t)r[k].z << 32) | r[k].w;
+    extern __shared__ __align__(16) unsigned char place_raw[];
+    PlaceSmem &S = *reinterpret_cast<PlaceSmem *>(place_raw);
+    if (f.stats->overflow) return;                       // uniform: grow and re-run
+    const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
+    const bool live = g < P;
+    const uint32_t cnt = live ? f.counts[g] : 0u;
+    if (__syncthreads_or(cnt != 0u) == 0) return;        // uniform per block
+    const uint4 info = f.ctainfo[blockIdx.x];            // (list base, entries, staged records)
+    for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) S.tab.key[i] = FGS_HT_EMPTY;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < info.y; i += FGS_PRE_THREADS) {
+        const uint4 ent = f.tablelist[info.x + i];       // (tile, range base, pairs, slot | wc offset)
+        const uint32_t e = ent.w >> 16;
+        S.tab.key[e] = ent.x;
+        S.tab.val[e] = 0u;
+        S.gbase[e] = (uint32_t)f.starts[ent.x] + ent.y;
+        S.wcoff[e] = (uint16_t)(ent.w & 0xffffu);
     }
+    __syncthreads();
+
+    TileJob job;
+    job.cand = 0;
+    job.cx = job.cy = job.a = job.b = job.c = job.keff = 0.f;
+    job.tx0 = job.ty0 = 0;
+    job.nx = 1;
+    job.mask = 0;
+    uint32_t bits = 0;
+    if (cnt) {
+        const ushort4 r = f.rects[g];
+        const int by0 = (int)r.y > band0 ? (int)r.y : band0;
+        const int by1 = (int)r.w < band1 ? (int)r.w : band1;
+        job.tx0 = r.x; job.ty0 = by0; job.nx = (int)r.z - (int)r.x + 1;
+        job.cand = (uint32_t)job.nx * (uint32_t)(by1 - by0 + 1);
+        if (STRAT == FGS_PRECISE) {
+            if (job.cand <= FGS_MASK_CAND) {
+                job.mask = f.passmask[g];                 // K1's verdicts, no test needed
+            } else {
+                const float4 *row = (const float4 *)(f.splat + (size_t)g * 12);
+                const float4 r0 = row[0], r1 = row[1], r2 = row[2];
+                const float k = r1.z, hx = r2.z, hy = r2.w;
+                // binning.py:187-193 conservative cutoff for the exact test
+                const float ex = fa(hx, 16.0f), ey = fa(hy, 16.0f);
+                const float term = fa(fa(fm(fm(r0.z, ex), ex), fm(fm(fm(2.0f, fabsf(r0.w)), ex), ey)),
+                                      fm(fm(r1.x, ey), ey));
+                job.keff = fa(k, fm(FGS_CUTOFF_SLACK, term));
+                job.cx = r0.x; job.cy = r0.y; job.a = r0.z; job.b = r0.w; job.c = r1.x;
+            }
+        }
+        bits = __float_as_uint(f.depth[g]);
+    }
+    const BinCtx bc{&S.tab, f.tilecount, S.gbase, S.wcoff, S.wcrec, S.wcdst, f.starts};
+    // records carry the caller's Gaussian index: the reference's pair value and tie-break
+    warp_walk_tiles<STRAT == FGS_PRECISE, WALK_PLACE>(job, width, height, grid_w, 0, bits,
+                                                      cnt ? orig[g] : 0u, f.keys[0], nullptr, &bc);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < info.z; i += FGS_PRE_THREADS) f.keys[0][S.wcdst[i]] = S.wcrec[i];
 }
 
-int fgs_launch_emit(int64_t P, const CamDev &cam, int strategy, int band0, int band1,
-                    int bucket, const FrameDev &f, cudaStream_t st)
+int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
+                    int band1, int bucket, const FrameDev &f, cudaStream_t st)
 {
     if (P == 0) return FGS_OK;
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     if (bucket) {
-        // sized from the capacity (the record count lives on the device)
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const int64_t want = (f.stage_capacity + 1023) / 1024;
-        const unsigned grid = (unsigned)(want < 1 ? 1 : (want > sms * 8 ? sms * 8 : want));
-        k_place<<<grid, 256, 0, st>>>(f.stage, f.starts, f.keys[0], f.stats);
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaError_t e = cudaFuncSetAttribute(k_place<FGS_PRECISE>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)sizeof(PlaceSmem));
+            if (e == cudaSuccess)
+                e = cudaFuncSetAttribute(k_place<FGS_TIGHT_AABB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(PlaceSmem));
+            if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+            attr_set = true;
+        }
+        if (strategy == FGS_PRECISE)
+            k_place<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, sizeof(PlaceSmem), st>>>(
+                (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
+        else
+            k_place<FGS_TIGHT_AABB><<<blocks, FGS_PRE_THREADS, sizeof(PlaceSmem), st>>>(
+                (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
     } else if (strategy == FGS_PRECISE) {
         k_emit<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, 0, st>>>(
             (int)P, cam.width, cam.height, cam.grid_w, band0, band1, f);

@@ -200,10 +200,20 @@ class Pipeline:
     sort on the packed tile|depth key).  Both give the bit-identical sorted list.
     """
 
-    def __init__(self, scene, sh_degree=3, device=None, sort_mode="tile-bucket"):
+    def __init__(self, scene, sh_degree=3, device=None, sort_mode="tile-bucket",
+                 spatial_order=None):
         if sort_mode not in _capi.SORT_MODES:
             raise ValueError(f"unknown sort_mode {sort_mode!r}, expected one of {tuple(_capi.SORT_MODES)}")
         self.sort_mode = sort_mode
+        # Slots in Morton order make a CTA's Gaussians hit the same few tiles: the binning
+        # kernels then reserve bucket ranges per (CTA, tile) and write contiguous runs, and
+        # the blend's gathers get denser.  Results do not depend on it.  The one-sweep
+        # sort's tie order needs the identity order.
+        if spatial_order is None:
+            spatial_order = sort_mode == "tile-bucket"
+        if spatial_order and sort_mode != "tile-bucket":
+            raise ValueError("spatial_order needs sort_mode='tile-bucket'")
+        self.spatial_order = bool(spatial_order)
         if is_raw_scene(scene):
             act = activate(scene)
         elif is_activated_scene(scene):
@@ -226,10 +236,23 @@ class Pipeline:
             sh = f32(act.sh, (P, 48))
             self.scene_bytes = int(L.fgs_scene_bytes(P))
             self.packed = torch.empty(max(self.scene_bytes, 16), dtype=torch.uint8, device=self.device)
+            st = _stream_ptr(torch, self.device)
+            order = None
+            if self.spatial_order and P:
+                order = torch.empty(P, dtype=torch.int32, device=self.device)
+                nbytes = int(L.fgs_scene_order_scratch_bytes(P))
+                scratch = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+                _capi.check(L.fgs_scene_order(means.data_ptr(), P, order.data_ptr(),
+                                              scratch.data_ptr(), nbytes, st))
             _capi.check(L.fgs_scene_pack(means.data_ptr(), opac.data_ptr(), scales.data_ptr(),
-                                         rots.data_ptr(), sh.data_ptr(), P,
-                                         self.packed.data_ptr(), _stream_ptr(torch, self.device)))
+                                         rots.data_ptr(), sh.data_ptr(),
+                                         order.data_ptr() if order is not None else None, P,
+                                         self.packed.data_ptr(), st))
             torch.cuda.current_stream(self.device).synchronize()
+            # slot -> caller index, for mapping slot-indexed results back at the boundary
+            self.slot_order = (order.cpu().numpy().view(np.uint32).astype(np.int64)
+                               if order is not None else None)
+            del order
         self._kcut = {}
         self._free = {}
         self._lock = threading.Lock()
@@ -327,14 +350,15 @@ class Pipeline:
                 _capi.check(L.fgs_preprocess(self.packed.data_ptr(), kcut.data_ptr(), self.count,
                                              C.byref(cam), float(tau), deg, sid, b0, b1, base, lay, st))
                 _capi.check(L.fgs_scan(base, lay, st))
-                _capi.check(L.fgs_emit(C.byref(cam), sid, b0, b1, base, lay, st))
+                _capi.check(L.fgs_emit(self.packed.data_ptr(), C.byref(cam), sid, b0, b1, base, lay, st))
                 if timing:
                     ev[1].record()
                 _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
                 _capi.check(L.fgs_ranges(base, lay, st))
                 if timing:
                     ev[2].record()
-                _capi.check(L.fgs_blend(bg_c, float(tau), flags, b0, b1, ws.rgb.data_ptr(),
+                _capi.check(L.fgs_blend(self.packed.data_ptr(), bg_c, float(tau), flags, b0, b1,
+                                        ws.rgb.data_ptr(),
                                         a_ptr, d_ptr, base, lay, st))
                 if timing:
                     ev[3].record()
@@ -360,7 +384,7 @@ class Pipeline:
                 if int(s["overflow"]):
                     # binning.py:134-143: grow, never truncate; counted in the stats
                     stats.buffer_regrows += 1
-                    need = max(int(s["pairs_emitted"]), int(s["stage_used"]))
+                    need = max(int(s["pairs_emitted"]), int(s["list_used"]))
                     capacity = max(int(capacity * 1.5) + 16, need + need // 8 + 4096)
                     if h_rgb is not None:
                         _pinned.give(h_rgb)
@@ -514,13 +538,13 @@ def sorted_pairs(pipe, camera, strategy="precise", tau=TAU_DEFAULT, band=None):
                                          C.byref(cam), float(tau), _check_sh_degree(pipe.sh_degree),
                                          sid, b0, b1, base, lay, st))
             _capi.check(L.fgs_scan(base, lay, st))
-            _capi.check(L.fgs_emit(C.byref(cam), sid, b0, b1, base, lay, st))
+            _capi.check(L.fgs_emit(pipe.packed.data_ptr(), C.byref(cam), sid, b0, b1, base, lay, st))
             _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
             _capi.check(L.fgs_ranges(base, lay, st))
             s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
             if int(s["overflow"]):
                 capacity = max(int(capacity * 1.5) + 16,
-                               max(int(s["pairs_emitted"]), int(s["stage_used"])) + 4096)
+                               max(int(s["pairs_emitted"]), int(s["list_used"])) + 4096)
                 continue
             break
         M, lay = int(s["pairs_emitted"]), ws.lay
@@ -609,7 +633,7 @@ def power_cutoffs(alpha0, tau=TAU_DEFAULT):
     t = [torch.from_numpy(x).to(dev) for x in (z3, a, z3, z4, zs)]
     packed = torch.empty(max(int(L.fgs_scene_bytes(n)), 16), dtype=torch.uint8, device=dev)
     st = _stream_ptr(torch, dev)
-    _capi.check(L.fgs_scene_pack(*[x.data_ptr() for x in t], n, packed.data_ptr(), st))
+    _capi.check(L.fgs_scene_pack(*[x.data_ptr() for x in t], None, n, packed.data_ptr(), st))
     k = torch.empty(max(n, 1), dtype=torch.float32, device=dev)
     _capi.check(L.fgs_power_cutoffs(packed.data_ptr(), n, float(tau), k.data_ptr(), st))
     return k[:n].cpu().numpy(), a > np.float32(tau)
@@ -647,11 +671,11 @@ def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, worke
             _capi.check(L.fgs_preprocess(pipe.packed.data_ptr(), kcut.data_ptr(), P, C.byref(cam),
                                          float(tau), deg, sid, b0, b1, base, lay, st))
             _capi.check(L.fgs_scan(base, lay, st))
-            _capi.check(L.fgs_emit(C.byref(cam), sid, b0, b1, base, lay, st))
+            _capi.check(L.fgs_emit(pipe.packed.data_ptr(), C.byref(cam), sid, b0, b1, base, lay, st))
             s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
             if int(s["overflow"]):
                 regrows += 1
-                need = max(int(s["pairs_emitted"]), int(s["stage_used"]))
+                need = max(int(s["pairs_emitted"]), int(s["list_used"]))
                 capacity = max(int(capacity * 1.5) + 16, need)
                 continue
             break
@@ -679,6 +703,14 @@ def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, worke
             vals = ws.view(torch, lay.off_vals[0], M * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
         cap = ws.capacity
         pipe._give_ws(ws)
+    if pipe.slot_order is not None:
+        # per-Gaussian frame buffers are indexed by slot: row of Gaussian slot_order[slot]
+        def by_index(a):
+            out = np.empty_like(a)
+            out[pipe.slot_order] = a
+            return out
+        flags, retained, splat, depth, rects, counts = (
+            by_index(x) for x in (flags, retained, splat, depth, rects, counts))
     nx = rects[:, 2] - rects[:, 0] + 1
     ny = rects[:, 3] - rects[:, 1] + 1
     return BinOutput(

@@ -116,7 +116,9 @@ def test_c1_survey_fingerprints(golden_c1):
 ])
 def test_oracle_parity_all_stages(preset, n, seed, w, h, radius, tau, deg, bg):
     act = fgs.activate(fgs.gen_synthetic(preset, n, seed))
-    pipe = fgs.Pipeline(act, sh_degree=deg)
+    pipe = fgs.Pipeline(act, sh_degree=deg)                          # tile-bucket, Morton slots
+    pipe1 = fgs.Pipeline(act, sh_degree=deg, sort_mode="onesweep")   # identity slots
+    assert pipe.spatial_order and not pipe1.spatial_order
     for cam in fgs.orbit_cameras(2, radius, w, h):
         for s in STRATS:
             ob = orc.preprocess_and_bin(act, cam, s, tau, deg)
@@ -127,7 +129,7 @@ def test_oracle_parity_all_stages(preset, n, seed, w, h, radius, tau, deg, bg):
             assert np.all(np.diff((tb.keys >> np.uint64(32)).astype(np.int64)) >= 0)
             tk, tv = _sorted_pairs(tb, n)
             assert np.array_equal(tk, ok) and np.array_equal(tv, ov)
-            gb = fgs.preprocess_and_bin(pipe, cam, s, tau, sh_degree=deg, sort_mode="onesweep")
+            gb = fgs.preprocess_and_bin(pipe1, cam, s, tau, sh_degree=deg)
             assert np.array_equal(gb.retained, ob.retained)
             assert np.array_equal(gb.depth.view(np.uint32), ob.depth.view(np.uint32))
             assert np.array_equal(gb.splat.view(np.uint32), ob.splat.view(np.uint32))
@@ -473,3 +475,63 @@ def test_frame_service_render_pose():
                 dict(req, width=8, height=8)):
         with pytest.raises(service.PoseError):
             svc.render_pose(bad)
+
+
+# ---------------------------------------------------------------------------
+# spatial slot order (per scene): a pure layout choice, results must not move
+# ---------------------------------------------------------------------------
+def _morton63(means):
+    m = np.asarray(means, dtype=np.float32)
+    lo, hi = m.min(axis=0), m.max(axis=0)
+    with np.errstate(invalid="ignore", divide="ignore"):
+        t = (m - lo) / (hi - lo)
+    t = np.where(hi > lo, t, np.float32(0)).astype(np.float32)
+    t = np.clip(t, np.float32(0), np.float32(1))
+    q = (t * np.float32(2097151.0)).astype(np.uint64)
+    code = np.zeros(m.shape[0], dtype=np.uint64)
+    for bit in range(21):
+        for a in range(3):
+            code |= ((q[:, a] >> np.uint64(bit)) & np.uint64(1)) << np.uint64(3 * bit + a)
+    return code
+
+
+@pytest.mark.parametrize("n", [1, 31, 1000, 70001])
+def test_scene_order_is_the_stable_morton_permutation(n):
+    act = fgs.activate(fgs.gen_synthetic("mixed", n, 21))
+    pipe = fgs.Pipeline(act)
+    assert pipe.spatial_order and pipe.slot_order.shape == (n,)
+    assert np.array_equal(np.sort(pipe.slot_order), np.arange(n))
+    want = np.lexsort((np.arange(n), _morton63(act.means)))
+    assert np.array_equal(pipe.slot_order, want)
+
+
+@pytest.mark.parametrize("preset,n,w,h,radius", [("mixed", 9000, 400, 240, 16.0),
+                                                 ("isotropic", 300, 640, 368, 9.5),    # huge splats
+                                                 ("elongated", 20000, 512, 288, 12.0)])
+def test_results_do_not_depend_on_slot_order(preset, n, w, h, radius):
+    """Morton slots (CTA tile tables mostly hit) against caller-order slots (tables overflow,
+    per-pair fallback path): same frames, same sorted lists, same stage outputs."""
+    act = fgs.activate(fgs.gen_synthetic(preset, n, 17))
+    cam = fgs.orbit_cameras(1, radius, w, h)[0]
+    a = fgs.Pipeline(act, spatial_order=True)
+    b = fgs.Pipeline(act, spatial_order=False)
+    for exact in (False, True):
+        fa, sa = a.render(cam, exact=exact, extras=True)
+        fb, sb = b.render(cam, exact=exact, extras=True)
+        assert np.array_equal(fa.image.view(np.uint32), fb.image.view(np.uint32))
+        assert np.array_equal(fa.alpha.view(np.uint32), fb.alpha.view(np.uint32))
+        assert np.array_equal(fa.depth.view(np.uint32), fb.depth.view(np.uint32))
+        assert (sa.pairs_emitted, sa.pairs_contributing, sa.tiles_nonempty) == \
+               (sb.pairs_emitted, sb.pairs_contributing, sb.tiles_nonempty)
+    for s in STRATS:
+        ka, va, ta = fgs.sorted_pairs(a, cam, s)
+        kb, vb, tb = fgs.sorted_pairs(b, cam, s)
+        assert np.array_equal(ka, kb) and np.array_equal(va, vb) and np.array_equal(ta, tb)
+        ob = orc.preprocess_and_bin(act, cam, s)
+        ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, n)
+        assert np.array_equal(ka, ok) and np.array_equal(va, ov)
+    ba, bb = fgs.preprocess_and_bin(a, cam), fgs.preprocess_and_bin(b, cam)
+    assert np.array_equal(ba.splat.view(np.uint32), bb.splat.view(np.uint32))
+    assert np.array_equal(ba.pair_counts, bb.pair_counts)
+    with pytest.raises(ValueError):
+        fgs.Pipeline(act, sort_mode="onesweep", spatial_order=True)

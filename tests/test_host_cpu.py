@@ -65,12 +65,16 @@ def test_workspace_layout_is_host_only_and_consistent(lib):
             lay.off_starts, lay.off_contrib]
     assert offs == sorted(offs) and all(o % 256 == 0 for o in offs)
     assert lay.total_bytes > lay.off_contrib + 8_000_000 - 256
+    # keys[1] | vals[0] | vals[1] are contiguous: the (CTA, tile) table list lives there
+    assert lay.off_vals[0] == lay.off_keys[1] + 8 * lay.capacity
+    assert lay.off_vals[1] == lay.off_vals[0] + 4 * lay.capacity
+    assert _capi.layout(10, 64, 64, 1000).capacity == 1024              # rounded up to 64
     assert _capi.layout(10_000_000, 7680, 4320, 1 << 20).sort_passes == 6   # 31 + 17 bits
     with pytest.raises(_capi.FgsError):
         _capi.layout(10, 64, 64, 1 << 31)                                   # FGS_E_SIZE
     with pytest.raises(_capi.FgsError):
         _capi.layout(-1, 64, 64, 10)
-    assert lib.fgs_scene_bytes(1000) == 1024 * 240
+    assert lib.fgs_scene_bytes(1000) == 1024 * 248
 
 
 def test_no_cpu_fallback():
