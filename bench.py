@@ -232,9 +232,9 @@ def main():
     ws = wss[0]
     lay = ws.lay
     npass = 0 if bucket else int(lay.sort_passes)
-    # kernels per frame: bucket  K1 K2 K3 tile_sort(small, medium, dense, hard) K6 ;
+    # kernels per frame: bucket  K1 K2 K3 tile_sort(small, medium, large, dense, hard) K6 ;
     #                     onesweep  K1 K2 K3 hist pass*npass K5 K6
-    n_marks = 8 if bucket else 6 + npass
+    n_marks = 9 if bucket else 6 + npass
     camc = _capi.camera_struct(cam)
     kcut = pipe._cutoffs(torch, 1.0 / 255.0)
     bg = (C.c_float * 3)(0.0, 0.0, 0.0)
@@ -362,7 +362,7 @@ def main():
     if rank == 0:
         if bucket:
             names = ["preprocess", "scan", "emit", "tile_sort", "tile_sort_medium",
-                     "tile_sort_dense", "tile_sort_hard", "blend"]
+                     "tile_sort_large", "tile_sort_dense", "tile_sort_hard", "blend"]
         else:
             names = ["preprocess", "scan", "emit", "sort_hist"] \
                 + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
@@ -393,7 +393,7 @@ def main():
         sort_ms = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass")))
         cand = {"blend": kmean[-1], "sort_pass": sort_ms, "preprocess": kmean[0], "emit": kmean[2]}
         if bucket:
-            cand["tile_sort"] = kmean[3] + kmean[4] + kmean[5] + kmean[6]
+            cand["tile_sort"] = float(kmean[3:8].sum())
         dom = max(cand, key=cand.get)
         if dom == "sort_pass":
             per_launch_ms = sort_ms / npass
@@ -415,11 +415,11 @@ def main():
                             "sm__inst_executed_pipe_fma / issue-slot utilisation from ncu"}
         else:
             idx = {"preprocess": 0, "emit": 2, "tile_sort": 3}[dom]
-            ms = float(kmean[idx] + (kmean[4] + kmean[5] + kmean[6] if dom == "tile_sort" else 0.0))
+            ms = float(kmean[3:8].sum() if dom == "tile_sort" else kmean[idx])
             ach = alg[dom] / (ms * 1e-3) / 1e9
             roof = {"kernel": "k_" + dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                     "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                    "launches_per_step": 4 if dom == "tile_sort" else 1, "ms_per_launch": ms,
+                    "launches_per_step": 5 if dom == "tile_sort" else 1, "ms_per_launch": ms,
                     "alg_bytes_per_launch": alg[dom]}
         roof["peak_source"] = peak_src
 

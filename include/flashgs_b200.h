@@ -100,7 +100,7 @@ typedef struct fgs_stats {
     uint32_t tile_out_of_grid;     /* sorting.py:150-151                    */
     uint32_t candidate_tiles_lo;   /* sum of nx*ny over retained, low/high  */
     uint32_t candidate_tiles_hi;
-    uint32_t dense_tiles;          /* TILE_BUCKET: tiles with > 4096 pairs       */
+    uint32_t dense_tiles;          /* TILE_BUCKET: tiles with > 8192 pairs       */
     uint32_t medium_tiles;         /* TILE_BUCKET: tiles with 1025..4096 pairs   */
     uint32_t hard_tiles;           /* TILE_BUCKET: tiles sent to the radix fallback */
     uint32_t list_used;            /* TILE_BUCKET: (CTA, tile) table entries of the frame;
@@ -156,7 +156,7 @@ const char *fgs_last_cuda_error(void);
  * (cudaEvent_t handles, caller-owned) on the launch stream.  fgs_profile_end
  * disarms and returns how many were recorded.  Frame order: preprocess, scan,
  * emit, then (ONESWEEP) sort histogram, one per sort pass, ranges, or
- * (TILE_BUCKET) tile sort for small, medium, dense, hard buckets; then blend. */
+ * (TILE_BUCKET) tile sort for small, medium, large, dense, hard buckets; then blend. */
 void    fgs_profile_begin(void **events, int32_t n_events);
 int32_t fgs_profile_end(void);
 

@@ -36,7 +36,14 @@
 // the dense list.  The lists live in spare words of the cursor slots: dense entry i
 // at cursor[i*FGS_CTR_STRIDE + 1], medium entry i at cursor[i*FGS_CTR_STRIDE + 2]
 #define FGS_SMALL_TILE    1024
-#define FGS_DENSE_TILE    4096
+#define FGS_DENSE_TILE    4096      // medium: 1025..4096
+#define FGS_LARGE_TILE    8192      // large: 4097..8192; beyond: dense (entry i of the large
+                                    // list at cursor[i*FGS_CTR_STRIDE + 4])
+// internal work counters live behind the public 64-byte stats block (the block is 256
+// bytes in the workspace and zeroed with it at the start of every frame)
+#define FGS_WORK_LARGE    0
+static __host__ __device__ inline uint32_t *fgs_work(fgs_stats *s) { return (uint32_t *)(s + 1); }
+static __host__ __device__ inline const uint32_t *fgs_work(const fgs_stats *s) { return (const uint32_t *)(s + 1); }
 
 // Camera as the kernels see it (passed by value: lives in the constant bank).
 struct CamDev {

@@ -789,8 +789,9 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
 {
     (void)g_dummy_cam;
     // stats and (TILE_BUCKET) the per-tile histogram sit back to back: one memset
+    // the stats block is 256 bytes in the workspace: public counters + internal work counters
     const size_t zero_bytes = bucket ? (size_t)((char *)(f.tilecount + (size_t)tiles * FGS_CTR_STRIDE) - (char *)f.stats)
-                                     : sizeof(fgs_stats);
+                                     : 256;
     cudaError_t e = cudaMemsetAsync(f.stats, 0, zero_bytes, st);
     if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
     if (P == 0) return FGS_OK;
@@ -934,8 +935,10 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     if (i < tiles) {
         const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
         starts[i] = (int32_t)e32;
-        if (v > FGS_DENSE_TILE)     // queue the bucket for its tile-sort size class
+        if (v > FGS_LARGE_TILE)     // queue the bucket for its tile-sort size class
             cursor[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE + 1] = (uint32_t)i;
+        else if (v > FGS_DENSE_TILE)
+            cursor[(size_t)atomicAdd(&fgs_work(stats)[FGS_WORK_LARGE], 1u) * FGS_CTR_STRIDE + 4] = (uint32_t)i;
         else if (v > FGS_SMALL_TILE)
             cursor[(size_t)atomicAdd(&stats->medium_tiles, 1u) * FGS_CTR_STRIDE + 2] = (uint32_t)i;
     }

@@ -329,7 +329,7 @@ __device__ __forceinline__ void ts_bitonic_smem(uint64_t *s, int npad)
 // equal-depth fix-up.  Every thread of the CTA calls it with the same arguments.
 template <int NT, int EMAX>
 __device__ __forceinline__ void ts_sort_small(TileSortSmem<NT, EMAX> &S,
-                                              const uint64_t *__restrict__ src, int m, int npass)
+                                              const uint64_t *src, int m, int npass)
 {
     constexpr int TS_E = EMAX;
     constexpr int WARPS = NT / 32;
@@ -467,6 +467,146 @@ __device__ __noinline__ void ts_bitonic_global(TileSortSmem<NT, EMAX> &S, uint64
     }
 }
 
+// ---- bucket-rank sort: the fast path for buckets of up to 4096 records -------------
+// Depths inside a tile are spread fairly evenly between the tile's nearest and
+// farthest splat, so a monotone linear map of the depth bits onto NB = CAP/4 bins
+// leaves a handful of records per bin.  One shared-memory atomic per record builds
+// the bin histogram (its return value is the record's slot inside the bin), a scan
+// turns it into bin offsets, the records are scattered bin-contiguously, and each
+// record then ranks itself inside its bin by comparing the full 64-bit word with
+// the bin's few other members -- which also settles equal depths by index.  Six
+// barriers per tile instead of twenty, no serial LDS -> match -> STS chains.
+// A tile where some bin holds more than TB_MAXBIN records (many equal or tightly
+// clustered depths) is pushed on the "hard" list and sorted by the radix kernel.
+constexpr int TB_MAXBIN = 64;
+
+// STAGE: keep a copy of the input records in shared memory (steps 2 and 4 read it);
+// without it they re-read the bucket through L1/L2 and the capacity doubles.
+template <int NT, int EMAX, bool STAGE = true>
+struct BucketSmem {
+    static constexpr int CAP = NT * EMAX;
+    static constexpr int NB = CAP / 4;
+    uint64_t a[STAGE ? CAP : 1];
+    uint64_t b[CAP];
+    uint32_t bin[NB + 1];
+    uint32_t red[64];
+};
+
+// Sorts the n <= CAP records at g; the result goes to vals_out / keys_out [start, start+n).
+// Returns false (nothing written) when the records have to go to the radix fallback.
+// Every thread of the CTA calls it with the same arguments.
+template <int NT, int EMAX, bool STAGE = true>
+__device__ __forceinline__ bool tb_sort_range(BucketSmem<NT, EMAX, STAGE> &S, const uint64_t *g,
+                                              int n, int start, uint64_t tile_hi,
+                                              uint32_t *__restrict__ vals_out,
+                                              uint64_t *__restrict__ keys_out, int write_keys)
+{
+    // (g is not __restrict__: a split bucket's chunks were written by this very CTA)
+    constexpr int NB = BucketSmem<NT, EMAX, STAGE>::NB;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+
+    // 1. stage the records, depth range of the tile
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = tid; i < n; i += NT) {
+        const uint64_t r = g[i];
+        if (STAGE) S.a[i] = r;
+        const uint32_t d = (uint32_t)(r >> 32);
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+    }
+    for (int i = tid; i <= NB; i += NT) S.bin[i] = 0u;
+    lo = __reduce_min_sync(FGS_FULL, lo);
+    hi = __reduce_max_sync(FGS_FULL, hi);
+    if (lane == 0) { S.red[w] = lo; S.red[32 + w] = hi; }
+    __syncthreads();
+    lo = 0xffffffffu; hi = 0u;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+        lo = S.red[i] < lo ? S.red[i] : lo;
+        hi = S.red[32 + i] > hi ? S.red[32 + i] : hi;
+    }
+    const uint32_t range = hi - lo;
+    const bool direct = range < (uint32_t)NB;                 // one depth value per bin
+    const uint64_t inv = direct ? 0ull : ((uint64_t)NB << 32) / ((uint64_t)range + 1ull);
+#define TB_BIN(d) (direct ? (d) - lo : (uint32_t)(((uint64_t)((d) - lo) * inv) >> 32))
+
+    // 2. histogram; the atomic's return value is the record's slot inside its bin
+    uint16_t slot[EMAX];
+    bool too_big = false;
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const int i = tid + k * NT;
+        if (i < n) {
+            const uint32_t d = (uint32_t)((STAGE ? S.a[i] : g[i]) >> 32);
+            const uint32_t sl = atomicAdd(&S.bin[1 + TB_BIN(d)], 1u);
+            slot[k] = (uint16_t)sl;
+            too_big |= sl >= (uint32_t)TB_MAXBIN;
+        }
+    }
+    if (__syncthreads_or(too_big)) return false;
+
+    // 3. bin offsets: inclusive scan of bin[1..NB] in place (bin[0] = 0)
+    {
+        constexpr int PER = (NB + NT - 1) / NT;               // consecutive bins per thread
+        uint32_t v[PER], sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = 1 + tid * PER + k;
+            v[k] = idx <= NB ? S.bin[idx] : 0u;
+            sum += v[k];
+        }
+        uint32_t incl = warp_incl_scan(sum, lane);
+        if (lane == 31) S.red[w] = incl;
+        __syncthreads();
+        uint32_t wsum = lane < NT / 32 ? S.red[lane] : 0u;
+        uint32_t wincl = warp_incl_scan(wsum, lane);
+        uint32_t run = __shfl_sync(FGS_FULL, wincl - wsum, w) + incl - sum;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int idx = 1 + tid * PER + k;
+            run += v[k];
+            if (idx <= NB) S.bin[idx] = run;
+        }
+    }
+    __syncthreads();
+
+    // 4. scatter bin-contiguously
+#pragma unroll
+    for (int k = 0; k < EMAX; ++k) {
+        const int i = tid + k * NT;
+        if (i < n) {
+            const uint64_t r = STAGE ? S.a[i] : g[i];
+            S.b[S.bin[TB_BIN((uint32_t)(r >> 32))] + slot[k]] = r;
+        }
+    }
+    __syncthreads();
+
+    // 5. rank inside the bin by full-word comparison; write straight to the output
+    for (int i = tid; i < n; i += NT) {
+        const uint64_t r = S.b[i];
+        const uint32_t bn = TB_BIN((uint32_t)(r >> 32));
+        const int b0 = (int)S.bin[bn], b1 = (int)S.bin[bn + 1];
+        int rank = 0;
+        for (int j = b0; j < b1; ++j) rank += S.b[j] < r ? 1 : 0;
+        vals_out[start + b0 + rank] = (uint32_t)r;
+        if (write_keys) keys_out[start + b0 + rank] = tile_hi | (r >> 32);
+    }
+#undef TB_BIN
+    return true;
+}
+
+template <int NT, int EMAX, bool STAGE = true>
+__device__ __forceinline__ bool tb_sort_tile(BucketSmem<NT, EMAX, STAGE> &S, int tile,
+                                             const uint64_t *__restrict__ rec,
+                                             uint32_t *__restrict__ vals_out,
+                                             uint64_t *__restrict__ keys_out,
+                                             const int32_t *__restrict__ starts, int write_keys)
+{
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    return tb_sort_range<NT, EMAX, STAGE>(S, rec + start, n, start, (uint64_t)(uint32_t)tile << 32,
+                                          vals_out, keys_out, write_keys);
+}
+
 // One bucket.  Every thread of the CTA calls it with the same arguments.  With
 // SPLIT = false the caller guarantees n <= CAP (and the split code is not compiled
 // in, which keeps the hot kernel inside the instruction cache).
@@ -475,7 +615,8 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
                                              uint64_t *__restrict__ rec,
                                              uint64_t *__restrict__ alt, uint32_t *__restrict__ vals_out,
                                              uint64_t *__restrict__ keys_out,
-                                             const int32_t *__restrict__ starts, int write_keys)
+                                             const int32_t *__restrict__ starts, int write_keys,
+                                             BucketSmem<NT, EMAX> *B = nullptr)
 {
     constexpr int CAP = TileSortSmem<NT, EMAX>::CAP;
     const int tid = threadIdx.x;
@@ -538,6 +679,14 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
         const int m = split ? (int)S.sub[S.grp[k + 1]] - b0 : n;
         if (m == 0) continue;                                 // uniform
         if (!SPLIT || m <= CAP) {
+            // chunks of a split bucket span a narrow depth range: the one-pass bucket-rank
+            // sort almost always takes them; the four-pass radix is the fallback
+            if (SPLIT && B != nullptr &&
+                tb_sort_range<NT, EMAX>(*B, src + b0, m, start + b0, tile_hi, vals_out, keys_out,
+                                        write_keys)) {
+                __syncthreads();
+                continue;
+            }
             ts_sort_small<NT, EMAX>(S, src + b0, m, 4);
             for (int i = tid; i < m; i += NT) {
                 const uint64_t r = s[i];
@@ -556,138 +705,13 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
     }
 }
 
-// ---- bucket-rank sort: the fast path for buckets of up to 4096 records -------------
-// Depths inside a tile are spread fairly evenly between the tile's nearest and
-// farthest splat, so a monotone linear map of the depth bits onto NB = CAP/4 bins
-// leaves a handful of records per bin.  One shared-memory atomic per record builds
-// the bin histogram (its return value is the record's slot inside the bin), a scan
-// turns it into bin offsets, the records are scattered bin-contiguously, and each
-// record then ranks itself inside its bin by comparing the full 64-bit word with
-// the bin's few other members -- which also settles equal depths by index.  Six
-// barriers per tile instead of twenty, no serial LDS -> match -> STS chains.
-// A tile where some bin holds more than TB_MAXBIN records (many equal or tightly
-// clustered depths) is pushed on the "hard" list and sorted by the radix kernel.
-constexpr int TB_MAXBIN = 64;
-
-template <int NT, int EMAX>
-struct BucketSmem {
-    static constexpr int CAP = NT * EMAX;
-    static constexpr int NB = CAP / 4;
-    uint64_t a[CAP];
-    uint64_t b[CAP];
-    uint32_t bin[NB + 1];
-    uint32_t red[64];
-};
-
-// Returns false (tile untouched) when the tile has to go to the radix fallback.
-template <int NT, int EMAX>
-__device__ __forceinline__ bool tb_sort_tile(BucketSmem<NT, EMAX> &S, int tile,
-                                             const uint64_t *__restrict__ rec,
-                                             uint32_t *__restrict__ vals_out,
-                                             uint64_t *__restrict__ keys_out,
-                                             const int32_t *__restrict__ starts, int write_keys)
-{
-    constexpr int NB = BucketSmem<NT, EMAX>::NB;
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int start = starts[tile], n = starts[tile + 1] - start;
-    const uint64_t *g = rec + start;
-    const uint64_t tile_hi = (uint64_t)(uint32_t)tile << 32;
-
-    // 1. stage the records, depth range of the tile
-    uint32_t lo = 0xffffffffu, hi = 0u;
-    for (int i = tid; i < n; i += NT) {
-        const uint64_t r = g[i];
-        S.a[i] = r;
-        const uint32_t d = (uint32_t)(r >> 32);
-        lo = d < lo ? d : lo;
-        hi = d > hi ? d : hi;
-    }
-    for (int i = tid; i <= NB; i += NT) S.bin[i] = 0u;
-    lo = __reduce_min_sync(FGS_FULL, lo);
-    hi = __reduce_max_sync(FGS_FULL, hi);
-    if (lane == 0) { S.red[w] = lo; S.red[32 + w] = hi; }
-    __syncthreads();
-    lo = 0xffffffffu; hi = 0u;
-#pragma unroll
-    for (int i = 0; i < NT / 32; ++i) {
-        lo = S.red[i] < lo ? S.red[i] : lo;
-        hi = S.red[32 + i] > hi ? S.red[32 + i] : hi;
-    }
-    const uint32_t range = hi - lo;
-    const bool direct = range < (uint32_t)NB;                 // one depth value per bin
-    const uint64_t inv = direct ? 0ull : ((uint64_t)NB << 32) / ((uint64_t)range + 1ull);
-#define TB_BIN(d) (direct ? (d) - lo : (uint32_t)(((uint64_t)((d) - lo) * inv) >> 32))
-
-    // 2. histogram; the atomic's return value is the record's slot inside its bin
-    uint16_t slot[EMAX];
-    bool too_big = false;
-#pragma unroll
-    for (int k = 0; k < EMAX; ++k) {
-        const int i = tid + k * NT;
-        if (i < n) {
-            const uint32_t d = (uint32_t)(S.a[i] >> 32);
-            const uint32_t sl = atomicAdd(&S.bin[1 + TB_BIN(d)], 1u);
-            slot[k] = (uint16_t)sl;
-            too_big |= sl >= (uint32_t)TB_MAXBIN;
-        }
-    }
-    if (__syncthreads_or(too_big)) return false;
-
-    // 3. bin offsets: inclusive scan of bin[1..NB] in place (bin[0] = 0)
-    {
-        constexpr int PER = (NB + NT - 1) / NT;               // consecutive bins per thread
-        uint32_t v[PER], sum = 0;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int idx = 1 + tid * PER + k;
-            v[k] = idx <= NB ? S.bin[idx] : 0u;
-            sum += v[k];
-        }
-        uint32_t incl = warp_incl_scan(sum, lane);
-        if (lane == 31) S.red[w] = incl;
-        __syncthreads();
-        uint32_t wsum = lane < NT / 32 ? S.red[lane] : 0u;
-        uint32_t wincl = warp_incl_scan(wsum, lane);
-        uint32_t run = __shfl_sync(FGS_FULL, wincl - wsum, w) + incl - sum;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int idx = 1 + tid * PER + k;
-            run += v[k];
-            if (idx <= NB) S.bin[idx] = run;
-        }
-    }
-    __syncthreads();
-
-    // 4. scatter bin-contiguously
-#pragma unroll
-    for (int k = 0; k < EMAX; ++k) {
-        const int i = tid + k * NT;
-        if (i < n) {
-            const uint64_t r = S.a[i];
-            S.b[S.bin[TB_BIN((uint32_t)(r >> 32))] + slot[k]] = r;
-        }
-    }
-    __syncthreads();
-
-    // 5. rank inside the bin by full-word comparison; write straight to the output
-    for (int i = tid; i < n; i += NT) {
-        const uint64_t r = S.b[i];
-        const uint32_t bn = TB_BIN((uint32_t)(r >> 32));
-        const int b0 = (int)S.bin[bn], b1 = (int)S.bin[bn + 1];
-        int rank = 0;
-        for (int j = b0; j < b1; ++j) rank += S.b[j] < r ? 1 : 0;
-        vals_out[start + b0 + rank] = (uint32_t)r;
-        if (write_keys) keys_out[start + b0 + rank] = tile_hi | (r >> 32);
-    }
-#undef TB_BIN
-    return true;
-}
-
 // Size classes (k_scan_tiles sorts the tiles into them):
 //   small   n <= 1024   one CTA per tile, bucket-rank sort
 //   medium  n <= 4096   persistent CTAs over the medium list, bucket-rank sort
-//   hard    n <= 4096   tiles the bucket-rank sort gave up on: radix sort
-//   dense   n >  4096   512 threads, radix sort with 8192-record capacity, split beyond
+//   large   n <= 8192   512 threads, bucket-rank sort without the staging copy
+//   hard    n <= 4096   small / medium tiles the bucket-rank sort gave up on: radix sort
+//   dense   n >  8192   (and large tiles that gave up) one counting pass on the top varying
+//                       depth bits, then each chunk of <= 4096 by bucket-rank (radix fallback)
 __global__ void __launch_bounds__(256, 6)
 k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
             uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
@@ -722,6 +746,26 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     }
 }
 
+__global__ void __launch_bounds__(512, 2)
+k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
+                  uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
+                  const uint32_t *__restrict__ list, uint32_t *__restrict__ dense_list,
+                  int write_keys, fgs_stats *__restrict__ stats)
+{
+    extern __shared__ __align__(16) unsigned char ts_raw[];
+    using Smem = BucketSmem<512, 16, false>;
+    Smem &S = *reinterpret_cast<Smem *>(ts_raw);
+    if (stats->overflow) return;
+    const uint32_t count = fgs_work(stats)[FGS_WORK_LARGE];
+    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
+        if (!tb_sort_tile<512, 16, false>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+            threadIdx.x == 0)      // clustered depths: let the splitting kernel take it
+            dense_list[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+        __syncthreads();
+    }
+}
+
 template <int NT, int EMAX, bool SPLIT, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
 k_tile_sort_list(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
@@ -732,11 +776,15 @@ k_tile_sort_list(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
     TileSortSmem<NT, EMAX> &S = *reinterpret_cast<TileSortSmem<NT, EMAX> *>(ts_raw);
+    // the splitting kernel carries a bucket-rank work area behind the radix one
+    BucketSmem<NT, EMAX> *B = SPLIT ? reinterpret_cast<BucketSmem<NT, EMAX> *>(
+                                          ts_raw + ((sizeof(TileSortSmem<NT, EMAX>) + 15) & ~size_t(15)))
+                                    : nullptr;
     if (stats->overflow) return;
     const uint32_t count = *list_len;
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
         ts_sort_tile<NT, EMAX, SPLIT>(S, (int)list[(size_t)i * FGS_CTR_STRIDE], rec, alt, vals_out,
-                                      keys_out, starts, write_keys);
+                                      keys_out, starts, write_keys, B);
         __syncthreads();
     }
 }
@@ -747,10 +795,13 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
 {
     if (tiles <= 0) return FGS_OK;
     auto hard = k_tile_sort_list<256, 16, false, 3>;
-    auto dense = k_tile_sort_list<512, 16, true, 2>;
+    auto dense = k_tile_sort_list<256, 16, true, 2>;
     using MediumSmem = BucketSmem<256, 16>;
+    using LargeSmem = BucketSmem<512, 16, false>;
+    static_assert(LargeSmem::CAP == FGS_LARGE_TILE, "large class = large capacity");
     using HardSmem = TileSortSmem<256, 16>;
-    using DenseSmem = TileSortSmem<512, 16>;
+    using DenseSmem = TileSortSmem<256, 16>;
+    constexpr size_t dense_bytes = ((sizeof(DenseSmem) + 15) & ~size_t(15)) + sizeof(BucketSmem<256, 16>);
     static_assert(BucketSmem<256, 4>::CAP == FGS_SMALL_TILE, "small class = small capacity");
     static_assert(MediumSmem::CAP == FGS_DENSE_TILE && HardSmem::CAP == FGS_DENSE_TILE,
                   "dense threshold = medium capacity");
@@ -769,8 +820,9 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         };
         prep((const void *)k_tile_sort, 0);
         prep((const void *)k_tile_sort_medium, sizeof(MediumSmem));
+        prep((const void *)k_tile_sort_large, sizeof(LargeSmem));
         prep((const void *)hard, sizeof(HardSmem));
-        prep((const void *)dense, sizeof(DenseSmem));
+        prep((const void *)dense, dense_bytes);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         int dev = 0;
         cudaGetDevice(&dev);
@@ -779,6 +831,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     }
     // lists in the spare words of the cursor slots: +1 dense, +2 medium, +3 hard
     uint32_t *dense_list = f.cursor + 1, *medium_list = f.cursor + 2, *hard_list = f.cursor + 3;
+    uint32_t *large_list = f.cursor + 4;
     k_tile_sort<<<(unsigned)tiles, 256, 0, st>>>(f.keys[0], f.vals[0], f.keys[1], f.starts,
                                                  hard_list, write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);
@@ -787,7 +840,10 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);
     const unsigned dgrid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);
-    dense<<<dgrid, 512, sizeof(DenseSmem), st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
+    k_tile_sort_large<<<dgrid, 512, sizeof(LargeSmem), st>>>(
+        f.keys[0], f.vals[0], f.keys[1], f.starts, large_list, dense_list, write_keys, f.stats);
+    FGS_AFTER_LAUNCH(st);
+    dense<<<dgrid, 256, dense_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
                                                  f.starts, dense_list, &f.stats->dense_tiles,
                                                  write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);

@@ -535,3 +535,22 @@ def test_results_do_not_depend_on_slot_order(preset, n, w, h, radius):
     assert np.array_equal(ba.pair_counts, bb.pair_counts)
     with pytest.raises(ValueError):
         fgs.Pipeline(act, sort_mode="onesweep", spatial_order=True)
+
+
+def test_overlapped_views_match_one_at_a_time_on_dense_tiles():
+    """Views in flight on several streams (render_many) against render() one at a time, on a
+    scene whose tiles span every tile-sort size class (small ... dense)."""
+    act = fgs.activate(fgs.gen_synthetic("mixed", 150_000, 23))
+    cams = fgs.orbit_cameras(6, 22.0, 480, 272)
+    pipe = fgs.Pipeline(act)
+    ref = [pipe.render(c, exact=True) for c in cams]
+    sizes = np.diff(fgs.sorted_pairs(pipe, cams[0])[2])
+    assert sizes.max() > 8192 and ((sizes > 4096) & (sizes <= 8192)).any() and (sizes < 1024).any()
+    for streams in (2, 3):
+        for rep in range(3):
+            got = pipe.render_many(cams, exact=True, streams=streams, depth=2 * streams)
+            for (fa, sa), (fb, sb) in zip(ref, got):
+                assert np.array_equal(fa.image.view(np.uint32), fb.image.view(np.uint32))
+                assert (sa.pairs_emitted, sa.pairs_contributing) == (sb.pairs_emitted, sb.pairs_contributing)
+    oimg, ost = orc.render(act, cams[0])
+    assert np.array_equal(ref[0][0].image.view(np.uint32), oimg.view(np.uint32))
