@@ -54,7 +54,11 @@ WORKLOADS = {
            "BASELINE configs[3]: 10M Gaussians (density-scaled), SH3, 7680x4320"),
     "c4-4k": (10_000_000, 3840, 2160, True,
               "north_star target: 10M Gaussians (density-scaled), SH3, 3840x2160"),
+    "c5": (3_000_000, 1920, 1080, True,
+           "BASELINE configs[4]: 64-view batch of a 3M-Gaussian scene (density-scaled), SH3, "
+           "1920x1080, views sharded over the ranks"),
 }
+VIEWS = {"c5": 64}       # workloads that are a batch of distinct views (orbit cameras)
 METRIC, UNIT = "views_per_sec", "views/s"
 
 
@@ -202,9 +206,12 @@ def main():
 
     act, W, H, desc = make_scene(fgs, args.workload)
     P = act.count
-    ncam = max(world, 1)
+    nviews = VIEWS.get(args.workload, 0)
+    ncam = nviews if nviews else max(world, 1)
     cams = fgs.orbit_cameras(ncam, 24.0, W, H)
     cam = cams[0] if args.mode == "bands" else cams[rank % ncam]
+    # a view batch: this rank's share of the views (view v -> rank v mod world), cycled
+    my_cams = [cams[v] for v in sharding.views_for_rank(ncam, world, rank)] if nviews else [cam]
     gh = -(-H // 16)
     band = None
     bands = sharding.band_partition(gh, world)
@@ -232,25 +239,26 @@ def main():
     ws = wss[0]
     lay = ws.lay
     npass = 0 if bucket else int(lay.sort_passes)
-    # kernels per frame: bucket  K1 K2 K3 tile_sort(small, medium, large, dense, hard) K6 ;
+    # kernels per frame: bucket  K1 K2 K3 tile_sort(small, medium, large, tail) K6 ;
     #                     onesweep  K1 K2 K3 hist pass*npass K5 K6
-    n_marks = 9 if bucket else 6 + npass
-    camc = _capi.camera_struct(cam)
+    n_marks = 8 if bucket else 6 + npass
+    camcs = [_capi.camera_struct(c) for c in my_cams]
     kcut = pipe._cutoffs(torch, 1.0 / 255.0)
     bg = (C.c_float * 3)(0.0, 0.0, 0.0)
     flags = (_capi.BLEND_EXACT if args.exact else 0) | _capi.BLEND_CONTRIB
     b0, b1 = band if band is not None else (0, gh - 1)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
 
-    def frame(lane=0):
+    def frame(lane=0, view=0):
         w_ = wss[lane]
-        _capi.check(L.fgs_render(pipe.packed.data_ptr(), kcut.data_ptr(), P, C.byref(camc),
+        _capi.check(L.fgs_render(pipe.packed.data_ptr(), kcut.data_ptr(), P,
+                                 C.byref(camcs[view % len(camcs)]),
                                  1.0 / 255.0, 3, 0, bg, flags, b0, b1, w_.next_epoch(),
                                  w_.rgb.data_ptr(), None, None, C.c_void_p(w_.base),
                                  C.byref(w_.lay), C.c_void_p(lanes[lane].cuda_stream)))
 
     for i in range(max(args.warmup, 2 * nlanes)):
-        frame(i % nlanes)
+        frame(i % nlanes, i)
     torch.cuda.synchronize(dev)
 
     # ---- pass A: one frame at a time, per-kernel CUDA events (latency + roofline) --
@@ -297,7 +305,7 @@ def main():
     for ln in lanes[1:]:
         ln.wait_event(t_begin)
     for i in range(K):
-        frame(i % nlanes)
+        frame(i % nlanes, i)
     for ln, e in zip(lanes, t_ends):
         e.record(ln)
     torch.cuda.synchronize(dev)
@@ -326,7 +334,8 @@ def main():
         # the batch call a views/s user makes: K views through Pipeline.render_many
         # (frame i's read-back overlaps frame i+1's kernels)
         nfr = 0
-        for fb, st_e in pipe.render_iter([cam] * K, exact=args.exact, streams=nlanes):
+        for fb, st_e in pipe.render_iter([my_cams[i % len(my_cams)] for i in range(K)],
+                                         exact=args.exact, streams=nlanes):
             assert fb.image.shape == (H, W, 3)      # frame is in host memory here
             nfr += 1
         assert nfr == K
@@ -362,7 +371,7 @@ def main():
     if rank == 0:
         if bucket:
             names = ["preprocess", "scan", "emit", "tile_sort", "tile_sort_medium",
-                     "tile_sort_large", "tile_sort_dense", "tile_sort_hard", "blend"]
+                     "tile_sort_large", "tile_sort_tail", "blend"]
         else:
             names = ["preprocess", "scan", "emit", "sort_hist"] \
                 + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
@@ -393,7 +402,7 @@ def main():
         sort_ms = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass")))
         cand = {"blend": kmean[-1], "sort_pass": sort_ms, "preprocess": kmean[0], "emit": kmean[2]}
         if bucket:
-            cand["tile_sort"] = float(kmean[3:8].sum())
+            cand["tile_sort"] = float(kmean[3:-1].sum())
         dom = max(cand, key=cand.get)
         if dom == "sort_pass":
             per_launch_ms = sort_ms / npass
@@ -415,11 +424,11 @@ def main():
                             "sm__inst_executed_pipe_fma / issue-slot utilisation from ncu"}
         else:
             idx = {"preprocess": 0, "emit": 2, "tile_sort": 3}[dom]
-            ms = float(kmean[3:8].sum() if dom == "tile_sort" else kmean[idx])
+            ms = float(kmean[3:-1].sum() if dom == "tile_sort" else kmean[idx])
             ach = alg[dom] / (ms * 1e-3) / 1e9
             roof = {"kernel": "k_" + dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                     "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                    "launches_per_step": 5 if dom == "tile_sort" else 1, "ms_per_launch": ms,
+                    "launches_per_step": 4 if dom == "tile_sort" else 1, "ms_per_launch": ms,
                     "alg_bytes_per_launch": alg[dom]}
         roof["peak_source"] = peak_src
 
@@ -437,7 +446,7 @@ def main():
                        "pairs": M, "retained": R, "tiles": T_tiles, "sort_mode": args.sort_mode,
                        "sort_passes": npass,
                        "blend": "exact" if args.exact else "ex2.approx+guard",
-                       "streams": nlanes,
+                       "streams": nlanes, "distinct_views": len(my_cams) * (world if nviews else 1),
                        "l2": "timed steps: inputs larger than L2 -- every view re-reads the 240 MB "
                              "packed scene and rewrites its own ~150 MB workspace, %d views in "
                              "flight, 126 MB L2; latency/roofline pass: 256 MiB buffer written "

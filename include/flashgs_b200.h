@@ -156,7 +156,8 @@ const char *fgs_last_cuda_error(void);
  * (cudaEvent_t handles, caller-owned) on the launch stream.  fgs_profile_end
  * disarms and returns how many were recorded.  Frame order: preprocess, scan,
  * emit, then (ONESWEEP) sort histogram, one per sort pass, ranges, or
- * (TILE_BUCKET) tile sort for small, medium, large, dense, hard buckets; then blend. */
+ * (TILE_BUCKET) tile sort for small, medium, large buckets and the dense + hard tail; then
+ * blend. */
 void    fgs_profile_begin(void **events, int32_t n_events);
 int32_t fgs_profile_end(void);
 
@@ -205,7 +206,8 @@ int fgs_workspace_layout(int64_t gaussians, int32_t width, int32_t height,
 int fgs_layout_set_sort_mode(fgs_layout *layout_host, int32_t sort_mode);
 
 /* Must be called once after the workspace is allocated (zeroes the sort
- * look-back table, whose entries are epoch-tagged afterwards). */
+ * look-back table, whose entries are epoch-tagged afterwards).  Asynchronous on
+ * `stream` like every call: a frame issued on ANOTHER stream must wait for it. */
 int fgs_workspace_init(void *workspace, const fgs_layout *layout_host, void *stream);
 
 /* binning.py:197-257 preprocess_and_bin, phase A + the count half of phase B:

@@ -766,25 +766,29 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     }
 }
 
-template <int NT, int EMAX, bool SPLIT, int MINB>
-__global__ void __launch_bounds__(NT, MINB)
-k_tile_sort_list(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
+// The tail of the tile sort, one launch: the dense list (split path), then the hard list
+// (small / medium buckets the bucket-rank sort gave up on: radix path, no second try).
+__global__ void __launch_bounds__(256, 2)
+k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
                  uint32_t *__restrict__ vals_out, uint64_t *__restrict__ keys_out,
-                 const int32_t *__restrict__ starts, const uint32_t *__restrict__ list,
-                 const uint32_t *__restrict__ list_len, int write_keys,
+                 const int32_t *__restrict__ starts, const uint32_t *__restrict__ dense_list,
+                 const uint32_t *__restrict__ hard_list, int write_keys,
                  const fgs_stats *__restrict__ stats)
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
-    TileSortSmem<NT, EMAX> &S = *reinterpret_cast<TileSortSmem<NT, EMAX> *>(ts_raw);
-    // the splitting kernel carries a bucket-rank work area behind the radix one
-    BucketSmem<NT, EMAX> *B = SPLIT ? reinterpret_cast<BucketSmem<NT, EMAX> *>(
-                                          ts_raw + ((sizeof(TileSortSmem<NT, EMAX>) + 15) & ~size_t(15)))
-                                    : nullptr;
+    using Radix = TileSortSmem<256, 16>;
+    Radix &S = *reinterpret_cast<Radix *>(ts_raw);
+    // a bucket-rank work area behind the radix one, for the chunks of split buckets
+    BucketSmem<256, 16> *B = reinterpret_cast<BucketSmem<256, 16> *>(
+        ts_raw + ((sizeof(Radix) + 15) & ~size_t(15)));
     if (stats->overflow) return;
-    const uint32_t count = *list_len;
-    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
-        ts_sort_tile<NT, EMAX, SPLIT>(S, (int)list[(size_t)i * FGS_CTR_STRIDE], rec, alt, vals_out,
-                                      keys_out, starts, write_keys, B);
+    const uint32_t ndense = stats->dense_tiles, nhard = stats->hard_tiles;
+    for (uint32_t i = blockIdx.x; i < ndense + nhard; i += gridDim.x) {
+        const bool dense = i < ndense;
+        const int tile = (int)(dense ? dense_list[(size_t)i * FGS_CTR_STRIDE]
+                                     : hard_list[(size_t)(i - ndense) * FGS_CTR_STRIDE]);
+        ts_sort_tile<256, 16, true>(S, tile, rec, alt, vals_out, keys_out, starts, write_keys,
+                                    dense ? B : nullptr);
         __syncthreads();
     }
 }
@@ -794,17 +798,14 @@ k_tile_sort_list(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
 int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st)
 {
     if (tiles <= 0) return FGS_OK;
-    auto hard = k_tile_sort_list<256, 16, false, 3>;
-    auto dense = k_tile_sort_list<256, 16, true, 2>;
     using MediumSmem = BucketSmem<256, 16>;
     using LargeSmem = BucketSmem<512, 16, false>;
     static_assert(LargeSmem::CAP == FGS_LARGE_TILE, "large class = large capacity");
-    using HardSmem = TileSortSmem<256, 16>;
-    using DenseSmem = TileSortSmem<256, 16>;
-    constexpr size_t dense_bytes = ((sizeof(DenseSmem) + 15) & ~size_t(15)) + sizeof(BucketSmem<256, 16>);
+    using TailRadix = TileSortSmem<256, 16>;
+    constexpr size_t tail_bytes = ((sizeof(TailRadix) + 15) & ~size_t(15)) + sizeof(BucketSmem<256, 16>);
     static_assert(BucketSmem<256, 4>::CAP == FGS_SMALL_TILE, "small class = small capacity");
-    static_assert(MediumSmem::CAP == FGS_DENSE_TILE && HardSmem::CAP == FGS_DENSE_TILE,
-                  "dense threshold = medium capacity");
+    static_assert(MediumSmem::CAP == FGS_DENSE_TILE && TailRadix::CAP == FGS_DENSE_TILE,
+                  "medium capacity = radix capacity = chunk size of split buckets");
     static bool attr_set = false;
     static int sms = 148;
     if (!attr_set) {
@@ -813,7 +814,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
             if (e == cudaSuccess && smem)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             // largest shared-memory carve-out, or the occupancy the launch bounds assume
-            // (6 x 17 KB, 3 x 69 KB, 3 x 43 KB, 2 x 83 KB per SM) is not reached
+            // (6 x 17 KB, 3 x 69 KB, 2 x 73 KB, 2 x 112 KB per SM) is not reached
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          cudaSharedmemCarveoutMaxShared);
@@ -821,8 +822,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         prep((const void *)k_tile_sort, 0);
         prep((const void *)k_tile_sort_medium, sizeof(MediumSmem));
         prep((const void *)k_tile_sort_large, sizeof(LargeSmem));
-        prep((const void *)hard, sizeof(HardSmem));
-        prep((const void *)dense, dense_bytes);
+        prep((const void *)k_tile_sort_tail, tail_bytes);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         int dev = 0;
         cudaGetDevice(&dev);
@@ -843,12 +843,9 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     k_tile_sort_large<<<dgrid, 512, sizeof(LargeSmem), st>>>(
         f.keys[0], f.vals[0], f.keys[1], f.starts, large_list, dense_list, write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);
-    dense<<<dgrid, 256, dense_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
-                                                 f.starts, dense_list, &f.stats->dense_tiles,
-                                                 write_keys, f.stats);
-    FGS_AFTER_LAUNCH(st);
-    hard<<<mgrid, 256, sizeof(HardSmem), st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1], f.starts,
-                                               hard_list, &f.stats->hard_tiles, write_keys, f.stats);
+    k_tile_sort_tail<<<dgrid, 256, tail_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
+                                                     f.starts, dense_list, hard_list, write_keys,
+                                                     f.stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }

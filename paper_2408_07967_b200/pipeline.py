@@ -168,6 +168,9 @@ class _Workspace:
         self.epoch = 1
         _capi.check(_capi.lib().fgs_workspace_init(C.c_void_p(self.base), C.byref(self.lay),
                                                    _stream_ptr(torch, device)))
+        # The workspace may be used on another stream next (render_iter's lanes): its
+        # initialisation must not still be running then.  Creation is rare; wait here.
+        torch.cuda.current_stream(device).synchronize()
 
     def set_mode(self, sort_mode, keep_sorted_keys=False):
         _capi.check(_capi.lib().fgs_layout_set_sort_mode(C.byref(self.lay), int(sort_mode)))
