@@ -71,6 +71,22 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)", 1965.0
 
 
+def profiled_kernels(workload):
+    """Per-kernel numbers of the newest committed ncu capture of `workload`."""
+    import glob
+    best = {}
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json"))):
+        try:
+            with open(path) as f:
+                d = json.load(f)
+        except (OSError, ValueError):
+            continue
+        if d.get("workload") == workload:
+            best = dict(d.get("kernels", {}))
+            best["_file"] = os.path.relpath(path, ROOT)
+    return best
+
+
 class ClockSampler:
     """Samples SM clock / throttle reasons through NVML while the timed region runs."""
 
@@ -398,6 +414,16 @@ def main():
                 ent["gbs"] = alg[nme] / (ms * 1e-3) / 1e9
                 ent["frac_hbm"] = ent["gbs"] / hbm_peak
             kernels.append(ent)
+        ncu_name = {"preprocess": "k_preprocess", "scan": "k_scan_tiles", "emit": "k_place",
+                    "tile_sort": "k_tile_sort", "tile_sort_medium": "k_tile_sort_medium",
+                    "tile_sort_large": "k_tile_sort_large", "tile_sort_tail": "k_tile_sort_tail",
+                    "blend": "k_blend"}
+        prof_all = profiled_kernels(args.workload)
+        for ent in kernels:
+            for k, v in prof_all.items():
+                if isinstance(v, dict) and k.split("<")[0] == ncu_name.get(ent["name"]):
+                    ent["ncu_dram_bytes"] = v["dram_bytes"]
+                    ent["ncu_issue_slots_busy_pct"] = v.get("issue_slots_busy_pct")
         # dominant kernel: sort passes are launches of ONE kernel -> judged together
         sort_ms = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass")))
         cand = {"blend": kmean[-1], "sort_pass": sort_ms, "preprocess": kmean[0], "emit": kmean[2]}
@@ -431,6 +457,22 @@ def main():
                     "launches_per_step": 4 if dom == "tile_sort" else 1, "ms_per_launch": ms,
                     "alg_bytes_per_launch": alg[dom]}
         roof["peak_source"] = peak_src
+        # traffic / instruction counts of the same kernel from the committed ncu capture of
+        # this workload (profiles/*_traffic.json, written by profiles/extract_traffic.py)
+        prof = profiled_kernels(args.workload)
+        hit = [v for k, v in prof.items() if isinstance(v, dict) and k.split("<")[0] == roof["kernel"]]
+        if hit:
+            roof["traffic"] = hit[0]["dram_bytes"]
+            roof["traffic_source"] = prof.get("_file")
+            if roof["kernel"] == "k_blend":
+                # the bound that applies: warp-instruction issue (4 schedulers x SMs x clock)
+                inst = hit[0]["warp_instructions"]
+                peak_issue = 4.0 * torch.cuda.get_device_properties(dev).multi_processor_count \
+                    * (clocks.get("sm_mhz") or sm_max) * 1e6
+                ach = inst / (roof["ms_per_launch"] * 1e-3)
+                roof["issue"] = {"warp_instructions_per_launch": inst, "achieved_ginst_s": ach / 1e9,
+                                 "peak_ginst_s": peak_issue / 1e9, "frac": ach / peak_issue,
+                                 "ncu_issue_slots_busy_pct": hit[0].get("issue_slots_busy_pct")}
 
         cpu = None
         if not args.no_cpu and world == 1:
