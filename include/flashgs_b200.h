@@ -164,6 +164,19 @@ int32_t fgs_profile_end(void);
 /* ---- per-scene (model_io.py:78-118 ActivatedScene; untimed in the reference,
  *      pipeline.py:1-5) ------------------------------------------------------ */
 
+/* model_io.py:93-118 activate, on the device: sign-split
+ * sigmoid of the opacity logits, exp of the log-scales, quaternion normalisation
+ * with zero-norm rows mapped to the identity.  Rotations are bit-identical to the
+ * reference's NumPy result (IEEE sqrt / divide, same summation order); opacities
+ * and scales use a correctly rounded exp (float64 exp rounded once), while NumPy's
+ * float32 SIMD exp is good to ~2 ulp: scales can differ from the reference's by
+ * 2 ulp, opacities by a few more.  Frames then agree within the 1e-3 pixel tolerance, but the bit-exact
+ * pair-list guarantee holds only for scenes activated by the reference itself.
+ * All pointers are device arrays; outputs feed fgs_scene_pack. */
+int fgs_scene_activate(const float *logit_opacities, const float *log_scales,
+                       const float *rotations, int64_t gaussians, float *opacities_out,
+                       float *scales_out, float *rotations_out, void *stream);
+
 /* Bytes of the packed device scene for P Gaussians (248 B per Gaussian, P rounded
  * up to 32). */
 size_t fgs_scene_bytes(int64_t gaussians);

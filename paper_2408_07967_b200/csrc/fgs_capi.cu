@@ -127,6 +127,19 @@ int fgs_scene_order(const float *means, int64_t P, uint32_t *order_out, void *sc
     return fgs_sort_pairs(codes, idx, P, 31, 0, codes_out, order_out, b, sort_bytes, 1u, stream);
 }
 
+int fgs_scene_activate(const float *logit_opacities, const float *log_scales, const float *rotations,
+                       int64_t P, float *opacities_out, float *scales_out, float *rotations_out,
+                       void *stream)
+{
+    if (P < 0) return FGS_E_ARG;
+    if (P && (!logit_opacities || !log_scales || !rotations || !opacities_out || !scales_out ||
+              !rotations_out))
+        return FGS_E_ARG;
+    if (((uintptr_t)rotations & 15) || ((uintptr_t)rotations_out & 15)) return FGS_E_ARG;
+    return fgs_launch_activate(logit_opacities, log_scales, rotations, P, opacities_out, scales_out,
+                               rotations_out, (cudaStream_t)stream);
+}
+
 int fgs_scene_pack(const float *means, const float *opacities, const float *scales,
                    const float *rotations, const float *sh, const uint32_t *order, int64_t P,
                    void *packed, void *stream)

@@ -168,6 +168,39 @@ int fgs_launch_morton_keys(const float *means, int64_t P, float *bbox6, uint64_t
     return FGS_OK;
 }
 
+// model_io.py:93-118 activate
+__global__ void __launch_bounds__(256)
+k_activate(const float *__restrict__ logit, const float *__restrict__ log_scales,
+           const float *__restrict__ rots, int64_t P, float *__restrict__ opac,
+           float *__restrict__ scales, float *__restrict__ unit)
+{
+    const int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (g >= P) return;
+    // sign-split sigmoid: exp never overflows (model_io.py:101-105)
+    const float x = logit[g];
+    const bool nonneg = x >= 0.0f;
+    const float t = (float)exp((double)(nonneg ? -x : x));
+    const float denom = fa(1.0f, t);
+    opac[g] = nonneg ? fd(1.0f, denom) : fd(t, denom);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) scales[3 * g + a] = (float)exp((double)log_scales[3 * g + a]);
+    const float4 q = reinterpret_cast<const float4 *>(rots)[g];
+    const float nrm = fsq(fa(fa(fa(fm(q.x, q.x), fm(q.y, q.y)), fm(q.z, q.z)), fm(q.w, q.w)));
+    reinterpret_cast<float4 *>(unit)[g] =
+        nrm > 0.0f ? make_float4(fd(q.x, nrm), fd(q.y, nrm), fd(q.z, nrm), fd(q.w, nrm))
+                   : make_float4(1.0f, 0.0f, 0.0f, 0.0f);
+}
+
+int fgs_launch_activate(const float *logit, const float *log_scales, const float *rots, int64_t P,
+                        float *opac, float *scales, float *unit, cudaStream_t st)
+{
+    if (P == 0) return FGS_OK;
+    k_activate<<<(unsigned)((P + 255) / 256), 256, 0, st>>>(logit, log_scales, rots, P, opac, scales,
+                                                            unit);
+    FGS_CHECK_LAUNCH();
+    return FGS_OK;
+}
+
 // extent.py:19-30
 __global__ void __launch_bounds__(256)
 k_power_cutoffs(const float4 *__restrict__ g0, int64_t P, double tau, float tau32,

@@ -204,7 +204,7 @@ class Pipeline:
     """
 
     def __init__(self, scene, sh_degree=3, device=None, sort_mode="tile-bucket",
-                 spatial_order=None):
+                 spatial_order=None, device_activate=False):
         if sort_mode not in _capi.SORT_MODES:
             raise ValueError(f"unknown sort_mode {sort_mode!r}, expected one of {tuple(_capi.SORT_MODES)}")
         self.sort_mode = sort_mode
@@ -217,29 +217,49 @@ class Pipeline:
         if spatial_order and sort_mode != "tile-bucket":
             raise ValueError("spatial_order needs sort_mode='tile-bucket'")
         self.spatial_order = bool(spatial_order)
-        if is_raw_scene(scene):
-            act = activate(scene)
+        # ``device_activate``: a raw Scene is activated by the library (fgs_scene_activate)
+        # instead of on the host.  Opacities / scales may then differ from the reference's
+        # NumPy activation by 1 ulp (see the header), so frames agree within the pixel
+        # tolerance but pair lists are no longer guaranteed bit-identical to the reference.
+        raw = is_raw_scene(scene)
+        on_device = bool(device_activate) and raw
+        if raw:
+            act = None if on_device else activate(scene)
         elif is_activated_scene(scene):
             act = scene
         else:
             raise TypeError("scene must be a Scene or ActivatedScene")
         torch = _torch()
         self.sh_degree = int(sh_degree)
-        self.activated = act
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
-        self.count = int(np.asarray(act.means).shape[0])
+        src = scene if on_device else act
+        self.count = int(np.asarray(src.means).shape[0])
         L = _capi.lib()
         with torch.cuda.device(self.device):
             f32 = lambda a, shape: torch.from_numpy(
                 np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(shape))).to(self.device)
             P = self.count
-            means, opac = f32(act.means, (P, 3)), f32(act.opacities, (P,))
-            scales, rots = f32(act.scales, (P, 3)), f32(act.rotations, (P, 4))
-            sh = f32(act.sh, (P, 48))
+            st = _stream_ptr(torch, self.device)
+            means, sh = f32(src.means, (P, 3)), f32(src.sh, (P, 48))
+            if on_device:
+                logit, logs = f32(scene.logit_opacities, (P,)), f32(scene.log_scales, (P, 3))
+                rawrot = f32(scene.rotations, (P, 4))
+                opac, scales, rots = (torch.empty_like(logit), torch.empty_like(logs),
+                                      torch.empty_like(rawrot))
+                _capi.check(L.fgs_scene_activate(logit.data_ptr(), logs.data_ptr(), rawrot.data_ptr(),
+                                                 P, opac.data_ptr(), scales.data_ptr(),
+                                                 rots.data_ptr(), st))
+                from .scene import ActivatedScene
+                act = ActivatedScene(np.asarray(scene.means, dtype=np.float32), opac.cpu().numpy(),
+                                     scales.cpu().numpy(), rots.cpu().numpy(),
+                                     np.asarray(scene.sh, dtype=np.float32))
+            else:
+                opac = f32(act.opacities, (P,))
+                scales, rots = f32(act.scales, (P, 3)), f32(act.rotations, (P, 4))
+            self.activated = act
             self.scene_bytes = int(L.fgs_scene_bytes(P))
             self.packed = torch.empty(max(self.scene_bytes, 16), dtype=torch.uint8, device=self.device)
-            st = _stream_ptr(torch, self.device)
             order = None
             if self.spatial_order and P:
                 order = torch.empty(P, dtype=torch.int32, device=self.device)

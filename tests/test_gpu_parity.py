@@ -554,3 +554,28 @@ def test_overlapped_views_match_one_at_a_time_on_dense_tiles():
                 assert (sa.pairs_emitted, sa.pairs_contributing) == (sb.pairs_emitted, sb.pairs_contributing)
     oimg, ost = orc.render(act, cams[0])
     assert np.array_equal(ref[0][0].image.view(np.uint32), oimg.view(np.uint32))
+
+
+def test_device_activate_tracks_the_reference_activation():
+    """fgs_scene_activate: rotations bit-identical to the NumPy
+    activation, scales / opacities within a few ulp, frames within the pixel tolerance."""
+    raw = fgs.gen_synthetic("mixed", 20000, 31)
+    raw.rotations[7] = 0.0                                  # zero-norm row -> identity
+    host = fgs.activate(raw)
+    pipe = fgs.Pipeline(raw, device_activate=True)
+    dev = pipe.activated
+    assert np.array_equal(dev.rotations.view(np.uint32), host.rotations.view(np.uint32))
+    assert np.array_equal(dev.rotations[7], np.array([1, 0, 0, 0], np.float32))
+
+    def ulps(a, b):
+        return np.abs(a.view(np.int32).astype(np.int64) - b.view(np.int32).astype(np.int64)).max()
+    # exp is correctly rounded here; NumPy's float32 SIMD exp is good to ~2 ulp, and the
+    # sigmoid's divide can stretch that to a few ulp of the (smaller) quotient
+    assert ulps(dev.scales, host.scales) <= 2 and ulps(dev.opacities, host.opacities) <= 6
+    cam = fgs.orbit_cameras(1, 20.0, 400, 240)[0]
+    fd_, sd = pipe.render(cam)
+    fh, sh_ = fgs.Pipeline(host).render(cam)
+    assert fgs.max_abs_diff(fd_.image, fh.image) <= PIX_TOL and _psnr_ok(fd_.image, fh.image)
+    assert abs(sd.pairs_emitted - sh_.pairs_emitted) <= max(2, sh_.pairs_emitted // 10000)
+    # an already activated scene is taken as is
+    assert fgs.Pipeline(host, device_activate=True).activated is host
