@@ -272,20 +272,22 @@ __device__ __forceinline__ int tile_hits32(int tx, int ty, int width, int height
     if (!out_u && !out_v) return 1;                       // intersect.py:84-86 centre in tile
     const float ue = u0 > 0.0f ? u0 : u1;                 // the edge facing the centre
     const float ve = v0 > 0.0f ? v0 : v1;
+    // (this unit is compiled with -fmad=false for the reference-order geometry; the
+    // screening is tolerance-guarded, so it uses explicit FMAs)
     float qmin = __int_as_float(0x7f800000);
     if (out_u) {                                          // edge u = ue, v in [v0, v1]
         const float bu = b * ue;
         const float vs = fminf(fmaxf(__fdividef(-bu, c), v0), v1);
-        qmin = a * ue * ue + (c * vs * vs + 2.0f * bu * vs);
+        qmin = fmaf(a * ue, ue, fmaf(c * vs, vs, 2.0f * bu * vs));
     }
     if (out_v) {                                          // edge v = ve, u in [u0, u1]
         const float bv = b * ve;
         const float us = fminf(fmaxf(__fdividef(-bv, a), u0), u1);
-        qmin = fminf(qmin, c * ve * ve + (a * us * us + 2.0f * bv * us));
+        qmin = fminf(qmin, fmaf(c * ve, ve, fmaf(a * us, us, 2.0f * bv * us)));
     }
     const float um = fmaxf(fabsf(u0), fabsf(u1)), vm = fmaxf(fabsf(v0), fabsf(v1));
-    const float tol = 1e-4f * (fabsf(a) * um * um + fabsf(c) * vm * vm + 2.0f * fabsf(b) * um * vm
-                               + fabsf(k));
+    const float tol = 1e-4f * fmaf(fabsf(a) * um, um, fmaf(fabsf(c) * vm, vm,
+                                   fmaf(2.0f * fabsf(b) * um, vm, fabsf(k))));
     if (qmin < k - tol) return 1;
     if (qmin > k + tol) return 0;
     return 2;                                             // too close (or not finite): ask float64
@@ -391,6 +393,9 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
     const uint32_t incl = warp_incl_scan(job.cand, lane);
     const uint32_t total = __shfl_sync(FGS_FULL, incl, 31);
     const uint32_t excl = incl - job.cand;
+    // ceil(2^32 / nx), or 0 = "divide" for a rectangle so large the reciprocal is not exact
+    const uint32_t rnx = (job.nx > 1 && (uint64_t)job.cand * (uint32_t)job.nx < (1ull << 32))
+                             ? 0xffffffffu / (uint32_t)job.nx + 1u : 0u;
     uint32_t mine = 0;
     uint64_t mymask = 0;
     // K3: does any lane of this warp need the exact test again?
@@ -410,8 +415,11 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
         const int tx0 = __shfl_sync(FGS_FULL, job.tx0, o);
         const int ty0 = __shfl_sync(FGS_FULL, job.ty0, o);
         const int nx = __shfl_sync(FGS_FULL, job.nx, o);
+        const uint32_t rnx_o = __shfl_sync(FGS_FULL, rnx, o);
         const uint32_t local = act ? j - excl_o : 0u;
-        const int ry = (int)(local / (uint32_t)(nx > 0 ? nx : 1));
+        // local / nx by the owner's reciprocal ceil(2^32 / nx): exact while local * nx < 2^32
+        // (a rectangle has at most grid tiles <= 2^31 candidates)
+        const int ry = (int)(nx <= 1 ? local : rnx_o ? __umulhi(local, rnx_o) : local / (uint32_t)nx);
         const int tx = tx0 + (int)local - ry * nx, ty = ty0 + ry;
         bool pass = act;
         if (PRECISE && !COUNTING) {
