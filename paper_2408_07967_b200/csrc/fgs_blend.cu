@@ -211,10 +211,16 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                 keep = !(u0 > q2.z || u1 < -q2.z || v0 > q2.w || v1 < -q2.w);
                 if (keep) keep = !ellipse_misses_block(q0.z, q0.w, q1.x, q1.z, u0, u1, v0, v1);
             }
-            uint32_t live = __ballot_sync(FGS_FULL, keep);
-            while (live) {
-                const int j = c0 + __ffs(live) - 1;
-                live &= live - 1;
+            const uint32_t live = __ballot_sync(FGS_FULL, keep);
+            // Fixed trip count with a warp-uniform skip per pair, unrolled: a survivor's row
+            // address and contrib slot are then immediate offsets from the chunk base.  (A
+            // find-first-set loop over `live` spends ten uniform-datapath instructions per
+            // survivor on bit scanning and address arithmetic, a fifth of the body.)
+            constexpr int kUnroll = FGS_BLEND_UNROLL;
+#pragma unroll kUnroll
+            for (int jj = 0; jj < 32; ++jj) {
+                if (!((live >> jj) & 1u)) continue;
+                const int j = c0 + jj;
                 // Straight-line body: a lane the reference would skip (render.py:211, 214,
                 // 219) carries alpha = 0 through the blend, which leaves C and T bit-for-bit
                 // unchanged.  With 18-28 of 32 lanes live per surviving pair, early-out
