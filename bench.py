@@ -195,7 +195,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-spatial", action="store_true",
                     help="keep the scene in the caller's order (no Morton slot order)")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=3,
                     help="CUDA streams the timed views are issued on round-robin (1 = back to back)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FGS_ABI_VERSION 3
+#define FGS_ABI_VERSION 4
 #define FGS_TILE 16              /* constants.py:4  TILE_SIZE */
 
 enum {
@@ -68,8 +68,10 @@ enum {
                                bit-identical to the reference's; default is the
                                ex2.approx path with an exact re-check at the
                                alpha<tau threshold (max-abs error ~1e-6)      */
-    FGS_BLEND_CONTRIB = 2   /* fill the per-pair "touched a pixel" flags and
+    FGS_BLEND_CONTRIB = 2,  /* fill the per-pair "touched a pixel" flags and
                                stats.pairs_contributing (render.py:200-231)  */
+    FGS_BLEND_SCALAR  = 4   /* default numerics on the one-pixel-per-thread kernel
+                               (kept as the A/B arm of the packed-f32x2 kernel) */
 };
 
 /* model_io.py:226-254 Camera, flattened.  Doubles are the Python floats the
@@ -136,6 +138,9 @@ typedef struct fgs_layout {
     uint64_t off_cursor;       /* uint32 [tiles][8]: size-class tile lists (words 1..3) */
     uint64_t off_ctainfo;      /* uint32 [preprocess blocks][4]: TILE_BUCKET, each K1 CTA's
                                   (first table entry, entries, write-combined records, 0) */
+    uint64_t off_tileorder;    /* uint32 [128 + tiles]: TILE_BUCKET, 64 size-bin counts, 64 bin
+                                  cursors, then the band's tiles ordered heaviest first (the
+                                  order the blend's CTAs take them in)                    */
     int64_t  gaussians, capacity;   /* capacity = the request rounded up to 64 pairs */
     int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
     int32_t  preprocess_blocks, sort_passes;

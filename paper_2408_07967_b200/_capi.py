@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # FGS_LIB selects another build of the same library (tuning variants, see build.py)
 LIB_PATH = os.environ.get("FGS_LIB") or os.path.join(HERE, "_lib", "libflashgs_b200.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 STRATEGIES = ("baseline-circle-aabb", "tight-aabb", "precise")   # binning.py:38 order
 STRATEGY_ID = {"precise": 0, "tight-aabb": 1, "baseline-circle-aabb": 2}
 BLEND_EXACT, BLEND_CONTRIB = 1, 2
@@ -69,6 +69,7 @@ class FgsLayout(C.Structure):
                 ("off_contrib", C.c_uint64), ("off_stats", C.c_uint64),
                 ("off_tilecount", C.c_uint64), ("off_cursor", C.c_uint64),
                 ("off_ctainfo", C.c_uint64),
+                ("off_tileorder", C.c_uint64),
                 ("gaussians", C.c_int64), ("capacity", C.c_int64),
                 ("width", C.c_int32), ("height", C.c_int32), ("grid_w", C.c_int32),
                 ("grid_h", C.c_int32), ("tiles", C.c_int32), ("tile_bits", C.c_int32),

@@ -27,6 +27,7 @@
 // are all finished skips the rest of a batch.
 
 #include "fgs_common.cuh"
+#include <stdlib.h>
 
 namespace {
 
@@ -120,16 +121,18 @@ template <bool EXACT, bool CONTRIB, bool EXTRAS>
 __global__ void __launch_bounds__(256)
 k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
-        const int32_t *__restrict__ starts, int width,
-        int height, int grid_w, int ty_first, float bg0, float bg1, float bg2, float tau,
+        const int32_t *__restrict__ starts, const uint32_t *__restrict__ order, int width,
+        int height, int grid_w, int first_tile, float bg0, float bg1, float bg2, float tau,
         float *__restrict__ rgb, float *__restrict__ alpha_out, float *__restrict__ depth_out,
         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
 {
     __shared__ BlendSmem S;
     if (stats != nullptr && stats->overflow) return;   // frame is re-run with a larger buffer
     const int tid = threadIdx.x;
-    const int tx = blockIdx.x, ty = ty_first + blockIdx.y;
-    const int tile = ty * grid_w + tx;
+    // CTA i takes the i-th tile of the blend order (heaviest first), or of the band in
+    // raster order when no order was built
+    const int tile = order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x;
+    const int ty = tile / grid_w, tx = tile - ty * grid_w;
     // each warp owns an 8x4 pixel block (squarer than 16x2, so fewer splat
     // rectangles reach it); lanes run row-major inside the block
     const int lane = tid & 31, wq = tid >> 5;
@@ -301,19 +304,307 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// k_blend2: the default-mode blend, two pixels per thread on Blackwell's packed float32
+// pipe (FFMA2 / FMUL2 / FADD2: one issue slot for two lanes' worth of float32 work).
+//
+// One CTA of 128 threads per 16x16 tile; a warp owns an 8x8 pixel block and lane l the
+// pixels (x, y) and (x, y+4), which share dx, so the quadratic form is a Horner chain in
+// the packed dy:   -log2(e) * s = dy * (c2*dy + b2*dx) + a2*dx*dx   (a2 = -log2e/2 * a ...)
+// = 4 scalar + 3 packed operations for two pixels against 22 scalar ones in k_blend.
+//
+// The reference's three skips (render.py:211 extent rectangle, :214 s > k/2, :219
+// alpha < tau) collapse into ONE comparison, alpha >= thr with thr = max(tau, op*exp(-k/2)):
+//   * s > k/2  <=>  op*exp(-s) < op*exp(-k/2)  (monotone), and
+//   * the extent rectangle is the bounding box of the cutoff ellipse (binning.py:181-182),
+//     so a pixel outside it has s > k/2 -- the transform pass below CHECKS that per pair
+//     from the row itself (hx^2 >= k*c/det, hy^2 >= k*a/det); a row that does not satisfy
+//     it (hand-made rows through fgs_blend_tiles) is blended by the exact path entirely.
+// Those equivalences hold in real arithmetic.  In float32 the fused evaluation here and the
+// reference's unfused one differ by at most ~1.3e-5*kappa relative in alpha
+// (kappa = a*c/det bounds the cancellation between the three terms), so whenever alpha
+// lands within eps = thr*(2e-5 + 2.5e-5*kappa) of thr the lane recomputes the pair the
+// reference's way -- unfused s, the three tests in order, glibc-equivalent expf -- and that
+// verdict (and alpha) is used.  Outside the band both evaluations agree on the verdict.
+// A band hit is rare (~1e-4 of evaluations), the exact path is a warp-level branch.
+//
+// Pipeline: as k_blend, at 128 pairs per batch; the thread that gathered a pair's row also
+// transforms it (a2, b2, c2, thr, eps) into the batch's fast-row table before the barrier.
+
+typedef float2 pk2;                   // two float32 lanes: x = pixel (x, y), y = pixel (x, y+4)
+__device__ __forceinline__ pk2 pk(float lo, float hi) { return make_float2(lo, hi); }
+__device__ __forceinline__ void upk(pk2 v, float &lo, float &hi) { lo = v.x; hi = v.y; }
+__device__ __forceinline__ pk2 mul2(pk2 a, pk2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ pk2 add2(pk2 a, pk2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ pk2 sub2(pk2 a, pk2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ pk2 fma2(pk2 a, pk2 b, pk2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ pk2 bc(float v) { return pk(v, v); }   // broadcast operand (R.F32 in SASS)
+
+#define FGS_B2_THREADS 128
+#define FGS_B2_BATCH   128
+#ifndef FGS_B2_MINCTAS
+#define FGS_B2_MINCTAS 1
+#endif
+#ifndef FGS_B2_UNROLL
+#define FGS_B2_UNROLL  8
+#endif
+
+struct Blend2Smem {
+    float4 row[2][FGS_B2_BATCH][3];    // reference rows (cp.async destination)
+    float4 fast[FGS_B2_BATCH][3];      // (cx,cy,a2,b2) (c2,op,thr,eps) (r,g,b,z)
+    float  z[2][FGS_B2_BATCH];
+    uint32_t touched[FGS_B2_BATCH];
+    unsigned long long tab[32];
+};
+
+// One pixel of a pair the reference's way (render.py:203-219): returns alpha, 0 if skipped.
+__device__ __forceinline__ float alpha_exact(const float4 r0, const float4 r1, const float4 r2,
+                                             float fx, float fy, float tau,
+                                             const unsigned long long *tab)
+{
+    const float dx = fs(fx, r0.x), dy = fs(fy, r0.y);
+    const float s = fa(fm(0.5f, fa(fm(fm(r0.z, dx), dx), fm(fm(r1.x, dy), dy))),
+                       fm(fm(r0.w, dx), dy));
+    if (fabsf(dx) > r2.z || fabsf(dy) > r2.w || s > fm(0.5f, r1.z)) return 0.0f;
+    float al = fm(r1.y, expf_exact(-s, tab));
+    al = al > FGS_ALPHA_CAP ? FGS_ALPHA_CAP : al;
+    return al < tau ? 0.0f : al;
+}
+
+template <bool CONTRIB, bool EXTRAS>
+__global__ void __launch_bounds__(FGS_B2_THREADS, FGS_B2_MINCTAS)
+k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
+         const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
+         const int32_t *__restrict__ starts, const uint32_t *__restrict__ order, int width,
+         int height, int grid_w, int first_tile,
+         float bg0, float bg1, float bg2, float tau, float *__restrict__ rgb,
+         float *__restrict__ alpha_out, float *__restrict__ depth_out,
+         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
+{
+    __shared__ Blend2Smem S;
+    if (stats != nullptr && stats->overflow) return;
+    constexpr int B = FGS_B2_BATCH;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, wq = tid >> 5;
+    if (tid < 32) S.tab[tid] = c_exp2_tab[tid];
+    uint32_t ncontrib = 0;
+    // CTA i takes the i-th tile of the blend order (heaviest first: longest-first list
+    // scheduling by the hardware's in-order CTA dispatch), or of the band in raster order.
+    // (Persistent CTAs pulling tiles from a ticket counter were slower: 72 registers, and the
+    // per-tile prologue no longer overlaps other CTAs' blending -- 197 us against 177 on C2.)
+    const int tile = order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x;
+    const int ty = tile / grid_w, tx = tile - ty * grid_w;
+    const int bx = tx * FGS_TILE + (wq & 1) * 8, by = ty * FGS_TILE + (wq >> 1) * 8;
+    const int px = bx + (lane & 7), py0 = by + (lane >> 3), py1 = py0 + 4;
+    const float wx_lo = (float)bx + 0.5f, wx_hi = (float)bx + 7.5f;
+    const float wy_lo = (float)by + 0.5f, wy_hi = (float)by + 7.5f;
+    const bool inside0 = px < width && py0 < height, inside1 = px < width && py1 < height;
+    // A finished pixel (outside the image, or T < 1e-4, render.py:228) parks its y centre at
+    // +inf: dy = inf, c2 < 0 => -log2e*s = -inf, alpha = 0 < thr, and the exact path's extent
+    // test rejects it too -- no separate "live" flag in the loop.
+    const float kInf = __int_as_float(0x7f800000);
+    const float fx = (float)px + 0.5f;
+    float fy0 = inside0 ? (float)py0 + 0.5f : kInf, fy1 = inside1 ? (float)py1 + 0.5f : kInf;
+    constexpr float kL = -1.4426950408889634f;       // -log2(e)
+
+    const int start = starts[tile], n = starts[tile + 1] - start;
+
+    pk2 T2 = pk(1.0f, 1.0f), cr2 = pk(0.0f, 0.0f), cg2 = cr2, cb2 = cr2, dz2 = cr2;
+
+    const int nb = (n + B - 1) / B;
+    const auto slot_of = [&](uint32_t v) { return inv ? inv[v] : v; };
+    if (tid < n) {
+        const uint32_t g = slot_of(vals[start + tid]);
+        const float4 *src = (const float4 *)(splat + (size_t)g * 12);
+        cp_async16(&S.row[0][tid][0], src);
+        cp_async16(&S.row[0][tid][1], src + 1);
+        cp_async16(&S.row[0][tid][2], src + 2);
+        if (EXTRAS) S.z[0][tid] = gdepth ? gdepth[g] : 0.0f;
+    }
+    cp_async_commit();
+    uint32_t idx_next = (B + tid < n) ? slot_of(vals[start + B + tid]) : 0u;
+    uint32_t val_next2 = (2 * B + tid < n) ? vals[start + 2 * B + tid] : 0u;
+
+    int b = 0;
+    for (; b < nb; ++b) {
+        const int cur = b & 1, nxt = cur ^ 1;
+        const int cnt = n - b * B < B ? n - b * B : B;
+        // step 0: this thread's own gather of batch b has landed (its own cp.async group):
+        // derive the pair's fast row.  fast[] is free: every warp passed the barrier that
+        // ended batch b-1.
+        cp_async_wait<0>();
+        if (tid < cnt) {
+            const float4 q0 = S.row[cur][tid][0], q1 = S.row[cur][tid][1], q2 = S.row[cur][tid][2];
+            const float a = q0.z, bb = q0.w, c = q1.x, op = q1.y, k = q1.z;
+            const float hk = 0.5f * k;
+            const float thr = fmaxf(tau, op * ex2_approx(hk * kL));
+            const float ac = a * c, det = fmaf(-bb, bb, ac);
+            const float kap = ac / det;
+            // extent rectangle contains the cutoff ellipse?  (x half-extent^2 = k*c/det)
+            const float slack = 1.0f - 1e-6f * kap;
+            const bool boxed = q2.z * q2.z * det >= k * c * slack && q2.w * q2.w * det >= k * a * slack;
+            float eps = thr * fmaf(2.5e-5f, kap, 2e-5f);
+            if (!(det > 0.0f) || !(kap < 400.0f) || !boxed || !(c > 0.0f) || !(a > 0.0f))
+                eps = __int_as_float(0x7f800000);    // every evaluation takes the exact path
+            S.fast[tid][0] = make_float4(q0.x, q0.y, a * (0.5f * kL), bb * kL);
+            S.fast[tid][1] = make_float4(c * (0.5f * kL), op, thr, eps);
+            S.fast[tid][2] = make_float4(q1.w, q2.x, q2.y, EXTRAS ? S.z[cur][tid] : 0.0f);
+        }
+        // step 1: gather the rows of batch b+1
+        if ((b + 1) * B + tid < n) {
+            const float4 *src = (const float4 *)(splat + (size_t)idx_next * 12);
+            cp_async16(&S.row[nxt][tid][0], src);
+            cp_async16(&S.row[nxt][tid][1], src + 1);
+            cp_async16(&S.row[nxt][tid][2], src + 2);
+            if (EXTRAS) S.z[nxt][tid] = gdepth ? gdepth[idx_next] : 0.0f;
+        }
+        cp_async_commit();
+        // step 2: slots of batch b+2, values of batch b+3
+        const uint32_t idx_next2 = ((b + 2) * B + tid < n) ? slot_of(val_next2) : 0u;
+        const int i3 = (b + 3) * B + tid;
+        val_next2 = i3 < n ? vals[start + i3] : 0u;
+        if (CONTRIB) S.touched[tid] = 0u;
+        __syncthreads();
+
+        // step 3: blend batch b
+        for (int c0 = 0; c0 < cnt; c0 += 32) {
+            if (__all_sync(FGS_FULL, fy0 == kInf && fy1 == kInf)) break;
+            const int jl = c0 + lane;
+            bool keep = false;
+            if (jl < cnt) {
+                const float4 q0 = S.row[cur][jl][0];
+                const float4 q1 = S.row[cur][jl][1];
+                const float4 q2 = S.row[cur][jl][2];
+                const float u0 = fs(wx_lo, q0.x), u1 = fs(wx_hi, q0.x);
+                const float v0 = fs(wy_lo, q0.y), v1 = fs(wy_hi, q0.y);
+                keep = !(u0 > q2.z || u1 < -q2.z || v0 > q2.w || v1 < -q2.w);
+                if (keep) keep = !ellipse_misses_block(q0.z, q0.w, q1.x, q1.z, u0, u1, v0, v1);
+            }
+            const uint32_t survivors = __ballot_sync(FGS_FULL, keep);
+            constexpr int kUnroll2 = FGS_B2_UNROLL;
+#pragma unroll kUnroll2
+            for (int jj = 0; jj < 32; ++jj) {
+                if (!((survivors >> jj) & 1u)) continue;
+                const int j = c0 + jj;
+                const float4 f0 = S.fast[j][0];
+                const float4 f1 = S.fast[j][1];
+                const float4 f2 = S.fast[j][2];
+                const float dx = fx - f0.x;
+                const float adx2 = (f0.z * dx) * dx, bdx = f0.w * dx;
+                const pk2 dy2 = sub2(pk(fy0, fy1), bc(f0.y));
+                const pk2 h2 = fma2(bc(f1.x), dy2, bc(bdx));
+                const pk2 m2 = fma2(dy2, h2, bc(adx2));              // -log2(e) * s
+                float m0, m1;
+                upk(m2, m0, m1);
+                pk2 al2 = mul2(bc(f1.y), pk(ex2_approx(m0), ex2_approx(m1)));
+                const pk2 d2 = sub2(al2, bc(f1.z));
+                float al0, al1, d0, d1;
+                upk(d2, d0, d1);
+                upk(al2, al0, al1);
+                bool on0 = d0 >= 0.0f, on1 = d1 >= 0.0f;
+                const bool band = !(fabsf(d0) > f1.w) | !(fabsf(d1) > f1.w);
+                if (band) {
+                    // within eps of the threshold (or a row the shortcut does not cover):
+                    // the reference's own evaluation decides, for both pixels
+                    const float4 r0 = S.row[cur][j][0], r1 = S.row[cur][j][1], r2 = S.row[cur][j][2];
+                    al0 = alpha_exact(r0, r1, r2, fx, fy0, tau, S.tab);
+                    al1 = alpha_exact(r0, r1, r2, fx, fy1, tau, S.tab);
+                    on0 = al0 > 0.0f;
+                    on1 = al1 > 0.0f;
+                }
+                al0 = fminf(al0, FGS_ALPHA_CAP);                     // render.py:217-218
+                al1 = fminf(al1, FGS_ALPHA_CAP);
+                al2 = pk(on0 ? al0 : 0.0f, on1 ? al1 : 0.0f);
+                const pk2 w2 = mul2(al2, T2);
+                cr2 = fma2(bc(f2.x), w2, cr2);
+                cg2 = fma2(bc(f2.y), w2, cg2);
+                cb2 = fma2(bc(f2.z), w2, cb2);
+                if (EXTRAS) dz2 = fma2(bc(f2.w), w2, dz2);
+                T2 = mul2(T2, sub2(pk(1.0f, 1.0f), al2));
+                if (CONTRIB && (on0 || on1)) S.touched[j] = 1u;
+                float t0, t1;
+                upk(T2, t0, t1);
+                if (t0 < FGS_T_STOP) fy0 = kInf;                     // render.py:228
+                if (t1 < FGS_T_STOP) fy1 = kInf;
+            }
+        }
+        const bool all_done = __syncthreads_and(fy0 == kInf && fy1 == kInf);
+        if (CONTRIB) {
+            if (tid < cnt) {
+                const uint32_t t = S.touched[tid];
+                contrib[start + b * B + tid] = (uint8_t)t;
+                ncontrib += t;
+            }
+        }
+        idx_next = idx_next2;
+        if (all_done) { ++b; break; }
+    }
+    cp_async_wait<0>();
+    if (CONTRIB)
+        for (int i = b * B + tid; i < n; i += B) contrib[start + i] = 0;
+
+    float t0, t1, r0, r1, g0, g1, b0, b1, z0, z1;
+    upk(T2, t0, t1);
+    upk(cr2, r0, r1);
+    upk(cg2, g0, g1);
+    upk(cb2, b0, b1);
+    upk(dz2, z0, z1);
+    if (inside0) {
+        const size_t o = (size_t)py0 * width + px;
+        rgb[3 * o + 0] = fmaf(t0, bg0, r0);                          // render.py:250-252
+        rgb[3 * o + 1] = fmaf(t0, bg1, g0);
+        rgb[3 * o + 2] = fmaf(t0, bg2, b0);
+        if (EXTRAS) {
+            if (alpha_out) alpha_out[o] = 1.0f - t0;
+            if (depth_out) depth_out[o] = z0;
+        }
+    }
+    if (inside1) {
+        const size_t o = (size_t)py1 * width + px;
+        rgb[3 * o + 0] = fmaf(t1, bg0, r1);
+        rgb[3 * o + 1] = fmaf(t1, bg1, g1);
+        rgb[3 * o + 2] = fmaf(t1, bg2, b1);
+        if (EXTRAS) {
+            if (alpha_out) alpha_out[o] = 1.0f - t1;
+            if (depth_out) depth_out[o] = z1;
+        }
+    }
+    if (CONTRIB) {
+        ncontrib = __reduce_add_sync(FGS_FULL, ncontrib);
+        if (lane == 0 && ncontrib) atomicAdd(&stats->pairs_contributing, ncontrib);
+    }
+}
+
+template <bool CONTRIB>
+int launch2(bool extras, dim3 grid, cudaStream_t st, const float *splat, const float *gdepth,
+            const uint32_t *vals, const uint32_t *inv, const int32_t *starts, const uint32_t *order,
+            int width, int height,
+            int grid_w, int first_tile, const float bg[3], float tau, float *rgb, float *alpha,
+            float *depth, uint8_t *contrib, fgs_stats *stats)
+{
+    if (extras)
+        k_blend2<CONTRIB, true><<<grid, FGS_B2_THREADS, 0, st>>>(splat, gdepth, vals, inv, starts, order,
+            width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+    else
+        k_blend2<CONTRIB, false><<<grid, FGS_B2_THREADS, 0, st>>>(splat, gdepth, vals, inv, starts, order,
+            width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+    FGS_AFTER_LAUNCH(st);
+    return FGS_OK;
+}
+
 template <bool EXACT, bool CONTRIB>
 int launch(bool extras, dim3 grid, cudaStream_t st, const float *splat, const float *gdepth,
-           const uint32_t *vals, const uint32_t *inv, const int32_t *starts, int width, int height,
-           int grid_w,
-           int ty_first, const float bg[3], float tau, float *rgb, float *alpha, float *depth,
+           const uint32_t *vals, const uint32_t *inv, const int32_t *starts, const uint32_t *order,
+           int width, int height, int grid_w,
+           int first_tile, const float bg[3], float tau, float *rgb, float *alpha, float *depth,
            uint8_t *contrib, fgs_stats *stats)
 {
     if (extras)
-        k_blend<EXACT, CONTRIB, true><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, width,
-            height, grid_w, ty_first, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+        k_blend<EXACT, CONTRIB, true><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, order, width,
+            height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
     else
-        k_blend<EXACT, CONTRIB, false><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, width,
-            height, grid_w, ty_first, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+        k_blend<EXACT, CONTRIB, false><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, order, width,
+            height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
@@ -321,23 +612,29 @@ int launch(bool extras, dim3 grid, cudaStream_t st, const float *splat, const fl
 }  // namespace
 
 int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
-                     const uint32_t *inv, const int32_t *starts, int width, int height,
+                     const uint32_t *inv, const int32_t *starts, const uint32_t *order,
+                     int width, int height,
                      const float bg[3], double tau,
                      int flags, int band0, int band1, float *rgb, float *alpha, float *depth,
                      uint8_t *contrib, fgs_stats *stats, cudaStream_t st)
 {
     const int grid_w = (width + FGS_TILE - 1) / FGS_TILE;
     if (band1 < band0) return FGS_OK;
-    const dim3 grid((unsigned)grid_w, (unsigned)(band1 - band0 + 1));
+    const dim3 grid((unsigned)(grid_w * (band1 - band0 + 1)));
+    const int first_tile = band0 * grid_w;
     const bool exact = flags & FGS_BLEND_EXACT, want_contrib = (flags & FGS_BLEND_CONTRIB) && contrib;
     const bool extras = (alpha != nullptr) || (depth != nullptr && gdepth != nullptr);
     if (depth != nullptr && gdepth == nullptr) return FGS_E_ARG;
     const float tau32 = (float)tau;
-#define FGS_GO(E, C) launch<E, C>(extras, grid, st, splat, gdepth, vals, inv, starts, width, height, \
-                                  grid_w, band0, bg, tau32, rgb, alpha, depth, contrib, stats)
+#define FGS_GO(E, C) launch<E, C>(extras, grid, st, splat, gdepth, vals, inv, starts, order, width, height, \
+                                  grid_w, first_tile, bg, tau32, rgb, alpha, depth, contrib, stats)
     if (exact) return want_contrib ? FGS_GO(true, true) : FGS_GO(true, false);
-    return want_contrib ? FGS_GO(false, true) : FGS_GO(false, false);
+    if (flags & FGS_BLEND_SCALAR) return want_contrib ? FGS_GO(false, true) : FGS_GO(false, false);
 #undef FGS_GO
+#define FGS_GO2(C) launch2<C>(extras, grid, st, splat, gdepth, vals, inv, starts, order, width, height, \
+                              grid_w, first_tile, bg, tau32, rgb, alpha, depth, contrib, stats)
+    return want_contrib ? FGS_GO2(true) : FGS_GO2(false);
+#undef FGS_GO2
 }
 
 // images.py:12-15 quantize (float64 like the reference); four values per thread

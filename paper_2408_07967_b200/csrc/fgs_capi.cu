@@ -189,6 +189,7 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     const uint64_t sort_tiles = (cap + FGS_SORT_TILE - 1) / FGS_SORT_TILE;
     L->off_stats = take(sizeof(fgs_stats));          // stats and tilecount are contiguous:
     L->off_tilecount = take((uint64_t)L->tiles * 4 * FGS_CTR_STRIDE); // one memset clears both
+    L->off_tileorder = take(((uint64_t)FGS_ORDER_HDR + L->tiles) * 4);  // ... and this header
     L->off_cursor = take((uint64_t)L->tiles * 4 * FGS_CTR_STRIDE);
     L->off_ctainfo = take((uint64_t)L->preprocess_blocks * 16 + 16);
     L->off_splat = take(p * 48);
@@ -305,7 +306,9 @@ int fgs_blend(const void *packed, const float bg[3], double tau, int32_t flags, 
     if (L->gaussians && !packed) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
     return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in],
-                            fgs_scene_view(packed, L->gaussians).inv, f.starts, L->width, L->height,
+                            fgs_scene_view(packed, L->gaussians).inv, f.starts,
+                            L->sort_mode == FGS_SORT_TILE_BUCKET ? f.tileorder + FGS_ORDER_HDR : nullptr,
+                            L->width, L->height,
                             bg, tau, flags, band0, band1, out_rgb, out_alpha, out_depth, f.contrib,
                             f.stats, (cudaStream_t)stream);
 }
@@ -404,7 +407,7 @@ int fgs_blend_tiles(const float *splat, const float *gaussian_depth, const uint3
     if ((flags & FGS_BLEND_CONTRIB) && (!contrib || !stats)) return FGS_E_ARG;
     const int gh = (height + FGS_TILE - 1) / FGS_TILE;
     if (band0 < 0 || band1 >= gh) return FGS_E_ARG;
-    return fgs_launch_blend(splat, gaussian_depth, sorted_values, nullptr, starts, width, height, bg, tau,
+    return fgs_launch_blend(splat, gaussian_depth, sorted_values, nullptr, starts, nullptr, width, height, bg, tau,
                             flags, band0, band1, out_rgb, out_alpha, out_depth, contrib, stats,
                             (cudaStream_t)stream);
 }

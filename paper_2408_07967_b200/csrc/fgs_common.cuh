@@ -45,6 +45,14 @@
 // internal work counters live behind the public 64-byte stats block (the block is 256
 // bytes in the workspace and zeroed with it at the start of every frame)
 #define FGS_WORK_LARGE    0
+// blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
+// empty = last) and the blend's CTAs take them in bin order, so the long tiles start first
+// and the grid's tail is made of short ones
+#define FGS_ORDER_BINS    64
+#ifndef FGS_ORDER_MBITS
+#define FGS_ORDER_MBITS   2        // mantissa bits of the size bins (2: quarter octaves)
+#endif
+#define FGS_ORDER_HDR     (2 * FGS_ORDER_BINS)
 static __host__ __device__ inline uint32_t *fgs_work(fgs_stats *s) { return (uint32_t *)(s + 1); }
 static __host__ __device__ inline const uint32_t *fgs_work(const fgs_stats *s) { return (const uint32_t *)(s + 1); }
 
@@ -113,6 +121,7 @@ struct FrameDev {
     uint4    *tablelist;    // TILE_BUCKET: (tile, range base, pairs, slot | wc offset) per
                             // (CTA, tile); aliases keys[1] + vals[0] + vals[1]
     uint4    *ctainfo;      // [preprocess blocks] (list base, entries, staged records, 0)
+    uint32_t *tileorder;    // [FGS_ORDER_HDR + tiles]: bin counts, bin cursors, blend tile order
     uint32_t list_capacity;
 };
 
@@ -142,6 +151,7 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.cursor = (uint32_t *)(b + L->off_cursor);
     f.tablelist = (uint4 *)(b + L->off_keys[1]);
     f.ctainfo = (uint4 *)(b + L->off_ctainfo);
+    f.tileorder = (uint32_t *)(b + L->off_tileorder);
     f.list_capacity = (uint32_t)L->capacity;
     return f;
 }
@@ -160,6 +170,7 @@ int  fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, con
                            int bucket, int tiles, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream_t st);
 int  fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st);
+int  fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st);
 int  fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
                      int band1, int bucket, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st);
@@ -178,7 +189,8 @@ int  fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev
 int  fgs_launch_ranges(const uint64_t *keys, const uint32_t *n_dev, int64_t n_max, int tiles,
                        int32_t *starts, fgs_stats *stats, cudaStream_t st);
 int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
-                      const uint32_t *inv, const int32_t *starts, int width, int height,
+                      const uint32_t *inv, const int32_t *starts, const uint32_t *order,
+                      int width, int height,
                       const float bg[3],
                       double tau, int flags, int band0, int band1, float *rgb, float *alpha,
                       float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st);
@@ -218,6 +230,20 @@ __device__ __forceinline__ float  fsq(float a)           { return __fsqrt_rn(a);
 __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+// size bin of a tile with v pairs: quarter-octave bins, heaviest first, empty last
+__device__ __forceinline__ int fgs_order_bin(uint32_t v)
+{
+    if (v == 0) return FGS_ORDER_BINS - 1;
+    int lb;
+    if (v < 4) lb = (int)v;
+    else {
+        const int e = 31 - __clz(v);
+        lb = e * 4 + (int)((v >> (e - 2)) & (3u & ~((1u << (2 - FGS_ORDER_MBITS)) - 1u))) - 4;   // v = 4 -> 4
+    }
+    lb = lb > FGS_ORDER_BINS - 2 ? FGS_ORDER_BINS - 2 : lb;
+    return FGS_ORDER_BINS - 2 - lb;
+}
 
 __device__ __forceinline__ uint32_t lanemask_lt()
 {

@@ -831,7 +831,8 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
     (void)g_dummy_cam;
     // stats and (TILE_BUCKET) the per-tile histogram sit back to back: one memset
     // the stats block is 256 bytes in the workspace: public counters + internal work counters
-    const size_t zero_bytes = bucket ? (size_t)((char *)(f.tilecount + (size_t)tiles * FGS_CTR_STRIDE) - (char *)f.stats)
+    // (stats | tile counters | tile-order header) are contiguous in the workspace
+    const size_t zero_bytes = bucket ? (size_t)((char *)(f.tileorder + FGS_ORDER_HDR) - (char *)f.stats)
                                      : 256;
     cudaError_t e = cudaMemsetAsync(f.stats, 0, zero_bytes, st);
     if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
@@ -930,10 +931,12 @@ int fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream
 // most 33 MB for an 8K frame's 129600 tiles, and no inter-CTA dependency at all.
 __global__ void __launch_bounds__(1024)
 k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
-             uint32_t *__restrict__ cursor, int tiles, unsigned long long capacity,
-             fgs_stats *__restrict__ stats)
+             uint32_t *__restrict__ cursor, uint32_t *__restrict__ bincount, int tiles,
+             unsigned long long capacity, fgs_stats *__restrict__ stats)
 {
     __shared__ unsigned long long s_w[32];
+    __shared__ uint32_t s_bin[FGS_ORDER_BINS];
+    if (threadIdx.x < FGS_ORDER_BINS) s_bin[threadIdx.x] = 0u;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int first = blockIdx.x * 1024;
     // prefix of everything before this CTA's slice
@@ -973,6 +976,11 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     }
     __syncthreads();
     const unsigned long long excl = carry + s_w[w] + incl - v;
+    // size-bin histogram for the blend's tile order (placement: k_tile_order)
+    if (i < tiles) atomicAdd(&s_bin[fgs_order_bin(v > 0xffffffffull ? 0xffffffffu : (uint32_t)v)], 1u);
+    __syncthreads();
+    if (threadIdx.x < FGS_ORDER_BINS && s_bin[threadIdx.x])
+        atomicAdd(&bincount[threadIdx.x], s_bin[threadIdx.x]);
     if (i < tiles) {
         const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
         starts[i] = (int32_t)e32;
@@ -999,8 +1007,58 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
 int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st)
 {
     k_scan_tiles<<<(unsigned)((tiles + 1023) / 1024), 1024, 0, st>>>(
-        f.tilecount, f.starts, f.cursor, tiles, (unsigned long long)capacity, f.stats);
+        f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats);
     FGS_AFTER_LAUNCH(st);
+    return FGS_OK;
+}
+
+// Blend tile order: the band's tiles, heaviest size bin first.  Bin bases come from the
+// histogram k_scan_tiles left in hdr[0..64); a CTA reserves its share of every bin with one
+// atomic on the bin's cursor (hdr[64..128)) and ranks its tiles inside it in shared memory.
+// Order inside a bin is arbitrary (every tile's output is independent of it).
+__global__ void __launch_bounds__(1024)
+k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int first_tile,
+             int band_tiles, const fgs_stats *__restrict__ stats)
+{
+    __shared__ uint32_t s_base[FGS_ORDER_BINS], s_cnt[FGS_ORDER_BINS], s_off[FGS_ORDER_BINS];
+    if (stats->overflow) return;
+    const int t = threadIdx.x;
+    if (t < FGS_ORDER_BINS) s_cnt[t] = 0u;
+    if (t < 32) {                                   // exclusive scan of the 64 bin counts
+        const uint32_t c0 = hdr[2 * t], c1 = hdr[2 * t + 1];
+        uint32_t incl = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(FGS_FULL, incl, o);
+            if (t >= o) incl += u;
+        }
+        s_base[2 * t] = incl - c0 - c1;
+        s_base[2 * t + 1] = incl - c1;
+    }
+    __syncthreads();
+    const int i = blockIdx.x * 1024 + t;
+    int bin = 0;
+    uint32_t rank = 0;
+    if (i < band_tiles) {
+        const int tile = first_tile + i;
+        bin = fgs_order_bin((uint32_t)(starts[tile + 1] - starts[tile]));
+        rank = atomicAdd(&s_cnt[bin], 1u);
+    }
+    __syncthreads();
+    if (t < FGS_ORDER_BINS && s_cnt[t]) s_off[t] = atomicAdd(&hdr[FGS_ORDER_BINS + t], s_cnt[t]);
+    __syncthreads();
+    // Tiles outside the band are empty and were counted in the last bin by k_scan_tiles;
+    // only the band's tiles are placed, so the first band_tiles entries are exactly the band.
+    if (i < band_tiles) hdr[FGS_ORDER_HDR + s_base[bin] + s_off[bin] + rank] = (uint32_t)(first_tile + i);
+}
+
+int fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st)
+{
+    if (band1 < band0) return FGS_OK;
+    const int band_tiles = (band1 - band0 + 1) * grid_w;
+    k_tile_order<<<(unsigned)((band_tiles + 1023) / 1024), 1024, 0, st>>>(
+        f.starts, f.tileorder, band0 * grid_w, band_tiles, f.stats);
+    FGS_CHECK_LAUNCH();
     return FGS_OK;
 }
 
@@ -1139,6 +1197,10 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
 int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
                     int band1, int bucket, const FrameDev &f, cudaStream_t st)
 {
+    if (bucket) {                       // also for an empty scene: the blend reads the order
+        const int rc = fgs_launch_tile_order(f, cam.grid_w, band0, band1, st);
+        if (rc) return rc;
+    }
     if (P == 0) return FGS_OK;
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     if (bucket) {

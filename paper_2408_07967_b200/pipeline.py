@@ -436,7 +436,7 @@ class Pipeline:
         return fb, stats
 
     def render_many(self, cameras, strategy="precise", tau=TAU_DEFAULT,
-                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=4, streams=2,
+                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=6, streams=3,
                     quantized=False):
         """``list(render_iter(...))``: every view's ``(Framebuffer, FrameStats)``."""
         return list(self.render_iter(cameras, strategy, tau, background, exact=exact,
@@ -452,7 +452,7 @@ class Pipeline:
         return pool[:n]
 
     def render_iter(self, cameras, strategy="precise", tau=TAU_DEFAULT,
-                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=4, streams=2,
+                    background=(0.0, 0.0, 0.0), *, exact=False, contrib=True, depth=6, streams=3,
                     quantized=False):
         """Throughput path for a batch of views (BASELINE config 5; the reference's
         ``bench_frames`` loop, ``pipeline.py:212-233``): same frames and stats as calling
