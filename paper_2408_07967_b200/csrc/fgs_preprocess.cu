@@ -535,6 +535,12 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
     bz[15] = fm(fm(C3_0, x), fs(xx, fm(3.0f, yy)));
 }
 
+__device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
+{
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
+}
+
 // ---------------------------------------------------------------------------
 // K1: preprocess + count
 // ---------------------------------------------------------------------------
@@ -547,6 +553,10 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     __shared__ uint32_t s_red[8];
     __shared__ TileTable s_tab;           // TILE_BUCKET: this CTA's pairs per tile
     __shared__ uint32_t s_bin[4], s_scan[8];
+    // SH staging: plane j of thread t at s_sh[j * 256 + t] (48 KB, dynamic).  A thread's 12
+    // cp.async gathers are issued as soon as its Gaussian passes the frustum test and land
+    // while the covariance chain runs -- no registers held, one DRAM round trip hidden.
+    extern __shared__ __align__(16) float4 s_sh[];
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = g < P;
@@ -570,7 +580,11 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     float zcam = 0.0f;
 
     if (live) {
+        // all four per-Gaussian geometry loads go out together (44 B; the culled ones waste 28)
         const float4 m = sc.g0[g];
+        const float4 sc4 = sc.g1[g];
+        const float4 q = sc.g2[g];
+        const float k = kcut[g];
         const float x = m.x, y = m.y, z = m.z, op = m.w;
         // projection.py:19-26 view_points
         const float t0 = fa(fa(fa(fm(cam.v[0], x), fm(cam.v[1], y)), fm(cam.v[2], z)), cam.v[3]);
@@ -581,9 +595,10 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         ushort4 rect = make_ushort4(0, 0, 0, 0);
         // projection.py:39-47 frustum_mask
         if ((t2 > FGS_Z_NEAR) && (op > frustum_thresh)) {
-            const float4 sc4 = sc.g1[g];
-            const float4 q = sc.g2[g];
-            const float k = kcut[g];
+#pragma unroll
+            for (int j = 0; j < 12; ++j)
+                cp_async16_pre(&s_sh[j * FGS_PRE_THREADS + threadIdx.x], &sc.sh[(int64_t)j * sc.n + g]);
+            asm volatile("cp.async.commit_group;" ::: "memory");
             // projection.py:59-76 quat_to_rotmat (w, x, y, z)
             const float qw = q.x, qx = q.y, qy = q.z, qz = q.w;
             float R[3][3];
@@ -701,9 +716,10 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                 sh_basis(fd(d0, nrm), fd(d1, nrm), fd(d2, nrm), bz);
                 // 48 coefficients as 12 coalesced float4 loads: c[3*i + ch]
                 float cf[48];
+                asm volatile("cp.async.wait_group 0;" ::: "memory");   // own gathers: no barrier needed
 #pragma unroll
                 for (int j = 0; j < 12; ++j) {
-                    const float4 v = sc.sh[(int64_t)j * sc.n + g];
+                    const float4 v = s_sh[j * FGS_PRE_THREADS + threadIdx.x];
                     cf[4 * j] = v.x; cf[4 * j + 1] = v.y; cf[4 * j + 2] = v.z; cf[4 * j + 3] = v.w;
                 }
                 float rgb[3];
@@ -729,6 +745,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                 row[1] = make_float4(cc, op, k, rgb[0]);
                 row[2] = make_float4(rgb[1], rgb[2], hx, hy);
             }
+            asm volatile("cp.async.wait_group 0;" ::: "memory");       // culled after the frustum test
         }
         f.rects[g] = rect;
         f.flags[g] = (uint8_t)((retained ? 1 : 0) | (degenerate ? 2 : 0));
@@ -840,7 +857,20 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
     const double th = tau > 1.0 / 255.0 ? tau : 1.0 / 255.0;       // projection.py:46
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     const float tau32 = (float)tau, fth = (float)th;
-#define FGS_K1(S, B) k_preprocess<S, B><<<blocks, FGS_PRE_THREADS, 0, st>>>( \
+    constexpr int kShBytes = 12 * FGS_PRE_THREADS * 16;            // SH staging, 48 KB
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t ea = cudaSuccess;
+#define FGS_ATTR(S, B) if (ea == cudaSuccess) ea = cudaFuncSetAttribute(k_preprocess<S, B>, \
+        cudaFuncAttributeMaxDynamicSharedMemorySize, kShBytes)
+        FGS_ATTR(FGS_PRECISE, true); FGS_ATTR(FGS_PRECISE, false);
+        FGS_ATTR(FGS_TIGHT_AABB, true); FGS_ATTR(FGS_TIGHT_AABB, false);
+        FGS_ATTR(FGS_BASELINE_CIRCLE_AABB, true); FGS_ATTR(FGS_BASELINE_CIRCLE_AABB, false);
+#undef FGS_ATTR
+        if (ea != cudaSuccess) { fgs_set_cuda_error(ea); return FGS_E_CUDA; }
+        attr_set = true;
+    }
+#define FGS_K1(S, B) k_preprocess<S, B><<<blocks, FGS_PRE_THREADS, kShBytes, st>>>( \
         sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f)
     switch (strategy) {
     case FGS_PRECISE:
