@@ -795,20 +795,28 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     // ---- TILE_BUCKET epilogue: one range per (CTA, tile) in the tile's bucket.  Thread t
     // owns table slots 4t .. 4t+3; entries go to the frame's table list in slot order, each
     // with its offset in K3's write-combining buffer (a prefix of the entries fits).
-    uint32_t cnt[4], nent = 0, npr = 0;
+    // The two global round trips of this epilogue -- the bucket reservations (one atomic per
+    // table entry, result needed for the list) and the list reservation (thread 0) -- are
+    // issued as early as their operands exist and consumed after the block scans, which
+    // hide them.
+    uint32_t cnt[4], tl[4], gb[4], nent = 0, npr = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int e = threadIdx.x * 4 + k;
-        const bool used = s_tab.key[e] != FGS_HT_EMPTY;
+        tl[k] = s_tab.key[e];
+        const bool used = tl[k] != FGS_HT_EMPTY;
         cnt[k] = used ? s_tab.val[e] : 0u;
         nent += used ? 1u : 0u;
         npr += cnt[k];
+        // the counters always get the pairs, so M stays exact when the frame overflows
+        gb[k] = used ? atomicAdd(&f.tilecount[(size_t)tl[k] * FGS_CTR_STRIDE], cnt[k]) : 0u;
     }
     uint32_t tot_ent, tot_pr;
     const uint32_t ent_off = block_excl_scan_256(nent, s_scan, tot_ent);
+    uint32_t lb = 0;
+    if (threadIdx.x == 0 && tot_ent) lb = atomicAdd(&f.stats->list_used, tot_ent);
     uint32_t pr_off = block_excl_scan_256(npr, s_scan, tot_pr);
     if (threadIdx.x == 0) {
-        const uint32_t lb = tot_ent ? atomicAdd(&f.stats->list_used, tot_ent) : 0u;
         s_bin[0] = lb;
         s_bin[1] = (lb + tot_ent <= f.list_capacity) ? 1u : 0u;
         if (tot_ent && lb + tot_ent > f.list_capacity) f.stats->overflow = 1u;   // grow and re-run
@@ -820,14 +828,11 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int e = threadIdx.x * 4 + k;
-        const uint32_t tile = s_tab.key[e];
-        if (tile != FGS_HT_EMPTY) {
-            // the counters always get the pairs, so M stays exact when the frame overflows
-            const uint32_t gb = atomicAdd(&f.tilecount[(size_t)tile * FGS_CTR_STRIDE], cnt[k]);
+        if (tl[k] != FGS_HT_EMPTY) {
             const bool wc = pr_off + cnt[k] <= FGS_WC_CAP;
             if (wc) staged_end = pr_off + cnt[k];
             if (fits)
-                f.tablelist[idx++] = make_uint4(tile, gb, cnt[k],
+                f.tablelist[idx++] = make_uint4(tl[k], gb[k], cnt[k],
                                                 ((uint32_t)e << 16) | (wc ? pr_off : FGS_WC_NONE));
         }
         pr_off += cnt[k];
