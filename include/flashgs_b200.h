@@ -103,7 +103,7 @@ typedef struct fgs_stats {
     uint32_t candidate_tiles_lo;   /* sum of nx*ny over retained, low/high  */
     uint32_t candidate_tiles_hi;
     uint32_t dense_tiles;          /* TILE_BUCKET: tiles with > 8192 pairs       */
-    uint32_t medium_tiles;         /* TILE_BUCKET: tiles with 1025..4096 pairs   */
+    uint32_t medium_tiles;         /* TILE_BUCKET: tiles with 2049..4096 pairs   */
     uint32_t hard_tiles;           /* TILE_BUCKET: tiles sent to the radix fallback */
     uint32_t list_used;            /* TILE_BUCKET: (CTA, tile) table entries of the frame;
                                       at most M, so it fits whenever M fits          */

@@ -38,8 +38,8 @@
 // tile-sort size classes: <= SMALL one CTA per tile; <= DENSE the medium list; beyond,
 // the dense list.  The lists live in spare words of the cursor slots: dense entry i
 // at cursor[i*FGS_CTR_STRIDE + 1], medium entry i at cursor[i*FGS_CTR_STRIDE + 2]
-#define FGS_SMALL_TILE    1024
-#define FGS_DENSE_TILE    4096      // medium: 1025..4096
+#define FGS_SMALL_TILE    2048
+#define FGS_DENSE_TILE    4096      // medium: 2049..4096
 #define FGS_LARGE_TILE    8192      // large: 4097..8192; beyond: dense (entry i of the large
                                     // list at cursor[i*FGS_CTR_STRIDE + 4])
 // internal work counters live behind the public 64-byte stats block (the block is 256

@@ -706,7 +706,7 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
 }
 
 // Size classes (k_scan_tiles sorts the tiles into them):
-//   small   n <= 1024   one CTA per tile, bucket-rank sort
+//   small   n <= 2048   one CTA per tile, bucket-rank sort (4 or 8 records per thread)
 //   medium  n <= 4096   persistent CTAs over the medium list, bucket-rank sort
 //   large   n <= 8192   512 threads, bucket-rank sort without the staging copy
 //   hard    n <= 4096   small / medium tiles the bucket-rank sort gave up on: radix sort
@@ -717,29 +717,46 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
             uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
             uint32_t *__restrict__ hard_list, int write_keys, fgs_stats *__restrict__ stats)
 {
-    __shared__ BucketSmem<256, 4> S;
+    // one buffer, two instantiations: up to 1024 records with 4 per thread, up to 2048 with 8
+    // (35 KB, still 6 CTAs per SM; the grid's dynamic CTA dispatch balances these tiles
+    // better than the medium class's persistent CTAs, which keep 69 KB each)
+    __shared__ __align__(16) unsigned char raw[sizeof(BucketSmem<256, 8>)];
     if (stats->overflow) return;
     const int tile = blockIdx.x;
     const int n = starts[tile + 1] - starts[tile];
     if (n <= 0 || n > FGS_SMALL_TILE) return;
-    if (!tb_sort_tile<256, 4>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+    const bool ok = n <= BucketSmem<256, 4>::CAP
+        ? tb_sort_tile<256, 4>(*reinterpret_cast<BucketSmem<256, 4> *>(raw), tile, rec, vals_out,
+                               keys_out, starts, write_keys)
+        : tb_sort_tile<256, 8>(*reinterpret_cast<BucketSmem<256, 8> *>(raw), tile, rec, vals_out,
+                               keys_out, starts, write_keys);
+    if (!ok &&
         threadIdx.x == 0)
         hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
 }
 
-__global__ void __launch_bounds__(256, 3)
+// medium class: threads per CTA x records per thread = 4096 (tuning knobs)
+#ifndef FGS_MED_NT
+#define FGS_MED_NT   512
+#endif
+#ifndef FGS_MED_MINB
+#define FGS_MED_MINB 3
+#endif
+#define FGS_MED_EMAX (4096 / FGS_MED_NT)
+__global__ void __launch_bounds__(FGS_MED_NT, FGS_MED_MINB)
 k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
                    uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
                    const uint32_t *__restrict__ list, uint32_t *__restrict__ hard_list,
                    int write_keys, fgs_stats *__restrict__ stats)
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
-    BucketSmem<256, 16> &S = *reinterpret_cast<BucketSmem<256, 16> *>(ts_raw);
+    using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX>;
+    Smem &S = *reinterpret_cast<Smem *>(ts_raw);
     if (stats->overflow) return;
     const uint32_t count = stats->medium_tiles;
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
-        if (!tb_sort_tile<256, 16>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+        if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
             threadIdx.x == 0)
             hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
@@ -798,12 +815,12 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
 int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st)
 {
     if (tiles <= 0) return FGS_OK;
-    using MediumSmem = BucketSmem<256, 16>;
+    using MediumSmem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX>;
     using LargeSmem = BucketSmem<512, 16, false>;
     static_assert(LargeSmem::CAP == FGS_LARGE_TILE, "large class = large capacity");
     using TailRadix = TileSortSmem<256, 16>;
     constexpr size_t tail_bytes = ((sizeof(TailRadix) + 15) & ~size_t(15)) + sizeof(BucketSmem<256, 16>);
-    static_assert(BucketSmem<256, 4>::CAP == FGS_SMALL_TILE, "small class = small capacity");
+    static_assert(BucketSmem<256, 8>::CAP == FGS_SMALL_TILE, "small class = small capacity");
     static_assert(MediumSmem::CAP == FGS_DENSE_TILE && TailRadix::CAP == FGS_DENSE_TILE,
                   "medium capacity = radix capacity = chunk size of split buckets");
     static bool attr_set = false;
@@ -836,7 +853,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
                                                  hard_list, write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);
     const unsigned mgrid = (unsigned)(tiles < 3 * sms ? tiles : 3 * sms);
-    k_tile_sort_medium<<<mgrid, 256, sizeof(MediumSmem), st>>>(
+    k_tile_sort_medium<<<mgrid, FGS_MED_NT, sizeof(MediumSmem), st>>>(
         f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
     FGS_AFTER_LAUNCH(st);
     const unsigned dgrid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);
