@@ -579,3 +579,65 @@ def test_device_activate_tracks_the_reference_activation():
     assert abs(sd.pairs_emitted - sh_.pairs_emitted) <= max(2, sh_.pairs_emitted // 10000)
     # an already activated scene is taken as is
     assert fgs.Pipeline(host, device_activate=True).activated is host
+
+
+# ---------------------------------------------------------------------------
+# packed-f32x2 blend: the single alpha >= thr test must reproduce the reference's
+# three skips exactly (contrib flags identical to the exact mode), frames within 2e-5
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("preset,n,seed,w,h,radius,tau", [
+    ("mixed", 40000, 21, 640, 368, 20.0, 1 / 255),
+    ("elongated", 30000, 22, 512, 300, 12.0, 1 / 255),      # kappa-scaled guard band
+    ("isotropic", 8000, 23, 330, 200, 10.0, 0.02),
+    ("mixed", 2000, 24, 97, 61, 5.0, 1 / 255),              # close-up: huge splats, ragged tiles
+])
+def test_packed_blend_never_flips_a_skip(preset, n, seed, w, h, radius, tau):
+    act = fgs.activate(fgs.gen_synthetic(preset, n, seed))
+    pipe = fgs.Pipeline(act)
+    for cam in fgs.orbit_cameras(2, radius, w, h):
+        b = fgs.preprocess_and_bin(pipe, cam, "precise", tau)
+        keys, vals = fgs.sort_pairs(b.keys, b.values, 1, b.grid_w * b.grid_h, n)
+        starts = fgs.tile_range_table(keys, b.grid_w, b.grid_h)
+        for bg in ((0, 0, 0), (1.0, 0.5, 0.25)):
+            ix, cx, _ = fgs.render_frame(b.splat, vals, starts, w, h, bg, tau, exact=True)
+            i2, c2, _ = fgs.render_frame(b.splat, vals, starts, w, h, bg, tau)
+            assert np.array_equal(c2, cx), "a pair's contributes/skipped verdict differs"
+            assert fgs.max_abs_diff(i2, ix) <= 2e-5
+        # alpha / depth maps ride the same packed accumulators
+        ix, _, _, ax, dx = fgs.render_frame(b.splat, vals, starts, w, h, (0, 0, 0), tau, exact=True,
+                                            gaussian_depth=b.depth)
+        i2, _, _, a2, d2 = fgs.render_frame(b.splat, vals, starts, w, h, (0, 0, 0), tau,
+                                            gaussian_depth=b.depth)
+        assert np.abs(a2 - ax).max() <= 2e-5
+        assert np.abs(d2 - dx).max() <= 2e-5 * max(1.0, float(dx.max()))
+
+
+def test_packed_blend_rows_outside_its_shortcut():
+    """Hand-made rows whose extent rectangle is NOT the cutoff ellipse's bounding box
+    (clipped rectangle, opacity above the cap, zero conic terms): the packed kernel must
+    hand them to the reference-order path, so the verdicts still match the exact mode."""
+    rng = np.random.default_rng(5)
+    n, w, h = 600, 160, 96
+    splat = np.zeros((n, 12), np.float32)
+    splat[:, 0] = rng.uniform(-10, w + 10, n)
+    splat[:, 1] = rng.uniform(-10, h + 10, n)
+    sx, sy = rng.uniform(1.5, 14, n), rng.uniform(1.5, 14, n)
+    rho = rng.uniform(-0.9, 0.9, n)
+    cov = np.stack([sx * sx, rho * sx * sy, sy * sy], 1)
+    det = cov[:, 0] * cov[:, 2] - cov[:, 1] ** 2
+    splat[:, 2], splat[:, 3], splat[:, 4] = cov[:, 2] / det, -cov[:, 1] / det, cov[:, 0] / det
+    splat[:, 5] = rng.uniform(0.05, 1.0, n)                       # some above the 0.99 cap
+    splat[:, 6] = np.minimum(9.0, 2 * np.log(splat[:, 5] * 255.0))
+    splat[:, 7:10] = rng.uniform(0, 1, (n, 3))
+    splat[:, 10] = np.sqrt(splat[:, 6] * cov[:, 0]) * rng.choice([1.0, 0.5, 0.25, 2.0], n)   # clipped / loose
+    splat[:, 11] = np.sqrt(splat[:, 6] * cov[:, 2]) * rng.choice([1.0, 0.6, 3.0], n)
+    splat[::50, 3] = 0.0
+    splat[::75, 2:5] = (0.02, 0.0, 0.0)                           # c = 0: degenerate conic
+    gw, gh = -(-w // 16), -(-h // 16)
+    # every Gaussian on every tile, in index order: the blend's own tests do all the culling
+    vals = np.tile(np.arange(n, dtype=np.uint32), gw * gh)
+    starts = np.arange(gw * gh + 1, dtype=np.int64) * n
+    ix, cx, _ = fgs.render_frame(splat, vals, starts, w, h, (0.2, 0.1, 0.0), 1 / 255, exact=True)
+    i2, c2, _ = fgs.render_frame(splat, vals, starts, w, h, (0.2, 0.1, 0.0), 1 / 255)
+    assert cx.any() and np.array_equal(c2, cx)
+    assert fgs.max_abs_diff(i2, ix) <= 2e-5
