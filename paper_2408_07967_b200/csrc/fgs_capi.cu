@@ -23,6 +23,8 @@ void fgs_prof_mark(cudaStream_t st)
         cudaEventRecord((cudaEvent_t)g_prof_events[g_prof_n++], st);
 }
 
+bool fgs_prof_armed() { return g_prof_events != nullptr; }
+
 static CamDev make_cam(const fgs_camera *c)
 {
     CamDev d;

@@ -201,6 +201,7 @@ void fgs_set_cuda_error(cudaError_t e);
 // Records the next caller-supplied profiling event on `st` (no-op unless
 // fgs_profile_begin armed this thread).  Called after every kernel launch.
 void fgs_prof_mark(cudaStream_t st);
+bool fgs_prof_armed();
 
 #define FGS_CHECK_LAUNCH()                                   \
     do {                                                     \

@@ -752,6 +752,9 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX>;
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
+    // the next size class sorts disjoint tiles: let it start beside this one
+    // (programmatic dependent launch, see fgs_launch_tile_sort)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (stats->overflow) return;
     const uint32_t count = stats->medium_tiles;
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
@@ -772,6 +775,7 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Smem = BucketSmem<512, 16, false>;
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (stats->overflow) return;
     const uint32_t count = fgs_work(stats)[FGS_WORK_LARGE];
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
@@ -849,17 +853,47 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     // lists in the spare words of the cursor slots: +1 dense, +2 medium, +3 hard
     uint32_t *dense_list = f.cursor + 1, *medium_list = f.cursor + 2, *hard_list = f.cursor + 3;
     uint32_t *large_list = f.cursor + 4;
-    k_tile_sort<<<(unsigned)tiles, 256, 0, st>>>(f.keys[0], f.vals[0], f.keys[1], f.starts,
-                                                 hard_list, write_keys, f.stats);
-    FGS_AFTER_LAUNCH(st);
     const unsigned mgrid = (unsigned)(tiles < 3 * sms ? tiles : 3 * sms);
-    k_tile_sort_medium<<<mgrid, FGS_MED_NT, sizeof(MediumSmem), st>>>(
-        f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
-    FGS_AFTER_LAUNCH(st);
     const unsigned dgrid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);
-    k_tile_sort_large<<<dgrid, 512, sizeof(LargeSmem), st>>>(
-        f.keys[0], f.vals[0], f.keys[1], f.starts, large_list, dense_list, write_keys, f.stats);
-    FGS_AFTER_LAUNCH(st);
+    // The small / medium / large classes sort disjoint tiles, so they may run side by side:
+    // the persistent kernels go first (all their CTAs are resident at once and trigger
+    // `griddepcontrol.launch_dependents` on entry), the next class is launched with
+    // programmatic stream serialization and starts beside them instead of behind their tail.
+    // None of them reads what another writes; the tail kernel (plain launch) waits for all.
+    // With per-kernel profiling events armed the classes run back to back as before.
+    const bool overlap = !fgs_prof_armed();
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.stream = st;
+    cfg.attrs = pdl;
+    {
+        k_tile_sort_medium<<<mgrid, FGS_MED_NT, sizeof(MediumSmem), st>>>(
+            f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
+        FGS_AFTER_LAUNCH(st);
+    }
+    {
+        cfg.gridDim = dim3(dgrid);
+        cfg.blockDim = dim3(512);
+        cfg.dynamicSmemBytes = sizeof(LargeSmem);
+        cfg.numAttrs = overlap ? 1 : 0;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_tile_sort_large, (const uint64_t *)f.keys[0],
+            f.vals[0], f.keys[1], (const int32_t *)f.starts, (const uint32_t *)large_list, dense_list,
+            write_keys, f.stats);
+        if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+        FGS_AFTER_LAUNCH(st);
+    }
+    {
+        cfg.gridDim = dim3((unsigned)tiles);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = 0;
+        cfg.numAttrs = overlap ? 1 : 0;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_tile_sort, (const uint64_t *)f.keys[0],
+            f.vals[0], f.keys[1], (const int32_t *)f.starts, hard_list, write_keys, f.stats);
+        if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+        FGS_AFTER_LAUNCH(st);
+    }
     k_tile_sort_tail<<<dgrid, 256, tail_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
                                                      f.starts, dense_list, hard_list, write_keys,
                                                      f.stats);
