@@ -393,6 +393,8 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
          uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
 {
     __shared__ Blend2Smem S;
+    fgs_pdl_wait();            // (the tail sort kernel before it is launched the plain way and
+                               // waits for every size class)
     if (stats != nullptr && stats->overflow) return;
     constexpr int B = FGS_B2_BATCH;
     const int tid = threadIdx.x;
@@ -594,11 +596,13 @@ int launch2(bool extras, dim3 grid, cudaStream_t st, const float *splat, const f
             float *depth, uint8_t *contrib, fgs_stats *stats)
 {
     if (extras)
-        k_blend2<CONTRIB, true><<<grid, FGS_B2_THREADS, 0, st>>>(splat, gdepth, vals, inv, starts, order,
-            width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+        FGS_CHAIN((k_blend2<CONTRIB, true>), grid, dim3(FGS_B2_THREADS), 0, st, splat, gdepth, vals, inv,
+                  starts, order, width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha,
+                  depth, contrib, stats);
     else
-        k_blend2<CONTRIB, false><<<grid, FGS_B2_THREADS, 0, st>>>(splat, gdepth, vals, inv, starts, order,
-            width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+        FGS_CHAIN((k_blend2<CONTRIB, false>), grid, dim3(FGS_B2_THREADS), 0, st, splat, gdepth, vals, inv,
+                  starts, order, width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha,
+                  depth, contrib, stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }

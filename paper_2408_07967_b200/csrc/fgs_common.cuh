@@ -220,6 +220,41 @@ bool fgs_prof_armed();
     } while (0)
 
 #ifdef __CUDACC__
+// ---- programmatic dependent launch (PDL) -------------------------------------------------
+// The kernels of a frame form a chain on one stream.  A kernel launched with programmatic
+// stream serialization may be scheduled while its predecessor is still draining; it calls
+// fgs_pdl_wait() before it touches global memory (blocks until the predecessor has completed
+// and its writes are visible) and then fgs_pdl_trigger(), which lets ITS successor be
+// scheduled the same way.  Wait-then-trigger keeps the chain transitive: when a kernel's wait
+// returns, every earlier kernel of the frame has completed.  What is gained is the launch
+// latency and the drain/fill bubble at every kernel boundary.  Both instructions are no-ops
+// in a kernel launched the plain way (profiling passes launch everything the plain way).
+__device__ __forceinline__ void fgs_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void fgs_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+static inline cudaError_t fgs_launch_chain(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                           cudaStream_t st, bool pdl, Args... args)
+{
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, KArgs(args)...);
+}
+#define FGS_CHAIN(kernel, grid, block, smem, st, ...)                                              \
+    do {                                                                                           \
+        const cudaError_t e__ = fgs_launch_chain(kernel, grid, block, smem, st, !fgs_prof_armed(), \
+                                                 __VA_ARGS__);                                     \
+        if (e__ != cudaSuccess) { fgs_set_cuda_error(e__); return FGS_E_CUDA; }                    \
+    } while (0)
+
 // Individually rounded float32 / float64 arithmetic: these intrinsics are never
 // contracted into FMAs, which is what keeps the geometry bit-identical to the
 // reference's NumPy ufunc chains.

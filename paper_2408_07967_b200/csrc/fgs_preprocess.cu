@@ -557,6 +557,8 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     // cp.async gathers are issued as soon as its Gaussian passes the frustum test and land
     // while the covariance chain runs -- no registers held, one DRAM round trip hidden.
     extern __shared__ __align__(16) float4 s_sh[];
+    fgs_pdl_trigger();                    // first kernel of the frame (plain launch): the tile
+                                          // scan may be scheduled behind this grid's last wave
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = g < P;
@@ -971,6 +973,8 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
 {
     __shared__ unsigned long long s_w[32];
     __shared__ uint32_t s_bin[FGS_ORDER_BINS];
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
     if (threadIdx.x < FGS_ORDER_BINS) s_bin[threadIdx.x] = 0u;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int first = blockIdx.x * 1024;
@@ -1041,8 +1045,8 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
 
 int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st)
 {
-    k_scan_tiles<<<(unsigned)((tiles + 1023) / 1024), 1024, 0, st>>>(
-        f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats);
+    FGS_CHAIN(k_scan_tiles, dim3((unsigned)((tiles + 1023) / 1024)), dim3(1024), 0, st,
+              f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
@@ -1056,6 +1060,8 @@ k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int
              int band_tiles, const fgs_stats *__restrict__ stats)
 {
     __shared__ uint32_t s_base[FGS_ORDER_BINS], s_cnt[FGS_ORDER_BINS], s_off[FGS_ORDER_BINS];
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
     if (stats->overflow) return;
     const int t = threadIdx.x;
     if (t < FGS_ORDER_BINS) s_cnt[t] = 0u;
@@ -1091,8 +1097,8 @@ int fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, c
 {
     if (band1 < band0) return FGS_OK;
     const int band_tiles = (band1 - band0 + 1) * grid_w;
-    k_tile_order<<<(unsigned)((band_tiles + 1023) / 1024), 1024, 0, st>>>(
-        f.starts, f.tileorder, band0 * grid_w, band_tiles, f.stats);
+    FGS_CHAIN(k_tile_order, dim3((unsigned)((band_tiles + 1023) / 1024)), dim3(1024), 0, st,
+              f.starts, f.tileorder, band0 * grid_w, band_tiles, f.stats);
     FGS_CHECK_LAUNCH();
     return FGS_OK;
 }
@@ -1171,6 +1177,8 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
 {
     extern __shared__ __align__(16) unsigned char place_raw[];
     PlaceSmem &S = *reinterpret_cast<PlaceSmem *>(place_raw);
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
     if (f.stats->overflow) return;                       // uniform: grow and re-run
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const bool live = g < P;
@@ -1252,11 +1260,11 @@ int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strate
             attr_set = true;
         }
         if (strategy == FGS_PRECISE)
-            k_place<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, sizeof(PlaceSmem), st>>>(
-                (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
+            FGS_CHAIN(k_place<FGS_PRECISE>, dim3(blocks), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,
+                      (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
         else
-            k_place<FGS_TIGHT_AABB><<<blocks, FGS_PRE_THREADS, sizeof(PlaceSmem), st>>>(
-                (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
+            FGS_CHAIN(k_place<FGS_TIGHT_AABB>, dim3(blocks), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,
+                      (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
     } else if (strategy == FGS_PRECISE) {
         k_emit<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, 0, st>>>(
             (int)P, cam.width, cam.height, cam.grid_w, band0, band1, f);

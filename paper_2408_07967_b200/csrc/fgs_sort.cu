@@ -752,9 +752,10 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX>;
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
-    // the next size class sorts disjoint tiles: let it start beside this one
-    // (programmatic dependent launch, see fgs_launch_tile_sort)
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    // first of the size classes: waits for the placement kernel, then lets the next class
+    // (disjoint tiles, launched without a wait of its own) start beside this one
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
     if (stats->overflow) return;
     const uint32_t count = stats->medium_tiles;
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
@@ -775,7 +776,7 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Smem = BucketSmem<512, 16, false>;
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    fgs_pdl_trigger();      // no wait: released only after the medium class's wait returned
     if (stats->overflow) return;
     const uint32_t count = fgs_work(stats)[FGS_WORK_LARGE];
     for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
@@ -796,6 +797,8 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
                  const uint32_t *__restrict__ hard_list, int write_keys,
                  const fgs_stats *__restrict__ stats)
 {
+    fgs_pdl_trigger();      // plain launch (waits for every size class); the blend may queue up
+
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Radix = TileSortSmem<256, 16>;
     Radix &S = *reinterpret_cast<Radix *>(ts_raw);
@@ -869,8 +872,8 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     cfg.stream = st;
     cfg.attrs = pdl;
     {
-        k_tile_sort_medium<<<mgrid, FGS_MED_NT, sizeof(MediumSmem), st>>>(
-            f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
+        FGS_CHAIN(k_tile_sort_medium, dim3(mgrid), dim3(FGS_MED_NT), sizeof(MediumSmem), st,
+                  f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
         FGS_AFTER_LAUNCH(st);
     }
     {
