@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("FGS_LIB") or os.path.join(HERE, "_lib", "libflashgs_b
 ABI_VERSION = 4
 STRATEGIES = ("baseline-circle-aabb", "tight-aabb", "precise")   # binning.py:38 order
 STRATEGY_ID = {"precise": 0, "tight-aabb": 1, "baseline-circle-aabb": 2}
-BLEND_EXACT, BLEND_CONTRIB = 1, 2
+BLEND_EXACT, BLEND_CONTRIB, BLEND_SCALAR = 1, 2, 4
 SORT_ONESWEEP, SORT_TILE_BUCKET = 0, 1
 SORT_MODES = {"onesweep": SORT_ONESWEEP, "tile-bucket": SORT_TILE_BUCKET}
 SORT_TILE = 4096
