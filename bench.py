@@ -521,7 +521,9 @@ def main():
                            "D2H behind the view's kernels on its stream; views round-robin on "
                            "%d streams) + FrameStats" % nlanes,
                     "single_call_ms": single_ms},
-            "gpu_launches": int(n_marks * K),
+            # kernels of this library launched inside the timed region: the profiling marks
+            # (one per stage kernel) + k_tile_order, which shares the emit stage's mark
+            "gpu_launches": int((n_marks + (1 if bucket else 0)) * K),
             "roofline": roof,
             "cpu_baseline": cpu,
             "kernels": kernels,
