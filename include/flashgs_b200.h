@@ -138,9 +138,9 @@ typedef struct fgs_layout {
     uint64_t off_cursor;       /* uint32 [tiles][8]: size-class tile lists (words 1..3) */
     uint64_t off_ctainfo;      /* uint32 [preprocess blocks][4]: TILE_BUCKET, each K1 CTA's
                                   (first table entry, entries, write-combined records, 0) */
-    uint64_t off_tileorder;    /* uint32 [128 + tiles]: TILE_BUCKET, 64 size-bin counts, 64 bin
-                                  cursors, then the band's tiles ordered heaviest first (the
-                                  order the blend's CTAs take them in)                    */
+    uint64_t off_tileorder;    /* uint32 [160 + tiles]: TILE_BUCKET, 64 size-bin counts, 64 bin
+                                  cursors, 32 control words, then the band's tiles ordered
+                                  heaviest first (the order the blend's CTAs take them in) */
     int64_t  gaussians, capacity;   /* capacity = the request rounded up to 64 pairs */
     int32_t  width, height, grid_w, grid_h, tiles, tile_bits;
     int32_t  preprocess_blocks, sort_passes;

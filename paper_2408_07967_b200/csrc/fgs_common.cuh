@@ -52,7 +52,7 @@
 #ifndef FGS_ORDER_MBITS
 #define FGS_ORDER_MBITS   2        // mantissa bits of the size bins (2: quarter octaves)
 #endif
-#define FGS_ORDER_HDR     (2 * FGS_ORDER_BINS)
+#define FGS_ORDER_HDR     (2 * FGS_ORDER_BINS + 32)   // bin counts, bin cursors, [128] = CTAs done
 static __host__ __device__ inline uint32_t *fgs_work(fgs_stats *s) { return (uint32_t *)(s + 1); }
 static __host__ __device__ inline const uint32_t *fgs_work(const fgs_stats *s) { return (const uint32_t *)(s + 1); }
 

@@ -1091,6 +1091,13 @@ k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int
     // Tiles outside the band are empty and were counted in the last bin by k_scan_tiles;
     // only the band's tiles are placed, so the first band_tiles entries are exactly the band.
     if (i < band_tiles) hdr[FGS_ORDER_HDR + s_base[bin] + s_off[bin] + rank] = (uint32_t)(first_tile + i);
+    // the last CTA out rewinds the cursors, so running the stage again on the same frame
+    // (fgs_emit is otherwise idempotent) rebuilds the same order instead of writing past it
+    __syncthreads();
+    if (t == 0 && atomicAdd(&hdr[2 * FGS_ORDER_BINS], 1u) == gridDim.x - 1) {
+        for (int b = 0; b < FGS_ORDER_BINS; ++b) hdr[FGS_ORDER_BINS + b] = 0u;
+        hdr[2 * FGS_ORDER_BINS] = 0u;
+    }
 }
 
 int fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st)

@@ -641,3 +641,38 @@ def test_packed_blend_rows_outside_its_shortcut():
     i2, c2, _ = fgs.render_frame(splat, vals, starts, w, h, (0.2, 0.1, 0.0), 1 / 255)
     assert cx.any() and np.array_equal(c2, cx)
     assert fgs.max_abs_diff(i2, ix) <= 2e-5
+
+
+def test_stages_can_be_repeated_on_one_frame():
+    """fgs_emit (tile order + placement) and fgs_blend are idempotent on a frame: running
+    them again -- another background, a re-issued stage -- gives the same frame."""
+    import ctypes as C
+    import torch
+    from paper_2408_07967_b200 import _capi
+    n, w, h = 30000, 400, 240
+    act = fgs.activate(fgs.gen_synthetic("mixed", n, 31))
+    cam = fgs.orbit_cameras(1, 20.0, w, h)[0]
+    pipe = fgs.Pipeline(act)
+    want, _ = pipe.render(cam)
+    L = _capi.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    ws = fgs.pipeline._Workspace(torch, dev, n, w, h, pipe._default_capacity())
+    ws.set_mode(_capi.SORT_MODES["tile-bucket"])
+    kcut = pipe._cutoffs(torch, 1 / 255)
+    camc = _capi.camera_struct(cam)
+    gh = -(-h // 16)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    base, lay = C.c_void_p(ws.base), C.byref(ws.lay)
+    bg = (C.c_float * 3)(0, 0, 0)
+    _capi.check(L.fgs_preprocess(pipe.packed.data_ptr(), kcut.data_ptr(), n, C.byref(camc), 1 / 255,
+                                 3, 0, 0, gh - 1, base, lay, st))
+    _capi.check(L.fgs_scan(base, lay, st))
+    for _ in range(3):
+        _capi.check(L.fgs_emit(pipe.packed.data_ptr(), C.byref(camc), 0, 0, gh - 1, base, lay, st))
+    _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
+    _capi.check(L.fgs_ranges(base, lay, st))
+    for _ in range(2):
+        _capi.check(L.fgs_blend(pipe.packed.data_ptr(), bg, 1 / 255, 2, 0, gh - 1, ws.rgb.data_ptr(),
+                                None, None, base, lay, st))
+    torch.cuda.synchronize()
+    assert np.array_equal(ws.rgb.cpu().numpy(), want.image)
