@@ -551,7 +551,6 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
              int sh_degree, int band0, int band1, FrameDev f)
 {
     __shared__ uint32_t s_red[8];
-    __shared__ TileTable s_tab;           // TILE_BUCKET: this CTA's pairs per tile
     __shared__ uint32_t s_bin[4], s_scan[8];
     // SH staging: plane j of thread t at s_sh[j * 256 + t] (48 KB, dynamic).  A thread's 12
     // cp.async gathers are issued as soon as its Gaussian passes the frustum test and land
@@ -562,14 +561,10 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = g < P;
-    if (BUCKET) {
-        for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) {
-            s_tab.key[i] = FGS_HT_EMPTY;
-            s_tab.val[i] = 0u;
-        }
-        if (threadIdx.x == 0) s_bin[2] = 0u;
-        __syncthreads();
-    }
+    // TILE_BUCKET: this CTA's pairs per tile.  The table takes over the SH staging buffer once
+    // every thread has consumed its coefficients (the CTA then needs 48 KB, not 56).
+    TileTable &s_tab = *reinterpret_cast<TileTable *>(s_sh);
+    if (BUCKET && threadIdx.x == 0) s_bin[2] = 0u;
 
     TileJob job;
     job.cand = 0;
@@ -716,31 +711,29 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                 nrm = nrm > 0.0f ? nrm : 1.0f;
                 float bz[16];
                 sh_basis(fd(d0, nrm), fd(d1, nrm), fd(d2, nrm), bz);
-                // 48 coefficients as 12 coalesced float4 loads: c[3*i + ch]
-                float cf[48];
+                // The 48 coefficients c[3*i + ch] stream out of the staging buffer one float4 at
+                // a time; every channel still accumulates its terms in the reference's order
+                // (render.py:60-85), so the colours stay bit-exact, and only the running sums
+                // are live (no 48-register coefficient array).
                 asm volatile("cp.async.wait_group 0;" ::: "memory");   // own gathers: no barrier needed
+                float rgb[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
                 for (int j = 0; j < 12; ++j) {
-                    const float4 v = s_sh[j * FGS_PRE_THREADS + threadIdx.x];
-                    cf[4 * j] = v.x; cf[4 * j + 1] = v.y; cf[4 * j + 2] = v.z; cf[4 * j + 3] = v.w;
-                }
-                float rgb[3];
+                    const float4 v4 = s_sh[j * FGS_PRE_THREADS + threadIdx.x];
+                    const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
-                for (int ch = 0; ch < 3; ++ch) {
-                    float res = fm(0.28209479177387814f, cf[ch]);
-                    if (sh_degree >= 1)
-                        res = fs(fa(fs(res, fm(bz[1], cf[3 + ch])), fm(bz[2], cf[6 + ch])),
-                                 fm(bz[3], cf[9 + ch]));
-                    if (sh_degree >= 2) {
-#pragma unroll
-                        for (int i = 4; i < 9; ++i) res = fa(res, fm(bz[i], cf[3 * i + ch]));
+                    for (int u = 0; u < 4; ++u) {
+                        const int fi = 4 * j + u, i = fi / 3, ch = fi % 3;
+                        const float v = vv[u];
+                        if (i == 0) rgb[ch] = fm(0.28209479177387814f, v);
+                        else if (i == 1 || i == 3) { if (sh_degree >= 1) rgb[ch] = fs(rgb[ch], fm(bz[i], v)); }
+                        else if (i == 2) { if (sh_degree >= 1) rgb[ch] = fa(rgb[ch], fm(bz[i], v)); }
+                        else if (i < 9) { if (sh_degree >= 2) rgb[ch] = fa(rgb[ch], fm(bz[i], v)); }
+                        else { if (sh_degree >= 3) rgb[ch] = fa(rgb[ch], fm(bz[i], v)); }
                     }
-                    if (sh_degree >= 3) {
-#pragma unroll
-                        for (int i = 9; i < 16; ++i) res = fa(res, fm(bz[i], cf[3 * i + ch]));
-                    }
-                    rgb[ch] = fmaxf(fa(res, 0.5f), 0.0f);
                 }
+#pragma unroll
+                for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(fa(rgb[ch], 0.5f), 0.0f);
                 // render.py:34-40 splat row, binning.py:235-241
                 float4 *row = (float4 *)(f.splat + (size_t)g * 12);
                 row[0] = make_float4(px, py, ca, cb);
@@ -756,6 +749,12 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     uint32_t npairs;
     uint64_t passmask = 0;
     if (BUCKET) {
+        __syncthreads();                  // every thread is done with the SH staging buffer
+        for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) {
+            s_tab.key[i] = FGS_HT_EMPTY;
+            s_tab.val[i] = 0u;
+        }
+        __syncthreads();
         const BinCtx bc{&s_tab, f.tilecount, nullptr, nullptr, nullptr, nullptr, nullptr};
         npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_BIN>(
             job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, &bc, &passmask);
