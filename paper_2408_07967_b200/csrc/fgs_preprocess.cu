@@ -535,6 +535,10 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
     bz[15] = fm(fm(C3_0, x), fs(xx, fm(3.0f, yy)));
 }
 
+#ifndef FGS_SH_STAGED
+#define FGS_SH_STAGED 12          // SH float4 planes staged in shared memory (of 12)
+#endif
+static_assert(FGS_SH_STAGED * FGS_PRE_THREADS * 16 >= (int)sizeof(TileTable), "the tile table aliases the staging buffer");
 __device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
 {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
@@ -593,7 +597,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         // projection.py:39-47 frustum_mask
         if ((t2 > FGS_Z_NEAR) && (op > frustum_thresh)) {
 #pragma unroll
-            for (int j = 0; j < 12; ++j)
+            for (int j = 0; j < FGS_SH_STAGED; ++j)
                 cp_async16_pre(&s_sh[j * FGS_PRE_THREADS + threadIdx.x], &sc.sh[(int64_t)j * sc.n + g]);
             asm volatile("cp.async.commit_group;" ::: "memory");
             // projection.py:59-76 quat_to_rotmat (w, x, y, z)
@@ -717,9 +721,15 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                 // are live (no 48-register coefficient array).
                 asm volatile("cp.async.wait_group 0;" ::: "memory");   // own gathers: no barrier needed
                 float rgb[3] = {0.0f, 0.0f, 0.0f};
+                // planes beyond the staged ones come straight from global memory, issued here
+                // and consumed last (the staging buffer is what caps the CTAs per SM)
+                float4 late[12 - FGS_SH_STAGED + 1];
+#pragma unroll
+                for (int j = FGS_SH_STAGED; j < 12; ++j) late[j - FGS_SH_STAGED] = sc.sh[(int64_t)j * sc.n + g];
 #pragma unroll
                 for (int j = 0; j < 12; ++j) {
-                    const float4 v4 = s_sh[j * FGS_PRE_THREADS + threadIdx.x];
+                    const float4 v4 = j < FGS_SH_STAGED ? s_sh[j * FGS_PRE_THREADS + threadIdx.x]
+                                                        : late[j < FGS_SH_STAGED ? 0 : j - FGS_SH_STAGED];
                     const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
@@ -863,7 +873,7 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
     const double th = tau > 1.0 / 255.0 ? tau : 1.0 / 255.0;       // projection.py:46
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     const float tau32 = (float)tau, fth = (float)th;
-    constexpr int kShBytes = 12 * FGS_PRE_THREADS * 16;            // SH staging, 48 KB
+    constexpr int kShBytes = FGS_SH_STAGED * FGS_PRE_THREADS * 16; // SH staging, 4 KB per plane
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t ea = cudaSuccess;
