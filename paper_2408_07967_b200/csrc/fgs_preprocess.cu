@@ -325,7 +325,12 @@ enum { WALK_COUNT = 0, WALK_BIN = 1, WALK_EMIT = 2, WALK_PLACE = 3 };
 #define FGS_HT_SIZE   1024
 #define FGS_HT_PROBES 16
 #define FGS_HT_EMPTY  0xffffffffu
+#ifndef FGS_WC_CAP
 #define FGS_WC_CAP    3072          // records the CTA's write-combining buffer holds
+#endif
+#ifndef FGS_PLACE_MINBLOCKS
+#define FGS_PLACE_MINBLOCKS 1
+#endif
 #define FGS_WC_NONE   0xffffu       // table entry whose range is written directly
 struct TileTable {
     uint32_t key[FGS_HT_SIZE];      // tile index, FGS_HT_EMPTY = free
@@ -1187,7 +1192,7 @@ struct PlaceSmem {
 };
 
 template <int STRAT>
-__global__ void __launch_bounds__(FGS_PRE_THREADS)
+__global__ void __launch_bounds__(FGS_PRE_THREADS, FGS_PLACE_MINBLOCKS)
 k_place(int P, int width, int height, int grid_w, int band0, int band1,
         const uint32_t *__restrict__ orig, FrameDev f)
 {
