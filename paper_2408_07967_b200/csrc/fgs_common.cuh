@@ -68,7 +68,8 @@ struct CamDev {
 };
 
 // Packed device scene: float4 planes of stride `n` (P rounded up to 32), in SLOT order.
-//   g0[i] = (mean.xyz, opacity)   g1[i] = (scale.xyz, 0)   g2[i] = quat wxyz
+//   g0[i] = (mean.xyz, opacity)   g1[i] = (S00, S01, S02, S11)   g2[i] = (S12, S22, 0, 0)
+//   with S the 3D covariance R diag(s^2) R^T evaluated once per scene (projection.py:59-85)
 //   sh[j*n + i] = floats 4j..4j+3 of slot i's 48 SH coefficients
 //   orig[i] = index the caller knows the Gaussian in slot i by;  inv[orig[i]] = i
 // Slot order is the caller's order unless fgs_scene_pack was given a permutation (the

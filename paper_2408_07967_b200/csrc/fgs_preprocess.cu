@@ -24,6 +24,35 @@
 // ---------------------------------------------------------------------------
 // per-scene kernels
 // ---------------------------------------------------------------------------
+// projection.py:59-76 quat_to_rotmat (w, x, y, z), 79-85 compute_cov3d: M = R diag(s),
+// S = M M^T as left-to-right 3-term sums of individually rounded products.  S is bitwise
+// symmetric (the products commute), so the six entries S00 S01 S02 S11 S12 S22 carry it.
+__device__ __forceinline__ void fgs_cov3d(float sx, float sy, float sz, float qw, float qx,
+                                          float qy, float qz, float *S6)
+{
+    float R[3][3];
+    R[0][0] = fs(1.0f, fm(2.0f, fa(fm(qy, qy), fm(qz, qz))));
+    R[0][1] = fm(2.0f, fs(fm(qx, qy), fm(qw, qz)));
+    R[0][2] = fm(2.0f, fa(fm(qx, qz), fm(qw, qy)));
+    R[1][0] = fm(2.0f, fa(fm(qx, qy), fm(qw, qz)));
+    R[1][1] = fs(1.0f, fm(2.0f, fa(fm(qx, qx), fm(qz, qz))));
+    R[1][2] = fm(2.0f, fs(fm(qy, qz), fm(qw, qx)));
+    R[2][0] = fm(2.0f, fs(fm(qx, qz), fm(qw, qy)));
+    R[2][1] = fm(2.0f, fa(fm(qy, qz), fm(qw, qx)));
+    R[2][2] = fs(1.0f, fm(2.0f, fa(fm(qx, qx), fm(qy, qy))));
+    const float s3[3] = {sx, sy, sz};
+    float M[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) M[i][j] = fm(R[i][j], s3[j]);
+    const int ii[6] = {0, 0, 0, 1, 1, 2}, kk[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+    for (int e = 0; e < 6; ++e)
+        S6[e] = fa(fa(fm(M[ii[e]][0], M[kk[e]][0]), fm(M[ii[e]][1], M[kk[e]][1])),
+                   fm(M[ii[e]][2], M[kk[e]][2]));
+}
+
 __global__ void __launch_bounds__(128)
 k_scene_pack(const float *__restrict__ means, const float *__restrict__ opac,
              const float *__restrict__ scales, const float *__restrict__ rots,
@@ -40,11 +69,17 @@ k_scene_pack(const float *__restrict__ means, const float *__restrict__ opac,
     const int64_t g = g0 + lane;
     const bool live = g < P;
     const int64_t src = live ? (order ? (int64_t)order[g] : g) : 0;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = make_float4(1.f, 0.f, 0.f, 0.f);
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
     if (live) {
         a = make_float4(means[3 * src], means[3 * src + 1], means[3 * src + 2], opac[src]);
-        b = make_float4(scales[3 * src], scales[3 * src + 1], scales[3 * src + 2], 0.f);
-        c = make_float4(rots[4 * src], rots[4 * src + 1], rots[4 * src + 2], rots[4 * src + 3]);
+        // The 3D covariance is camera-independent (projection.py:59-85), so it is evaluated
+        // once per scene, here, with the reference's individually rounded operations; K1
+        // reads its six distinct entries instead of scale + quaternion (same 32 bytes).
+        float S[6];
+        fgs_cov3d(scales[3 * src], scales[3 * src + 1], scales[3 * src + 2], rots[4 * src],
+                  rots[4 * src + 1], rots[4 * src + 2], rots[4 * src + 3], S);
+        b = make_float4(S[0], S[1], S[2], S[3]);       // S00 S01 S02 S11
+        c = make_float4(S[4], S[5], 0.f, 0.f);         // S12 S22
     }
     out[g] = a;
     out[n + g] = b;
@@ -605,31 +640,10 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
             for (int j = 0; j < FGS_SH_STAGED; ++j)
                 cp_async16_pre(&s_sh[j * FGS_PRE_THREADS + threadIdx.x], &sc.sh[(int64_t)j * sc.n + g]);
             asm volatile("cp.async.commit_group;" ::: "memory");
-            // projection.py:59-76 quat_to_rotmat (w, x, y, z)
-            const float qw = q.x, qx = q.y, qy = q.z, qz = q.w;
-            float R[3][3];
-            R[0][0] = fs(1.0f, fm(2.0f, fa(fm(qy, qy), fm(qz, qz))));
-            R[0][1] = fm(2.0f, fs(fm(qx, qy), fm(qw, qz)));
-            R[0][2] = fm(2.0f, fa(fm(qx, qz), fm(qw, qy)));
-            R[1][0] = fm(2.0f, fa(fm(qx, qy), fm(qw, qz)));
-            R[1][1] = fs(1.0f, fm(2.0f, fa(fm(qx, qx), fm(qz, qz))));
-            R[1][2] = fm(2.0f, fs(fm(qy, qz), fm(qw, qx)));
-            R[2][0] = fm(2.0f, fs(fm(qx, qz), fm(qw, qy)));
-            R[2][1] = fm(2.0f, fa(fm(qy, qz), fm(qw, qx)));
-            R[2][2] = fs(1.0f, fm(2.0f, fa(fm(qx, qx), fm(qy, qy))));
-            // projection.py:79-85 compute_cov3d: M = R diag(s), S = M M^T
-            const float s3[3] = {sc4.x, sc4.y, sc4.z};
-            float M[3][3], S[3][3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int j = 0; j < 3; ++j) M[i][j] = fm(R[i][j], s3[j]);
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-#pragma unroll
-                for (int kx = 0; kx < 3; ++kx)
-                    S[i][kx] = fa(fa(fm(M[i][0], M[kx][0]), fm(M[i][1], M[kx][1])),
-                                  fm(M[i][2], M[kx][2]));
+            // projection.py:59-85: the 3D covariance, evaluated per scene by fgs_scene_pack
+            float S[3][3];
+            S[0][0] = sc4.x; S[0][1] = S[1][0] = sc4.y; S[0][2] = S[2][0] = sc4.z;
+            S[1][1] = sc4.w; S[1][2] = S[2][1] = q.x;   S[2][2] = q.y;
             // projection.py:88-121 compute_cov2d
             const float tz = t2 > 1e-3f ? t2 : 1e-3f;
             const float rx = fd(t0, tz), ry = fd(t1, tz);
