@@ -343,7 +343,7 @@ __device__ __forceinline__ pk2 bc(float v) { return pk(v, v); }   // broadcast o
 #define FGS_B2_THREADS 128
 #define FGS_B2_BATCH   128
 #ifndef FGS_B2_MINCTAS
-#define FGS_B2_MINCTAS 1
+#define FGS_B2_MINCTAS 9       // 56 registers, no spills: 36 warps/SM (10 = 48 registers + spills: slower)
 #endif
 #ifndef FGS_B2_UNROLL
 #define FGS_B2_UNROLL  16
