@@ -45,6 +45,8 @@
 // internal work counters live behind the public 64-byte stats block (the block is 256
 // bytes in the workspace and zeroed with it at the start of every frame)
 #define FGS_WORK_LARGE    0
+#define FGS_WORK_MEDIUM_TICKET 2   // (+1: CTAs out) tile tickets of the persistent sort kernels
+#define FGS_WORK_LARGE_TICKET  4   // (+1: CTAs out)
 // blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
 // empty = last) and the blend's CTAs take them in bin order, so the long tiles start first
 // and the grid's tail is made of short ones

@@ -705,6 +705,40 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
     }
 }
 
+// Persistent size-class kernels take their tiles from a ticket counter (the frame's zeroed
+// work block: word `slot` = next list entry, word `slot + 1` = CTAs that have left): tiles
+// of one class differ 2x in size, and a static stride leaves SMs idle behind the unlucky
+// CTAs.  The next ticket is drawn before the current tile is sorted, so its round trip is
+// hidden.  The last CTA out rewinds both words: the stage can be re-issued on the frame.
+struct TileTickets {
+    uint32_t *ctr;
+    uint32_t next;
+    __device__ __forceinline__ void open(fgs_stats *stats, int slot)
+    {
+        ctr = fgs_work(stats) + slot;
+        next = threadIdx.x == 0 ? atomicAdd(ctr, 1u) : 0u;
+    }
+    // returns the list entry this CTA sorts now (uniform), draws the one after it
+    __device__ __forceinline__ uint32_t take(uint32_t *bcast)
+    {
+        if (threadIdx.x == 0) {
+            *bcast = next;
+            next = atomicAdd(ctr, 1u);
+        }
+        __syncthreads();
+        const uint32_t i = *bcast;
+        __syncthreads();
+        return i;
+    }
+    __device__ __forceinline__ void close()
+    {
+        if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+            ctr[0] = 0u;
+            ctr[1] = 0u;
+        }
+    }
+};
+
 // Size classes (k_scan_tiles sorts the tiles into them):
 //   small   n <= 2048   one CTA per tile, bucket-rank sort (4 or 8 records per thread)
 //   medium  n <= 4096   persistent CTAs over the medium list, bucket-rank sort
@@ -757,14 +791,19 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     fgs_pdl_wait();
     fgs_pdl_trigger();
     if (stats->overflow) return;
+    __shared__ uint32_t s_ticket;
     const uint32_t count = stats->medium_tiles;
-    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+    if (count == 0u) return;               // empty class: no ticket traffic
+    TileTickets tk;
+    tk.open(stats, FGS_WORK_MEDIUM_TICKET);
+    for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
         if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
             threadIdx.x == 0)
             hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
     }
+    tk.close();
 }
 
 __global__ void __launch_bounds__(512, 2)
@@ -778,14 +817,19 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
     fgs_pdl_trigger();      // no wait: released only after the medium class's wait returned
     if (stats->overflow) return;
+    __shared__ uint32_t s_ticket;
     const uint32_t count = fgs_work(stats)[FGS_WORK_LARGE];
-    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+    if (count == 0u) return;
+    TileTickets tk;
+    tk.open(stats, FGS_WORK_LARGE_TICKET);
+    for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
         if (!tb_sort_tile<512, 16, false>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
             threadIdx.x == 0)      // clustered depths: let the splitting kernel take it
             dense_list[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
     }
+    tk.close();
 }
 
 // The tail of the tile sort, one launch: the dense list (split path), then the hard list
