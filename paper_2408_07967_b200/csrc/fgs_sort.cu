@@ -705,25 +705,30 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
     }
 }
 
-// Persistent size-class kernels take their tiles from a ticket counter (the frame's zeroed
-// work block: word `slot` = next list entry, word `slot + 1` = CTAs that have left): tiles
-// of one class differ 2x in size, and a static stride leaves SMs idle behind the unlucky
-// CTAs.  The next ticket is drawn before the current tile is sorted, so its round trip is
-// hidden.  The last CTA out rewinds both words: the stage can be re-issued on the frame.
+// Persistent size-class kernels: CTA b sorts list entry b first and then takes further
+// entries from a ticket counter (the frame's zeroed work block: word `slot` = tickets drawn,
+// word `slot + 1` = CTAs that have left) -- tiles of one class differ 2x in size, and a
+// static stride leaves SMs idle behind the unlucky CTAs.  The next ticket is drawn before
+// the current tile is sorted, so its round trip is hidden; CTAs without a first entry never
+// touch the counter (L2 serialises same-address atomics: ~20 ns each).  The last working CTA
+// out rewinds both words, so the stage can be re-issued on the frame.
 struct TileTickets {
     uint32_t *ctr;
-    uint32_t next;
-    __device__ __forceinline__ void open(fgs_stats *stats, int slot)
+    uint32_t next, count;
+    // false: this CTA has no work at all
+    __device__ __forceinline__ bool open(fgs_stats *stats, int slot, uint32_t n)
     {
         ctr = fgs_work(stats) + slot;
-        next = threadIdx.x == 0 ? atomicAdd(ctr, 1u) : 0u;
+        count = n;
+        next = blockIdx.x;
+        return blockIdx.x < n;
     }
-    // returns the list entry this CTA sorts now (uniform), draws the one after it
+    // returns the list entry this CTA sorts now (uniform; >= count: done), draws the one after
     __device__ __forceinline__ uint32_t take(uint32_t *bcast)
     {
         if (threadIdx.x == 0) {
             *bcast = next;
-            next = atomicAdd(ctr, 1u);
+            if (next < count) next = gridDim.x + atomicAdd(ctr, 1u);
         }
         __syncthreads();
         const uint32_t i = *bcast;
@@ -732,7 +737,8 @@ struct TileTickets {
     }
     __device__ __forceinline__ void close()
     {
-        if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == gridDim.x - 1) {
+        const uint32_t workers = count < gridDim.x ? count : gridDim.x;
+        if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == workers - 1u) {
             ctr[0] = 0u;
             ctr[1] = 0u;
         }
@@ -793,9 +799,8 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     if (stats->overflow) return;
     __shared__ uint32_t s_ticket;
     const uint32_t count = stats->medium_tiles;
-    if (count == 0u) return;               // empty class: no ticket traffic
     TileTickets tk;
-    tk.open(stats, FGS_WORK_MEDIUM_TICKET);
+    if (!tk.open(stats, FGS_WORK_MEDIUM_TICKET, count)) return;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
         if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
@@ -819,9 +824,8 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     if (stats->overflow) return;
     __shared__ uint32_t s_ticket;
     const uint32_t count = fgs_work(stats)[FGS_WORK_LARGE];
-    if (count == 0u) return;
     TileTickets tk;
-    tk.open(stats, FGS_WORK_LARGE_TICKET);
+    if (!tk.open(stats, FGS_WORK_LARGE_TICKET, count)) return;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
         if (!tb_sort_tile<512, 16, false>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
