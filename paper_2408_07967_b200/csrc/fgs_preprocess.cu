@@ -594,7 +594,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
              const __grid_constant__ CamDev cam, float tau32, float frustum_thresh,
              int sh_degree, int band0, int band1, FrameDev f)
 {
-    __shared__ uint32_t s_red[8];
+    __shared__ uint32_t s_red[8], s_red1[8], s_red2[8];
     __shared__ uint32_t s_bin[4], s_scan[8];
     // SH staging: plane j of thread t at s_sh[j * 256 + t] (48 KB, dynamic).  A thread's 12
     // cp.async gathers are issued as soon as its Gaussian passes the frustum test and land
@@ -809,16 +809,21 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     }
     if (lane == 0) {
         s_red[threadIdx.x >> 5] = v0;
-        if (v1 & 0xffffu) atomicAdd(&f.stats->gaussians_retained, v1 & 0xffffu);
-        if (v1 >> 16) atomicAdd(&f.stats->gaussians_degenerate, v1 >> 16);
-        if (v2) atomicAdd((unsigned long long *)&f.stats->candidate_tiles_lo, (unsigned long long)v2);
+        s_red1[threadIdx.x >> 5] = v1;
+        s_red2[threadIdx.x >> 5] = v2;
     }
     __syncthreads();                      // also: every warp's walk is done, the table is final
     if (threadIdx.x == 0) {
-        uint32_t t = 0;
+        // one atomic per CTA and counter: every CTA of the grid hits the same three words,
+        // and L2 serialises atomics on one address
+        uint32_t t = 0, t1 = 0;
+        unsigned long long t2 = 0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) t += s_red[i];
+        for (int i = 0; i < 8; ++i) { t += s_red[i]; t1 += s_red1[i]; t2 += s_red2[i]; }
         f.blocksums[blockIdx.x] = t;
+        if (t1 & 0xffffu) atomicAdd(&f.stats->gaussians_retained, t1 & 0xffffu);
+        if (t1 >> 16) atomicAdd(&f.stats->gaussians_degenerate, t1 >> 16);
+        if (t2) atomicAdd((unsigned long long *)&f.stats->candidate_tiles_lo, t2);
     }
     if (!BUCKET) return;
 
