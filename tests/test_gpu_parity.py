@@ -676,3 +676,75 @@ def test_stages_can_be_repeated_on_one_frame():
                                 None, None, base, lay, st))
     torch.cuda.synchronize()
     assert np.array_equal(ws.rgb.cpu().numpy(), want.image)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE.json's full sizes
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n,w,h", [(1_000_000, 1920, 1080),      # configs[1]
+                                   (3_000_000, 3840, 2160)])     # configs[2]
+def test_full_size_configs_against_the_oracle(n, w, h):
+    """C2 and C3 in full (the oracle finishes them in seconds): sorted
+    (key, value) list and range table bit-exact, counters equal, default frame inside
+    the pixel tolerance, exact-mode frame and contrib flags bit-identical."""
+    act = fgs.activate(fgs.gen_synthetic("mixed", n, 1, density_scale=True))
+    cam = fgs.orbit_cameras(1, 24.0, w, h)[0]
+    pipe = fgs.Pipeline(act)
+    ob = orc.preprocess_and_bin(act, cam)
+    ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, act.count)
+    ostarts = orc.tile_range_table(ok, ob.grid_w, ob.grid_h)
+    keys, vals, starts = fgs.sorted_pairs(pipe, cam)
+    assert np.array_equal(keys, ok) and np.array_equal(vals, ov)
+    assert np.array_equal(starts, ostarts)
+    del keys, vals, ok, ov, ob
+    oimg, ost = orc.render(act, cam)
+    fb, st = pipe.render(cam)
+    assert (st.gaussians_retained, st.pairs_emitted, st.tiles_nonempty) == \
+        (ost["gaussians_retained"], ost["pairs_emitted"], ost["tiles_nonempty"])
+    assert fgs.max_abs_diff(fb.image, oimg) <= PIX_TOL and _psnr_ok(fb.image, oimg)
+    fbx, stx = pipe.render(cam, exact=True)
+    assert np.array_equal(fbx.image.view(np.uint32), oimg.view(np.uint32))
+    assert stx.pairs_contributing == ost["pairs_contributing"]
+
+
+def test_north_star_size_properties():
+    """10M Gaussians at 3840x2160 (the north-star frame) through size-independent
+    properties: both sort modes give the same sorted list and bit-identical frames,
+    the sorted list is non-decreasing in (key, value) and consistent with the range
+    table, the pair count equals the sum of the per-Gaussian counts, the union of
+    four row bands is bit-identical to the whole frame, and the default frame stays
+    within the pixel tolerance of the exact-mode one (itself bit-identical to the
+    reference at every size the oracle is run on)."""
+    n, w, h = 10_000_000, 3840, 2160
+    act = fgs.activate(fgs.gen_synthetic("mixed", n, 1, density_scale=True))
+    cam = fgs.orbit_cameras(1, 24.0, w, h)[0]
+    pipe = fgs.Pipeline(act)
+    keys, vals, starts = fgs.sorted_pairs(pipe, cam)
+    b = fgs.preprocess_and_bin(pipe, cam)
+    assert keys.size == int(b.pair_counts.sum()) == starts[-1]
+    dk = np.diff(keys.view(np.int64))
+    assert np.all(dk >= 0) and np.all(np.diff(vals.astype(np.int64))[dk == 0] > 0)
+    tiles = (keys >> np.uint64(32)).astype(np.int64)
+    assert np.array_equal(starts, np.searchsorted(tiles, np.arange(starts.size)))
+    assert hashlib.sha256(np.sort(b.keys).tobytes()).digest() == \
+        hashlib.sha256(np.sort(keys).tobytes()).digest()
+    del b, dk, tiles
+    full, st = pipe.render(cam)
+    fx, stx = pipe.render(cam, exact=True)
+    assert st.pairs_emitted == keys.size
+    assert fgs.max_abs_diff(full.image, fx.image) <= 1e-4
+    gh = -(-h // 16)
+    out = np.zeros_like(full.image)
+    edges = [0, gh // 4, gh // 2, 3 * gh // 4, gh]
+    total = 0
+    for b0, b1 in zip(edges[:-1], edges[1:]):
+        fb, s = pipe.render(cam, band=(b0, b1 - 1))
+        out[b0 * 16:min(b1 * 16, h)] = fb.image[b0 * 16:min(b1 * 16, h)]
+        total += s.pairs_emitted
+    assert total == st.pairs_emitted and np.array_equal(out, full.image)
+    del pipe
+    pipe1 = fgs.Pipeline(act, sort_mode="onesweep")
+    k1, v1, s1 = fgs.sorted_pairs(pipe1, cam)
+    assert np.array_equal(k1, keys) and np.array_equal(v1, vals) and np.array_equal(s1, starts)
+    f1, _ = pipe1.render(cam)
+    assert np.array_equal(f1.image, full.image)
