@@ -1223,8 +1223,19 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const bool live = g < P;
     const uint32_t cnt = live ? f.counts[g] : 0u;
-    if (__syncthreads_or(cnt != 0u) == 0) return;        // uniform per block
     const uint4 info = f.ctainfo[blockIdx.x];            // (list base, entries, staged records)
+    // The Gaussian's own inputs are independent of the table: they go out with the first
+    // round trip's successors (table list, bucket starts) instead of after the barriers.
+    ushort4 r = make_ushort4(0, 0, 0, 0);
+    uint64_t pm = 0;
+    uint32_t bits = 0, og = 0;
+    if (cnt) {
+        r = f.rects[g];
+        if (STRAT == FGS_PRECISE) pm = f.passmask[g];
+        bits = __float_as_uint(f.depth[g]);
+        og = orig[g];
+    }
+    if (__syncthreads_or(cnt != 0u) == 0) return;        // uniform per block
     for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) S.tab.key[i] = FGS_HT_EMPTY;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < info.y; i += FGS_PRE_THREADS) {
@@ -1243,16 +1254,14 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
     job.tx0 = job.ty0 = 0;
     job.nx = 1;
     job.mask = 0;
-    uint32_t bits = 0;
     if (cnt) {
-        const ushort4 r = f.rects[g];
         const int by0 = (int)r.y > band0 ? (int)r.y : band0;
         const int by1 = (int)r.w < band1 ? (int)r.w : band1;
         job.tx0 = r.x; job.ty0 = by0; job.nx = (int)r.z - (int)r.x + 1;
         job.cand = (uint32_t)job.nx * (uint32_t)(by1 - by0 + 1);
         if (STRAT == FGS_PRECISE) {
             if (job.cand <= FGS_MASK_CAND) {
-                job.mask = f.passmask[g];                 // K1's verdicts, no test needed
+                job.mask = pm;                            // K1's verdicts, no test needed
             } else {
                 const float4 *row = (const float4 *)(f.splat + (size_t)g * 12);
                 const float4 r0 = row[0], r1 = row[1], r2 = row[2];
@@ -1265,14 +1274,13 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
                 job.cx = r0.x; job.cy = r0.y; job.a = r0.z; job.b = r0.w; job.c = r1.x;
             }
         }
-        bits = __float_as_uint(f.depth[g]);
     }
     const BinCtx bc{&S.tab, f.tilecount, S.gbase, S.wcoff, S.wcrec, S.wcdst, f.starts};
     // records carry the caller's Gaussian index: the reference's pair value and tie-break
     // (measured: letting each lane walk the set bits of its own mask instead -- no owner
     // search, no shuffles -- is 13 % slower: the divergence costs more than the walk)
     warp_walk_tiles<STRAT == FGS_PRECISE, WALK_PLACE>(job, width, height, grid_w, 0, bits,
-                                                      cnt ? orig[g] : 0u, f.keys[0], nullptr, &bc);
+                                                      og, f.keys[0], nullptr, &bc);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < info.z; i += FGS_PRE_THREADS) f.keys[0][S.wcdst[i]] = S.wcrec[i];
 }
