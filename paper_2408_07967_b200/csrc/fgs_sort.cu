@@ -482,10 +482,10 @@ constexpr int TB_MAXBIN = 64;
 
 // STAGE: keep a copy of the input records in shared memory (steps 2 and 4 read it);
 // without it they re-read the bucket through L1/L2 and the capacity doubles.
-template <int NT, int EMAX, bool STAGE = true>
+template <int NT, int EMAX, bool STAGE = true, int NBDIV = 4>
 struct BucketSmem {
     static constexpr int CAP = NT * EMAX;
-    static constexpr int NB = CAP / 4;
+    static constexpr int NB = CAP / NBDIV;                    // depth bins: NBDIV records per bin when full
     uint64_t a[STAGE ? CAP : 1];
     uint64_t b[CAP];
     uint32_t bin[NB + 1];
@@ -495,14 +495,14 @@ struct BucketSmem {
 // Sorts the n <= CAP records at g; the result goes to vals_out / keys_out [start, start+n).
 // Returns false (nothing written) when the records have to go to the radix fallback.
 // Every thread of the CTA calls it with the same arguments.
-template <int NT, int EMAX, bool STAGE = true>
-__device__ __forceinline__ bool tb_sort_range(BucketSmem<NT, EMAX, STAGE> &S, const uint64_t *g,
+template <int NT, int EMAX, bool STAGE = true, int NBDIV = 4>
+__device__ __forceinline__ bool tb_sort_range(BucketSmem<NT, EMAX, STAGE, NBDIV> &S, const uint64_t *g,
                                               int n, int start, uint64_t tile_hi,
                                               uint32_t *__restrict__ vals_out,
                                               uint64_t *__restrict__ keys_out, int write_keys)
 {
     // (g is not __restrict__: a split bucket's chunks were written by this very CTA)
-    constexpr int NB = BucketSmem<NT, EMAX, STAGE>::NB;
+    constexpr int NB = BucketSmem<NT, EMAX, STAGE, NBDIV>::NB;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
 
     // 1. stage the records, depth range of the tile
@@ -595,15 +595,15 @@ __device__ __forceinline__ bool tb_sort_range(BucketSmem<NT, EMAX, STAGE> &S, co
     return true;
 }
 
-template <int NT, int EMAX, bool STAGE = true>
-__device__ __forceinline__ bool tb_sort_tile(BucketSmem<NT, EMAX, STAGE> &S, int tile,
+template <int NT, int EMAX, bool STAGE = true, int NBDIV = 4>
+__device__ __forceinline__ bool tb_sort_tile(BucketSmem<NT, EMAX, STAGE, NBDIV> &S, int tile,
                                              const uint64_t *__restrict__ rec,
                                              uint32_t *__restrict__ vals_out,
                                              uint64_t *__restrict__ keys_out,
                                              const int32_t *__restrict__ starts, int write_keys)
 {
     const int start = starts[tile], n = starts[tile + 1] - start;
-    return tb_sort_range<NT, EMAX, STAGE>(S, rec + start, n, start, (uint64_t)(uint32_t)tile << 32,
+    return tb_sort_range<NT, EMAX, STAGE, NBDIV>(S, rec + start, n, start, (uint64_t)(uint32_t)tile << 32,
                                           vals_out, keys_out, write_keys);
 }
 
@@ -752,6 +752,12 @@ struct TileTickets {
 //   hard    n <= 4096   small / medium tiles the bucket-rank sort gave up on: radix sort
 //   dense   n >  8192   (and large tiles that gave up) one counting pass on the top varying
 //                       depth bits, then each chunk of <= 4096 by bucket-rank (radix fallback)
+#ifndef FGS_MED_NBDIV
+#define FGS_MED_NBDIV 2           // medium class: 2048 depth bins (rank loops half as long; 3 x 74 KB per SM)
+#endif
+#ifndef FGS_SMALL_NBDIV
+#define FGS_SMALL_NBDIV 2         // small class: 512 / 1024 bins (37 KB, still 6 CTAs per SM)
+#endif
 __global__ void __launch_bounds__(256, 6)
 k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
             uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
@@ -760,15 +766,15 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
     // one buffer, two instantiations: up to 1024 records with 4 per thread, up to 2048 with 8
     // (35 KB, still 6 CTAs per SM; the grid's dynamic CTA dispatch balances these tiles
     // better than the medium class's persistent CTAs, which keep 69 KB each)
-    __shared__ __align__(16) unsigned char raw[sizeof(BucketSmem<256, 8>)];
+    __shared__ __align__(16) unsigned char raw[sizeof(BucketSmem<256, 8, true, FGS_SMALL_NBDIV>)];
     if (stats->overflow) return;
     const int tile = blockIdx.x;
     const int n = starts[tile + 1] - starts[tile];
     if (n <= 0 || n > FGS_SMALL_TILE) return;
     const bool ok = n <= BucketSmem<256, 4>::CAP
-        ? tb_sort_tile<256, 4>(*reinterpret_cast<BucketSmem<256, 4> *>(raw), tile, rec, vals_out,
+        ? tb_sort_tile<256, 4, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 4, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
                                keys_out, starts, write_keys)
-        : tb_sort_tile<256, 8>(*reinterpret_cast<BucketSmem<256, 8> *>(raw), tile, rec, vals_out,
+        : tb_sort_tile<256, 8, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 8, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
                                keys_out, starts, write_keys);
     if (!ok &&
         threadIdx.x == 0)
@@ -782,6 +788,12 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
 #ifndef FGS_MED_MINB
 #define FGS_MED_MINB 3
 #endif
+#ifndef FGS_MED_STAGE
+#define FGS_MED_STAGE true       // records staged in shared memory (false: re-read from L2)
+#endif
+#ifndef FGS_LARGE_MINB
+#define FGS_LARGE_MINB 3       // 40 registers, 3 x 73 KB of shared memory per SM (2: 302 us at 10M@4K, 3: 256)
+#endif
 #define FGS_MED_EMAX (4096 / FGS_MED_NT)
 __global__ void __launch_bounds__(FGS_MED_NT, FGS_MED_MINB)
 k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
@@ -790,7 +802,7 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
                    int write_keys, fgs_stats *__restrict__ stats)
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
-    using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX>;
+    using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>;
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
     // first of the size classes: waits for the placement kernel, then lets the next class
     // (disjoint tiles, launched without a wait of its own) start beside this one
@@ -803,7 +815,7 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     if (!tk.open(stats, FGS_WORK_MEDIUM_TICKET, count)) return;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
-        if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+        if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
             threadIdx.x == 0)
             hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
@@ -811,7 +823,7 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     tk.close();
 }
 
-__global__ void __launch_bounds__(512, 2)
+__global__ void __launch_bounds__(512, FGS_LARGE_MINB)
 k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
                   uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
                   const uint32_t *__restrict__ list, uint32_t *__restrict__ dense_list,
@@ -870,7 +882,7 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
 int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st)
 {
     if (tiles <= 0) return FGS_OK;
-    using MediumSmem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX>;
+    using MediumSmem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>;
     using LargeSmem = BucketSmem<512, 16, false>;
     static_assert(LargeSmem::CAP == FGS_LARGE_TILE, "large class = large capacity");
     using TailRadix = TileSortSmem<256, 16>;
@@ -886,7 +898,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
             if (e == cudaSuccess && smem)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             // largest shared-memory carve-out, or the occupancy the launch bounds assume
-            // (6 x 17 KB, 3 x 69 KB, 2 x 73 KB, 2 x 112 KB per SM) is not reached
+            // (6 x 17 KB, 3 x 69 KB, 3 x 73 KB, 2 x 112 KB per SM) is not reached
             if (e == cudaSuccess)
                 e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
                                          cudaSharedmemCarveoutMaxShared);
@@ -904,8 +916,8 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     // lists in the spare words of the cursor slots: +1 dense, +2 medium, +3 hard
     uint32_t *dense_list = f.cursor + 1, *medium_list = f.cursor + 2, *hard_list = f.cursor + 3;
     uint32_t *large_list = f.cursor + 4;
-    const unsigned mgrid = (unsigned)(tiles < 3 * sms ? tiles : 3 * sms);
-    const unsigned dgrid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);
+    const unsigned mgrid = (unsigned)(tiles < FGS_MED_MINB * sms ? tiles : FGS_MED_MINB * sms);
+    const unsigned dgrid = (unsigned)(tiles < FGS_LARGE_MINB * sms ? tiles : FGS_LARGE_MINB * sms);
     // The small / medium / large classes sort disjoint tiles, so they may run side by side:
     // the persistent kernels go first (all their CTAs are resident at once and trigger
     // `griddepcontrol.launch_dependents` on entry), the next class is launched with
