@@ -791,6 +791,9 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
 #ifndef FGS_MED_STAGE
 #define FGS_MED_STAGE true       // records staged in shared memory (false: re-read from L2)
 #endif
+#ifndef FGS_LARGE_NT
+#define FGS_LARGE_NT 512
+#endif
 #ifndef FGS_LARGE_MINB
 #define FGS_LARGE_MINB 3       // 40 registers, 3 x 73 KB of shared memory per SM (2: 302 us at 10M@4K, 3: 256)
 #endif
@@ -823,14 +826,14 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     tk.close();
 }
 
-__global__ void __launch_bounds__(512, FGS_LARGE_MINB)
+__global__ void __launch_bounds__(FGS_LARGE_NT, FGS_LARGE_MINB)
 k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
                   uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
                   const uint32_t *__restrict__ list, uint32_t *__restrict__ dense_list,
                   int write_keys, fgs_stats *__restrict__ stats)
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
-    using Smem = BucketSmem<512, 16, false>;
+    using Smem = BucketSmem<FGS_LARGE_NT, 8192 / FGS_LARGE_NT, false>;
     Smem &S = *reinterpret_cast<Smem *>(ts_raw);
     fgs_pdl_trigger();      // no wait: released only after the medium class's wait returned
     if (stats->overflow) return;
@@ -840,7 +843,7 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     if (!tk.open(stats, FGS_WORK_LARGE_TICKET, count)) return;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
-        if (!tb_sort_tile<512, 16, false>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+        if (!tb_sort_tile<FGS_LARGE_NT, 8192 / FGS_LARGE_NT, false>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
             threadIdx.x == 0)      // clustered depths: let the splitting kernel take it
             dense_list[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
@@ -883,7 +886,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
 {
     if (tiles <= 0) return FGS_OK;
     using MediumSmem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>;
-    using LargeSmem = BucketSmem<512, 16, false>;
+    using LargeSmem = BucketSmem<FGS_LARGE_NT, 8192 / FGS_LARGE_NT, false>;
     static_assert(LargeSmem::CAP == FGS_LARGE_TILE, "large class = large capacity");
     using TailRadix = TileSortSmem<256, 16>;
     constexpr size_t tail_bytes = ((sizeof(TailRadix) + 15) & ~size_t(15)) + sizeof(BucketSmem<256, 16>);
@@ -938,7 +941,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     }
     {
         cfg.gridDim = dim3(dgrid);
-        cfg.blockDim = dim3(512);
+        cfg.blockDim = dim3(FGS_LARGE_NT);
         cfg.dynamicSmemBytes = sizeof(LargeSmem);
         cfg.numAttrs = overlap ? 1 : 0;
         const cudaError_t e = cudaLaunchKernelEx(&cfg, k_tile_sort_large, (const uint64_t *)f.keys[0],
