@@ -169,6 +169,20 @@ int32_t fgs_profile_end(void);
 /* ---- per-scene (model_io.py:78-118 ActivatedScene; untimed in the reference,
  *      pipeline.py:1-5) ------------------------------------------------------ */
 
+/* model_io.py:136-199 load_ply / _scene_from_payload, the payload split on the device
+ * (scene ingest): `vertex_payload` is the PLY body already in device
+ * memory -- `gaussians` records of 62 little-endian float32 (x y z, nx ny nz, f_dc_0..2,
+ * f_rest_0..44 channel-major, opacity, scale_0..2, rot_0..3; VERTEX_STRIDE = 248 bytes,
+ * model_io.py:42-51).  Writes the reference Scene's arrays (model_io.py:57-76): means (P,3),
+ * sh (P,16,3) coefficient-major with RGB innermost, logit opacities (P,), log scales (P,3),
+ * rotations (P,4) as stored; normals are parsed and dropped.  Values are copied bit for bit.
+ * Header parsing and its PlyParseError / PlySchemaError / PlyLengthError stay on the host
+ * (paper_2408_07967_b200/scene_io.py).  Outputs feed fgs_scene_activate and fgs_scene_pack;
+ * rotations_out must be 16-byte aligned for fgs_scene_activate. */
+int fgs_scene_unpack_ply(const float *vertex_payload, int64_t gaussians, float *means_out,
+                         float *sh_out, float *logit_opacities_out, float *log_scales_out,
+                         float *rotations_out, void *stream);
+
 /* model_io.py:93-118 activate, on the device: sign-split
  * sigmoid of the opacity logits, exp of the log-scales, quaternion normalisation
  * with zero-norm rows mapped to the identity.  Rotations are bit-identical to the

@@ -16,9 +16,15 @@ from . import service
 from .scene import (ActivatedScene, Camera, CameraValidationError, Scene, activate,
                     gen_synthetic, look_at_camera, make_camera, orbit_cameras)
 
+from .scene_io import (CameraSchemaError, DeviceScene, PlyLengthError, PlyParseError,
+                       PlySchemaError, load_cameras, load_ply, load_ply_device, save_cameras,
+                       save_ply)
+
 __version__ = "0.1.0"
 
 __all__ = [
+    "CameraSchemaError", "DeviceScene", "PlyLengthError", "PlyParseError", "PlySchemaError",
+    "load_cameras", "load_ply", "load_ply_device", "save_cameras", "save_ply",
     "ActivatedScene", "BinOutput", "Camera", "CameraValidationError", "CompareReport",
     "Framebuffer", "REPORT_SCHEMA_VERSION", "bench_frames", "compare_modes",
     "FrameStats", "Pipeline", "STRATEGIES", "Scene", "TAU_DEFAULT", "TILE_SIZE",

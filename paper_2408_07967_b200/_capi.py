@@ -27,7 +27,7 @@ SORT_TILE = 4096
 # every symbol include/flashgs_b200.h declares (checked by the CPU test-suite)
 SYMBOLS = (
     "fgs_abi_version", "fgs_error_string", "fgs_last_cuda_error", "fgs_scene_bytes",
-    "fgs_scene_order_scratch_bytes", "fgs_scene_order", "fgs_scene_pack", "fgs_scene_activate", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_layout_set_sort_mode",
+    "fgs_scene_order_scratch_bytes", "fgs_scene_order", "fgs_scene_pack", "fgs_scene_activate", "fgs_scene_unpack_ply", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_layout_set_sort_mode",
     "fgs_workspace_init",
     "fgs_preprocess", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
     "fgs_render", "fgs_sort_pairs_scratch_bytes", "fgs_sort_pairs", "fgs_tile_ranges",
@@ -100,6 +100,7 @@ def _declare(L):
         "fgs_last_cuda_error": (C.c_char_p, []),
         "fgs_scene_bytes": (C.c_size_t, [i64]),
         "fgs_scene_activate": (C.c_int, [vp, vp, vp, i64, vp, vp, vp, vp]),
+        "fgs_scene_unpack_ply": (C.c_int, [vp, i64, vp, vp, vp, vp, vp, vp]),
         "fgs_scene_order_scratch_bytes": (C.c_size_t, [i64]),
         "fgs_scene_order": (C.c_int, [vp, i64, vp, vp, C.c_size_t, vp]),
         "fgs_scene_pack": (C.c_int, [vp, vp, vp, vp, vp, vp, i64, vp, vp]),

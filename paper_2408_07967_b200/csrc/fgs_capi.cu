@@ -129,6 +129,19 @@ int fgs_scene_order(const float *means, int64_t P, uint32_t *order_out, void *sc
     return fgs_sort_pairs(codes, idx, P, 31, 0, codes_out, order_out, b, sort_bytes, 1u, stream);
 }
 
+int fgs_scene_unpack_ply(const float *vertex_payload, int64_t P, float *means_out, float *sh_out,
+                         float *logit_opacities_out, float *log_scales_out, float *rotations_out,
+                         void *stream)
+{
+    if (P < 0) return FGS_E_ARG;
+    if (P > 0x7fffff00ll) return FGS_E_SIZE;
+    if (P && (!vertex_payload || !means_out || !sh_out || !logit_opacities_out || !log_scales_out ||
+              !rotations_out))
+        return FGS_E_ARG;
+    return fgs_launch_unpack_ply(vertex_payload, P, means_out, sh_out, logit_opacities_out,
+                                 log_scales_out, rotations_out, (cudaStream_t)stream);
+}
+
 int fgs_scene_activate(const float *logit_opacities, const float *log_scales, const float *rotations,
                        int64_t P, float *opacities_out, float *scales_out, float *rotations_out,
                        void *stream)

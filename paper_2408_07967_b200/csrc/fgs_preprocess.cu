@@ -236,6 +236,56 @@ int fgs_launch_activate(const float *logit, const float *log_scales, const float
     return FGS_OK;
 }
 
+// model_io.py:167-199 (load_ply's payload split, _scene_from_payload) on the device: the
+// PLY body is an array of 62-float vertex records (x y z, nx ny nz, f_dc_0..2, f_rest_0..44
+// channel-major, opacity, scale_0..2, rot_0..3).  A CTA stages 128 records in shared memory
+// with coalesced loads and writes the reference's arrays -- means (P,3), sh (P,16,3) with RGB
+// innermost, logit opacities (P,), log scales (P,3), rotations (P,4) -- with coalesced
+// stores.  Pure data movement (values bit-identical to the host loader's); normals are
+// parsed and dropped as in the reference.  HBM-bound: 248 B read + 236 B written per vertex.
+#define FGS_PLY_FLOATS 62
+#define FGS_PLY_CHUNK  128
+__global__ void __launch_bounds__(256)
+k_unpack_ply(const float *__restrict__ payload, int64_t P, float *__restrict__ means,
+             float *__restrict__ sh, float *__restrict__ logit, float *__restrict__ logs,
+             float *__restrict__ rots)
+{
+    __shared__ float s[FGS_PLY_CHUNK * FGS_PLY_FLOATS];
+    const int64_t v0 = (int64_t)blockIdx.x * FGS_PLY_CHUNK;
+    const int nv = (int)(P - v0 < FGS_PLY_CHUNK ? P - v0 : FGS_PLY_CHUNK);
+    const float *src = payload + v0 * FGS_PLY_FLOATS;
+    for (int i = threadIdx.x; i < nv * FGS_PLY_FLOATS; i += 256) s[i] = src[i];
+    __syncthreads();
+    // record stride 62 is even: lanes reading consecutive vertices hit 2-way bank conflicts
+    // at worst, which a bandwidth-bound copy does not notice
+    for (int i = threadIdx.x; i < nv * 3; i += 256) {
+        const int v = i / 3, c = i - v * 3;
+        means[v0 * 3 + i] = s[v * FGS_PLY_FLOATS + c];
+        logs[v0 * 3 + i] = s[v * FGS_PLY_FLOATS + 55 + c];
+    }
+    for (int i = threadIdx.x; i < nv; i += 256) logit[v0 + i] = s[i * FGS_PLY_FLOATS + 54];
+    for (int i = threadIdx.x; i < nv * 4; i += 256) {
+        const int v = i >> 2, c = i & 3;
+        rots[v0 * 4 + i] = s[v * FGS_PLY_FLOATS + 58 + c];
+    }
+    for (int i = threadIdx.x; i < nv * 48; i += 256) {
+        const int v = i / 48, r = i - v * 48, coef = r / 3, ch = r - coef * 3;
+        // coefficient 0 = f_dc_ch; coefficient k >= 1 = f_rest_[ch * 15 + k - 1]
+        const int off = coef == 0 ? 6 + ch : 9 + ch * 15 + coef - 1;
+        sh[v0 * 48 + i] = s[v * FGS_PLY_FLOATS + off];
+    }
+}
+
+int fgs_launch_unpack_ply(const float *payload, int64_t P, float *means, float *sh, float *logit,
+                          float *logs, float *rots, cudaStream_t st)
+{
+    if (P == 0) return FGS_OK;
+    k_unpack_ply<<<(unsigned)((P + FGS_PLY_CHUNK - 1) / FGS_PLY_CHUNK), 256, 0, st>>>(
+        payload, P, means, sh, logit, logs, rots);
+    FGS_CHECK_LAUNCH();
+    return FGS_OK;
+}
+
 // extent.py:19-30
 __global__ void __launch_bounds__(256)
 k_power_cutoffs(const float4 *__restrict__ g0, int64_t P, double tau, float tau32,

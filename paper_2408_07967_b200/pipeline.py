@@ -221,9 +221,13 @@ class Pipeline:
         # instead of on the host.  Opacities / scales may then differ from the reference's
         # NumPy activation by 1 ulp (see the header), so frames agree within the pixel
         # tolerance but pair lists are no longer guaranteed bit-identical to the reference.
-        raw = is_raw_scene(scene)
-        on_device = bool(device_activate) and raw
-        if raw:
+        from .scene_io import DeviceScene
+        resident = isinstance(scene, DeviceScene)     # arrays already in HBM (load_ply_device)
+        raw = is_raw_scene(scene) and not resident
+        on_device = (bool(device_activate) and raw) or resident
+        if resident:
+            act = None
+        elif raw:
             act = None if on_device else activate(scene)
         elif is_activated_scene(scene):
             act = scene
@@ -234,11 +238,14 @@ class Pipeline:
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None \
             else torch.device(device)
         src = scene if on_device else act
-        self.count = int(np.asarray(src.means).shape[0])
+        self.count = int(src.means.shape[0]) if resident else int(np.asarray(src.means).shape[0])
         L = _capi.lib()
         with torch.cuda.device(self.device):
-            f32 = lambda a, shape: torch.from_numpy(
-                np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(shape))).to(self.device)
+            if resident:
+                f32 = lambda a, shape: a.to(self.device, torch.float32).reshape(shape).contiguous()
+            else:
+                f32 = lambda a, shape: torch.from_numpy(
+                    np.ascontiguousarray(np.asarray(a, dtype=np.float32).reshape(shape))).to(self.device)
             P = self.count
             st = _stream_ptr(torch, self.device)
             means, sh = f32(src.means, (P, 3)), f32(src.sh, (P, 48))
@@ -251,13 +258,20 @@ class Pipeline:
                                                  P, opac.data_ptr(), scales.data_ptr(),
                                                  rots.data_ptr(), st))
                 from .scene import ActivatedScene
-                act = ActivatedScene(np.asarray(scene.means, dtype=np.float32), opac.cpu().numpy(),
-                                     scales.cpu().numpy(), rots.cpu().numpy(),
-                                     np.asarray(scene.sh, dtype=np.float32))
+                if resident:
+                    # the host copy of a device-ingested scene is made on first use only
+                    parts = (means, opac, scales, rots, sh)
+                    self._activated_lazy = lambda: ActivatedScene(
+                        parts[0].cpu().numpy(), parts[1].cpu().numpy(), parts[2].cpu().numpy(),
+                        parts[3].cpu().numpy(), parts[4].cpu().numpy().reshape(P, 16, 3))
+                else:
+                    act = ActivatedScene(np.asarray(scene.means, dtype=np.float32), opac.cpu().numpy(),
+                                         scales.cpu().numpy(), rots.cpu().numpy(),
+                                         np.asarray(scene.sh, dtype=np.float32))
             else:
                 opac = f32(act.opacities, (P,))
                 scales, rots = f32(act.scales, (P, 3)), f32(act.rotations, (P, 4))
-            self.activated = act
+            self._activated = act
             self.scene_bytes = int(L.fgs_scene_bytes(P))
             self.packed = torch.empty(max(self.scene_bytes, 16), dtype=torch.uint8, device=self.device)
             order = None
@@ -280,6 +294,22 @@ class Pipeline:
         self._free = {}
         self._lock = threading.Lock()
         self._last_pairs = 0
+
+    @property
+    def activated(self):
+        """The activated scene as host arrays (for a device-ingested scene: copied back
+        on first use)."""
+        if self._activated is None:
+            self._activated = self._activated_lazy()
+            self._activated_lazy = None
+        return self._activated
+
+    @classmethod
+    def from_ply(cls, path, **kw):
+        """Scene ingest on the device: ``load_ply_device`` +
+        on-device activation + packing; the host never re-lays the scene out."""
+        from .scene_io import load_ply_device
+        return cls(load_ply_device(path, kw.get("device")), **kw)
 
     # -- per-tau cutoff table (extent.py:19-30), cached -------------------------
     def _cutoffs(self, torch, tau):

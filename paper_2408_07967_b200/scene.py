@@ -14,7 +14,7 @@ reference's own dataclasses (duck-typed on field names), so this module is
 only needed when the reference package is not importable (e.g. on the GPU
 box, where ``/root/reference`` does not exist).
 
-PLY / JSON file I/O is out of scope.
+PLY / JSON file I/O lives in ``scene_io.py``.
 """
 
 from __future__ import annotations
