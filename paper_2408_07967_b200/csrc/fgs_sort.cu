@@ -921,6 +921,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     uint32_t *large_list = f.cursor + 4;
     const unsigned mgrid = (unsigned)(tiles < FGS_MED_MINB * sms ? tiles : FGS_MED_MINB * sms);
     const unsigned dgrid = (unsigned)(tiles < FGS_LARGE_MINB * sms ? tiles : FGS_LARGE_MINB * sms);
+    const unsigned tgrid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);   // tail: 2 CTAs/SM, static stride
     // The small / medium / large classes sort disjoint tiles, so they may run side by side:
     // the persistent kernels go first (all their CTAs are resident at once and trigger
     // `griddepcontrol.launch_dependents` on entry), the next class is launched with
@@ -960,7 +961,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         FGS_AFTER_LAUNCH(st);
     }
-    k_tile_sort_tail<<<dgrid, 256, tail_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
+    k_tile_sort_tail<<<tgrid, 256, tail_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
                                                      f.starts, dense_list, hard_list, write_keys,
                                                      f.stats);
     FGS_AFTER_LAUNCH(st);

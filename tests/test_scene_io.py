@@ -148,8 +148,12 @@ def test_device_ingest_is_bit_identical_to_the_host_loader(tmp_path, n):
 @pytest.mark.gpu
 def test_pipeline_from_ply_matches_device_activation_of_the_host_scene(tmp_path):
     """Pipeline.from_ply (header on the host, body split + activated + packed on the device)
-    renders the frame Pipeline(load_ply(...), device_activate=True) renders, bit for bit,
-    and stays within the pixel tolerance of the host-activated scene."""
+    renders the frame Pipeline(load_ply(...), device_activate=True) renders, bit for bit.
+    Against the HOST-activated scene the frame is not bit-comparable: the device's exp is
+    correctly rounded, NumPy's float32 SIMD exp is not, and a 1-ulp opacity difference can
+    flip one of the reference's hard skips (alpha < tau) for a pixel -- one contribution
+    of at most ~tau * colour.  So: PSNR >= 60 dB, no pixel off by more than one such
+    contribution, and almost all pixels within 1e-3."""
     scene = fgs.gen_synthetic("mixed", 20_000, 11)
     path = tmp_path / "s.ply"
     fgs.save_ply(scene, path)
@@ -162,7 +166,10 @@ def test_pipeline_from_ply_matches_device_activation_of_the_host_scene(tmp_path)
     for name in ("means", "opacities", "scales", "rotations", "sh"):
         assert np.array_equal(getattr(a.activated, name), getattr(b.activated, name)), name
     fh, _ = fgs.Pipeline(fgs.load_ply(path)).render(cam)
-    assert fgs.max_abs_diff(fa.image, fh.image) <= 1e-3
+    d = np.abs(fa.image - fh.image)
+    p = fgs.psnr(fa.image, fh.image)
+    assert (p == "identical" or p >= 60.0) and d.max() <= 5e-3
+    assert (d > 1e-3).any(axis=2).mean() <= 1e-4
     with pytest.raises(fgs.PlyLengthError):
         path.write_bytes(path.read_bytes()[:-8])
         fgs.load_ply_device(path)
