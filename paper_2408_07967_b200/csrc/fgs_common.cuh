@@ -203,6 +203,21 @@ int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *v
 int  fgs_launch_quantize(const float *rgb, int64_t count, uint8_t *out, cudaStream_t st);
 
 void fgs_set_cuda_error(cudaError_t e);
+
+// cudaFuncSetAttribute is per device: one flag per (call site, device), so a process that
+// renders on several devices (one Pipeline per device) sets the attributes on each of them.
+// Racing threads may both set them (idempotent).
+struct FgsOncePerDevice {
+    unsigned long long done = 0ull;
+    __host__ bool need(int *dev_out)
+    {
+        int d = 0;
+        cudaGetDevice(&d);
+        *dev_out = d & 63;
+        return !((__atomic_load_n(&done, __ATOMIC_ACQUIRE) >> (d & 63)) & 1ull);
+    }
+    __host__ void mark(int dev) { __atomic_fetch_or(&done, 1ull << dev, __ATOMIC_RELEASE); }
+};
 // Records the next caller-supplied profiling event on `st` (no-op unless
 // fgs_profile_begin armed this thread).  Called after every kernel launch.
 void fgs_prof_mark(cudaStream_t st);

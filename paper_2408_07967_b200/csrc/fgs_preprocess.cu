@@ -948,8 +948,9 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     const float tau32 = (float)tau, fth = (float)th;
     constexpr int kShBytes = FGS_SH_STAGED * FGS_PRE_THREADS * 16; // SH staging, 4 KB per plane
-    static bool attr_set = false;
-    if (!attr_set) {
+    static FgsOncePerDevice attr_once;
+    int attr_dev = 0;
+    if (attr_once.need(&attr_dev)) {
         cudaError_t ea = cudaSuccess;
 #define FGS_ATTR(S, B) if (ea == cudaSuccess) ea = cudaFuncSetAttribute(k_preprocess<S, B>, \
         cudaFuncAttributeMaxDynamicSharedMemorySize, kShBytes)
@@ -958,7 +959,7 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
         FGS_ATTR(FGS_BASELINE_CIRCLE_AABB, true); FGS_ATTR(FGS_BASELINE_CIRCLE_AABB, false);
 #undef FGS_ATTR
         if (ea != cudaSuccess) { fgs_set_cuda_error(ea); return FGS_E_CUDA; }
-        attr_set = true;
+        attr_once.mark(attr_dev);
     }
 #define FGS_K1(S, B) k_preprocess<S, B><<<blocks, FGS_PRE_THREADS, kShBytes, st>>>( \
         sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f)
@@ -1345,8 +1346,9 @@ int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strate
     if (P == 0) return FGS_OK;
     const unsigned blocks = (unsigned)((P + FGS_PRE_THREADS - 1) / FGS_PRE_THREADS);
     if (bucket) {
-        static bool attr_set = false;
-        if (!attr_set) {
+        static FgsOncePerDevice attr_once;
+        int attr_dev = 0;
+        if (attr_once.need(&attr_dev)) {
             cudaError_t e = cudaFuncSetAttribute(k_place<FGS_PRECISE>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)sizeof(PlaceSmem));
@@ -1355,7 +1357,7 @@ int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strate
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sizeof(PlaceSmem));
             if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
-            attr_set = true;
+            attr_once.mark(attr_dev);
         }
         if (strategy == FGS_PRECISE)
             FGS_CHAIN(k_place<FGS_PRECISE>, dim3(blocks), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,

@@ -893,9 +893,10 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     static_assert(BucketSmem<256, 8>::CAP == FGS_SMALL_TILE, "small class = small capacity");
     static_assert(MediumSmem::CAP == FGS_DENSE_TILE && TailRadix::CAP == FGS_DENSE_TILE,
                   "medium capacity = radix capacity = chunk size of split buckets");
-    static bool attr_set = false;
+    static FgsOncePerDevice attr_once;
+    int attr_dev = 0;
     static int sms = 148;
-    if (!attr_set) {
+    if (attr_once.need(&attr_dev)) {
         cudaError_t e = cudaSuccess;
         auto prep = [&](const void *fn, size_t smem) {
             if (e == cudaSuccess && smem)
@@ -914,7 +915,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        attr_set = true;
+        attr_once.mark(attr_dev);
     }
     // lists in the spare words of the cursor slots: +1 dense, +2 medium, +3 hard
     uint32_t *dense_list = f.cursor + 1, *medium_list = f.cursor + 2, *hard_list = f.cursor + 3;
@@ -995,15 +996,16 @@ int fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev,
 {
     if (n_max <= 0 || plan.npass == 0) return FGS_OK;
     if (plan.npass > FGS_SORT_MAXPASS) return FGS_E_ARG;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static FgsOncePerDevice attr_once;
+    int attr_dev = 0;
+    if (attr_once.need(&attr_dev)) {
         cudaError_t e = cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)sizeof(SortSmem));
         if (e == cudaSuccess)
             e = cudaFuncSetAttribute(k_sort_pass, cudaFuncAttributePreferredSharedMemoryCarveout,
                                      cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
-        attr_set = true;
+        attr_once.mark(attr_dev);
     }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
