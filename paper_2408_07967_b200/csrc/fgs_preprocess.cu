@@ -1280,9 +1280,9 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
     ushort4 r = make_ushort4(0, 0, 0, 0);
     uint64_t pm = 0;
     uint32_t bits = 0, og = 0;
-    if (cnt) {
-        r = f.rects[g];
-        if (STRAT == FGS_PRECISE) pm = f.passmask[g];
+    if (live) {                                          // not `if (cnt)`: that would chain them
+        r = f.rects[g];                                  // behind the count's round trip
+        if (STRAT == FGS_PRECISE) pm = f.passmask[g];    // (stale when cnt == 0, and unused)
         bits = __float_as_uint(f.depth[g]);
         og = orig[g];
     }
