@@ -395,7 +395,8 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
     __shared__ Blend2Smem S;
     fgs_pdl_wait();            // (the tail sort kernel before it is launched the plain way and
                                // waits for every size class)
-    if (stats != nullptr && stats->overflow) return;
+    const uint32_t over = stats != nullptr ? stats->overflow : 0u;   // consumed below, after the
+                                                                     // tile lookup is out too
     constexpr int B = FGS_B2_BATCH;
     const int tid = threadIdx.x;
     const int lane = tid & 31, wq = tid >> 5;
@@ -406,6 +407,7 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
     // (Persistent CTAs pulling tiles from a ticket counter were slower: 72 registers, and the
     // per-tile prologue no longer overlaps other CTAs' blending -- 197 us against 177 on C2.)
     const int tile = order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x;
+    if (over) return;                                    // uniform: grow and re-run
     const int ty = tile / grid_w, tx = tile - ty * grid_w;
     const int bx = tx * FGS_TILE + (wq & 1) * 8, by = ty * FGS_TILE + (wq >> 1) * 8;
     const int px = bx + (lane & 7), py0 = by + (lane >> 3), py1 = py0 + 4;

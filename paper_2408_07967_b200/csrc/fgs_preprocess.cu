@@ -1270,7 +1270,7 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
     PlaceSmem &S = *reinterpret_cast<PlaceSmem *>(place_raw);
     fgs_pdl_wait();
     fgs_pdl_trigger();
-    if (f.stats->overflow) return;                       // uniform: grow and re-run
+    const uint32_t over = f.stats->overflow;             // consumed after the loads below are out
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const bool live = g < P;
     const uint32_t cnt = live ? f.counts[g] : 0u;
@@ -1286,6 +1286,7 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
         bits = __float_as_uint(f.depth[g]);
         og = orig[g];
     }
+    if (over) return;                                    // uniform: grow and re-run
     if (__syncthreads_or(cnt != 0u) == 0) return;        // uniform per block
     for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) S.tab.key[i] = FGS_HT_EMPTY;
     __syncthreads();

@@ -767,9 +767,10 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
     // (35 KB, still 6 CTAs per SM; the grid's dynamic CTA dispatch balances these tiles
     // better than the medium class's persistent CTAs, which keep 69 KB each)
     __shared__ __align__(16) unsigned char raw[sizeof(BucketSmem<256, 8, true, FGS_SMALL_NBDIV>)];
-    if (stats->overflow) return;
+    const uint32_t over = stats->overflow;               // one round trip with the range lookup
     const int tile = blockIdx.x;
     const int n = starts[tile + 1] - starts[tile];
+    if (over) return;
     if (n <= 0 || n > FGS_SMALL_TILE) return;
     const bool ok = n <= BucketSmem<256, 4>::CAP
         ? tb_sort_tile<256, 4, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 4, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
