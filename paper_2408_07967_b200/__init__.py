@@ -12,7 +12,8 @@ from .pipeline import (BinOutput, Framebuffer, FrameStats, Pipeline, STRATEGIES,
                        power_cutoffs, preprocess_and_bin, psnr, render_frame,
                        run_frame, sort_pairs, sorted_pairs, tile_range_table)
 from .reports import REPORT_SCHEMA_VERSION, CompareReport, bench_frames, compare_modes
-from . import service
+from . import images, service
+from .images import read_ppm, write_png, write_ppm
 from .scene import (ActivatedScene, Camera, CameraValidationError, Scene, activate,
                     gen_synthetic, look_at_camera, make_camera, orbit_cameras)
 
@@ -30,5 +31,6 @@ __all__ = [
     "FrameStats", "Pipeline", "STRATEGIES", "Scene", "TAU_DEFAULT", "TILE_SIZE",
     "UnsortedPairsError", "activate", "gen_synthetic", "look_at_camera", "make_camera",
     "max_abs_diff", "orbit_cameras", "power_cutoffs", "preprocess_and_bin", "psnr",
+    "read_ppm", "write_png", "write_ppm", "images",
     "render_frame", "run_frame", "service", "sort_pairs", "sorted_pairs", "tile_range_table",
 ]

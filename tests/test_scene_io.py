@@ -173,3 +173,57 @@ def test_pipeline_from_ply_matches_device_activation_of_the_host_scene(tmp_path)
     with pytest.raises(fgs.PlyLengthError):
         path.write_bytes(path.read_bytes()[:-8])
         fgs.load_ply_device(path)
+
+
+# ---------------------------------------------------------------------------
+# frame export (reference images.py:12-55, tests/test_images.py)
+# ---------------------------------------------------------------------------
+def test_quantize_rounds_half_away_from_zero_and_clips():
+    img = np.array([[[0.0, 0.5 / 255.0, 1.0], [-0.2, 1.7, 254.5 / 255.0],
+                     [0.499 / 255.0, 127.5 / 255.0, 0.25]]], dtype=np.float32)
+    q = fgs.images.quantize(img)
+    want = np.floor(np.clip(img.astype(np.float64), 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+    assert q.dtype == np.uint8 and np.array_equal(q, want)
+    assert q[0, 0].tolist() == [0, 1, 255] and q[0, 1].tolist()[:2] == [0, 255]
+
+
+def test_ppm_round_trip(tmp_path):
+    rng = np.random.default_rng(3)
+    img = rng.random((37, 53, 3), dtype=np.float32)
+    path = tmp_path / "f.ppm"
+    fgs.write_ppm(img, path)
+    raw = path.read_bytes()
+    assert raw.startswith(b"P6\n53 37\n255\n") and len(raw) == len(b"P6\n53 37\n255\n") + 37 * 53 * 3
+    back = fgs.read_ppm(path)
+    assert np.array_equal(back, fgs.images.quantize(img))
+    path.write_bytes(b"P5\n1 1\n255\n\x00")
+    with pytest.raises(ValueError, match="not a P6"):
+        fgs.read_ppm(path)
+    path.write_bytes(b"P6\n1 1\n65535\n\x00\x00\x00")
+    with pytest.raises(ValueError, match="maxval"):
+        fgs.read_ppm(path)
+
+
+def test_png_round_trip(tmp_path):
+    Image = pytest.importorskip("PIL.Image")
+    img = np.random.default_rng(4).random((20, 31, 3), dtype=np.float32)
+    path = tmp_path / "f.png"
+    fgs.write_png(img, path)
+    assert np.array_equal(np.asarray(Image.open(path).convert("RGB")), fgs.images.quantize(img))
+
+
+@pytest.mark.gpu
+def test_device_frames_export_the_same_bytes(tmp_path):
+    """A frame left on the device is quantised there; the PPM equals the one written
+    from the host copy of the same frame."""
+    act = fgs.activate(fgs.gen_synthetic("mixed", 5000, 2))
+    cam = fgs.orbit_cameras(1, 16.0, 333, 210)[0]
+    pipe = fgs.Pipeline(act)
+    fb_dev, _ = pipe.render(cam, as_numpy=False)
+    fb_host, _ = pipe.render(cam)
+    assert fb_dev.image.is_cuda
+    p1, p2 = tmp_path / "d.ppm", tmp_path / "h.ppm"
+    fgs.write_ppm(fb_dev.image, p1)
+    fgs.write_ppm(fb_host.image, p2)
+    assert p1.read_bytes() == p2.read_bytes()
+    assert np.array_equal(fgs.read_ppm(p1), fgs.images.quantize(fb_host.image))
