@@ -414,7 +414,7 @@ enum { WALK_COUNT = 0, WALK_BIN = 1, WALK_EMIT = 2, WALK_PLACE = 3 };
 #define FGS_WC_CAP    3072          // records the CTA's write-combining buffer holds
 #endif
 #ifndef FGS_PLACE_MINBLOCKS
-#define FGS_PLACE_MINBLOCKS 1
+#define FGS_PLACE_MINBLOCKS 4
 #endif
 #define FGS_WC_NONE   0xffffu       // table entry whose range is written directly
 struct TileTable {
@@ -635,6 +635,9 @@ __device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(a), "l"(gmem) : "memory");
 }
 
+#ifndef FGS_PLACE_PF_DIST
+#define FGS_PLACE_PF_DIST 592    // K3: CTAs ahead for the L2 prefetch (4 per SM x 148; 0 = off)
+#endif
 // ---------------------------------------------------------------------------
 // K1: preprocess + count
 // ---------------------------------------------------------------------------
@@ -1287,6 +1290,25 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
         og = orig[g];
     }
     if (over) return;                                    // uniform: grow and re-run
+#if FGS_PLACE_PF_DIST
+    // L2 prefetch one wave ahead (the CTA that will take this one's place): its per-Gaussian
+    // inputs now, its table list at the end of this kernel (the header has arrived by then).
+    const int64_t gp = ((int64_t)blockIdx.x + FGS_PLACE_PF_DIST) * FGS_PRE_THREADS;
+    uint4 info_pf = make_uint4(0u, 0u, 0u, 0u);
+    if (gp < P) {
+        if (threadIdx.x == 0) info_pf = f.ctainfo[blockIdx.x + FGS_PLACE_PF_DIST];
+        const int t = threadIdx.x;                      // 56 lines of 128 B
+        const void *a = nullptr;
+        int64_t first = P;
+        if (t < 8) { a = f.counts + gp + t * 32; first = gp + t * 32; }
+        else if (t < 24) { a = f.rects + gp + (t - 8) * 16; first = gp + (t - 8) * 16; }
+        else if (t < 40) { a = f.passmask + gp + (t - 24) * 16; first = gp + (t - 24) * 16; }
+        else if (t < 48) { a = f.depth + gp + (t - 40) * 32; first = gp + (t - 40) * 32; }
+        else if (t < 56) { a = orig + gp + (t - 48) * 32; first = gp + (t - 48) * 32; }
+        if (first < P && !(STRAT != FGS_PRECISE && t >= 24 && t < 40))
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+#endif
     if (__syncthreads_or(cnt != 0u) == 0) return;        // uniform per block
     for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) S.tab.key[i] = FGS_HT_EMPTY;
     __syncthreads();
@@ -1335,6 +1357,14 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
                                                       og, f.keys[0], nullptr, &bc);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < info.z; i += FGS_PRE_THREADS) f.keys[0][S.wcdst[i]] = S.wcrec[i];
+#if FGS_PLACE_PF_DIST
+    if (threadIdx.x < 32 && gp < P) {
+        info_pf.x = __shfl_sync(FGS_FULL, info_pf.x, 0);
+        info_pf.y = __shfl_sync(FGS_FULL, info_pf.y, 0);
+        for (uint32_t l = threadIdx.x; l * 8u < info_pf.y; l += 32u)      // 8 entries per line
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(f.tablelist + info_pf.x + l * 8u));
+    }
+#endif
 }
 
 int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
