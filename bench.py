@@ -190,6 +190,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="views", choices=["views", "bands"])
+    ap.add_argument("--band-split", default="balanced", choices=["balanced", "equal"],
+                    help="--mode bands: bands of equal estimated work (default) or equal height")
     ap.add_argument("--exact", action="store_true", help="bit-exact blend mode")
     ap.add_argument("--sort-mode", default="tile-bucket", choices=["tile-bucket", "onesweep"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
@@ -236,6 +238,12 @@ def main():
 
     pipe = fgs.Pipeline(act, sort_mode=args.sort_mode,
                         spatial_order=False if args.no_spatial else None)
+    if args.mode == "bands" and world > 1 and args.band_split == "balanced":
+        # work-balanced bands: every rank derives the same edges from the same integer
+        # row histogram (no communication); the frame does not depend on the cut
+        rw = pipe.row_weights(cam)
+        bands = sharding.balanced_band_partition(rw, world, fixed_rows=0.3 * float(rw.mean()))
+        band = bands[rank]
     L = _capi.lib()
     hbm_peak, peak_src, sm_max = peaks()
 
@@ -499,7 +507,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak" if args.mode == "views" else "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "mode": args.mode, "strategy": "precise",
+            "config": {"workload": desc, "mode": args.mode, "band_split": (args.band_split if args.mode == "bands" else None), "strategy": "precise",
                        "tau": 1.0 / 255.0, "sh_degree": 3, "gaussians": P, "width": W, "height": H,
                        "pairs": M, "retained": R, "tiles": T_tiles, "sort_mode": args.sort_mode,
                        "sort_passes": npass,

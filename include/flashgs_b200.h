@@ -258,6 +258,16 @@ int fgs_preprocess(const void *packed_scene, const float *k_cut, int64_t gaussia
                    int32_t strategy, int32_t band_ty0, int32_t band_ty1,
                    void *workspace, const fgs_layout *layout_host, void *stream);
 
+/* Row-band load estimate for the multi-GPU row-band split (the reference
+ * has no counterpart -- its tiles are split over a thread pool, render.py:276-304): writes
+ * rows_out[ty] = number of Gaussians passing the frustum test (projection.py:39-47) whose
+ * projected centre (projection.py:158-171) lies in tile row ty, for ty in 0..ceil(height/16)-1
+ * (device array, zeroed by the call).  Integer counts, identical on every rank, so ranks
+ * derive the same work-balanced band edges (paper_2408_07967_b200.sharding) without
+ * communicating.  The rendered frame does not depend on the band edges. */
+int fgs_row_histogram(const void *packed_scene, int64_t gaussians, const fgs_camera *camera_host,
+                      double tau, uint32_t *rows_out, void *stream);
+
 /* binning.py:292 (np.cumsum) / 129-147 (shared cursor): exclusive scan of the
  * per-block pair counts; fixes M, the overflow flag, and resets sort counters. */
 int fgs_scan(void *workspace, const fgs_layout *layout_host, void *stream);

@@ -29,7 +29,7 @@ SYMBOLS = (
     "fgs_abi_version", "fgs_error_string", "fgs_last_cuda_error", "fgs_scene_bytes",
     "fgs_scene_order_scratch_bytes", "fgs_scene_order", "fgs_scene_pack", "fgs_scene_activate", "fgs_scene_unpack_ply", "fgs_power_cutoffs", "fgs_workspace_layout", "fgs_layout_set_sort_mode",
     "fgs_workspace_init",
-    "fgs_preprocess", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
+    "fgs_preprocess", "fgs_row_histogram", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
     "fgs_render", "fgs_sort_pairs_scratch_bytes", "fgs_sort_pairs", "fgs_tile_ranges",
     "fgs_blend_tiles", "fgs_profile_begin", "fgs_profile_end", "fgs_quantize_rgb8",
 )
@@ -109,6 +109,7 @@ def _declare(L):
         "fgs_layout_set_sort_mode": (C.c_int, [lay_p, i32]),
         "fgs_workspace_init": (C.c_int, [vp, lay_p, vp]),
         "fgs_preprocess": (C.c_int, [vp, vp, i64, cam_p, dbl, i32, i32, i32, i32, vp, lay_p, vp]),
+        "fgs_row_histogram": (C.c_int, [vp, i64, cam_p, dbl, vp, vp]),
         "fgs_scan": (C.c_int, [vp, lay_p, vp]),
         "fgs_emit": (C.c_int, [vp, cam_p, i32, i32, i32, vp, lay_p, vp]),
         "fgs_sort": (C.c_int, [vp, lay_p, u32, vp]),

@@ -267,6 +267,16 @@ int fgs_preprocess(const void *packed, const float *k_cut, int64_t P, const fgs_
                                  L->tiles, fgs_frame_view(ws, L), (cudaStream_t)stream);
 }
 
+int fgs_row_histogram(const void *packed, int64_t P, const fgs_camera *cam, double tau,
+                      uint32_t *rows_out, void *stream)
+{
+    if (!cam || !rows_out || P < 0 || !(tau > 0.0)) return FGS_E_ARG;
+    if (cam->width < FGS_TILE || cam->height < FGS_TILE) return FGS_E_ARG;
+    if (P && !packed) return FGS_E_ARG;
+    return fgs_launch_row_histogram(fgs_scene_view(packed, P), P, make_cam(cam), tau, rows_out,
+                                    (cudaStream_t)stream);
+}
+
 int fgs_scan(void *ws, const fgs_layout *L, void *stream)
 {
     if (!ws || !L) return FGS_E_ARG;

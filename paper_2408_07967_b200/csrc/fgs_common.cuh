@@ -165,6 +165,8 @@ int  fgs_launch_pack(const float *means, const float *opac, const float *scales,
                      void *packed, cudaStream_t st);
 int  fgs_launch_morton_keys(const float *means, int64_t P, float *bbox6, uint64_t *keys,
                             uint32_t *vals, cudaStream_t st);
+int  fgs_launch_row_histogram(const SceneDev &sc, int64_t P, const CamDev &cam, double tau,
+                              uint32_t *hist, cudaStream_t st);
 int  fgs_launch_unpack_ply(const float *payload, int64_t P, float *means, float *sh, float *logit,
                            float *logs, float *rots, cudaStream_t st);
 int  fgs_launch_activate(const float *logit, const float *log_scales, const float *rots, int64_t P,

@@ -286,6 +286,55 @@ int fgs_launch_unpack_ply(const float *payload, int64_t P, float *means, float *
     return FGS_OK;
 }
 
+// Row-band load estimate (multi-GPU row bands): how many in-frustum Gaussians
+// have their projected centre in each tile row.  Every rank of a band job runs it on the
+// same scene and camera and gets the same integers, so the ranks agree on work-balanced band
+// edges without talking to each other.  A proxy only (centres, not pairs) -- the frame does
+// not depend on where the bands are cut.  16 B read per Gaussian.
+#define FGS_ROWHIST_SMEM 4096
+__global__ void __launch_bounds__(256)
+k_row_histogram(const float4 *__restrict__ g0, int64_t P, const __grid_constant__ CamDev cam,
+                float frustum_thresh, uint32_t *__restrict__ hist)
+{
+    __shared__ uint32_t s_h[FGS_ROWHIST_SMEM];
+    const int gh = cam.grid_h;
+    const bool in_smem = gh <= FGS_ROWHIST_SMEM;
+    if (in_smem)
+        for (int i = threadIdx.x; i < gh; i += 256) s_h[i] = 0u;
+    __syncthreads();
+    for (int64_t g = (int64_t)blockIdx.x * 256 + threadIdx.x; g < P; g += (int64_t)gridDim.x * 256) {
+        const float4 m = g0[g];
+        const float t2 = fa(fa(fa(fm(cam.v[8], m.x), fm(cam.v[9], m.y)), fm(cam.v[10], m.z)), cam.v[11]);
+        if (!((t2 > FGS_Z_NEAR) && (m.w > frustum_thresh))) continue;
+        const float h1 = fa(fa(fa(fm(cam.p1[0], m.x), fm(cam.p1[1], m.y)), fm(cam.p1[2], m.z)), cam.p1[3]);
+        const float h3 = fa(fa(fa(fm(cam.p3[0], m.x), fm(cam.p3[1], m.y)), fm(cam.p3[2], m.z)), cam.p3[3]);
+        const float den = fabsf(h3) > 1e-7f ? h3 : 1e-7f;
+        const float py = fm(fs(fm(fa(fd(h1, den), 1.0f), cam.hf), 1.0f), 0.5f);
+        const float ty = floorf(fm(py, 0.0625f));
+        if (!(ty >= -1.0f && ty <= (float)gh)) continue;             // well outside the frame
+        const int row = (int)fminf(fmaxf(ty, 0.0f), (float)(gh - 1));
+        atomicAdd(in_smem ? &s_h[row] : &hist[row], 1u);
+    }
+    __syncthreads();
+    if (in_smem)
+        for (int i = threadIdx.x; i < gh; i += 256)
+            if (s_h[i]) atomicAdd(&hist[i], s_h[i]);
+}
+
+int fgs_launch_row_histogram(const SceneDev &sc, int64_t P, const CamDev &cam, double tau,
+                             uint32_t *hist, cudaStream_t st)
+{
+    cudaError_t e = cudaMemsetAsync(hist, 0, (size_t)cam.grid_h * sizeof(uint32_t), st);
+    if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+    if (P == 0) return FGS_OK;
+    const double th = tau > 1.0 / 255.0 ? tau : 1.0 / 255.0;       // projection.py:46
+    int64_t blocks = (P + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_row_histogram<<<(unsigned)blocks, 256, 0, st>>>(sc.g0, P, cam, (float)th, hist);
+    FGS_CHECK_LAUNCH();
+    return FGS_OK;
+}
+
 // extent.py:19-30
 __global__ void __launch_bounds__(256)
 k_power_cutoffs(const float4 *__restrict__ g0, int64_t P, double tau, float tau32,
@@ -641,7 +690,7 @@ __device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
 // ---------------------------------------------------------------------------
 // K1: preprocess + count
 // ---------------------------------------------------------------------------
-template <int STRAT, bool BUCKET>
+template <int STRAT, bool BUCKET, bool BANDED>
 __global__ void __launch_bounds__(FGS_PRE_THREADS, FGS_PRE_MINBLOCKS)
 k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
              const __grid_constant__ CamDev cam, float tau32, float frustum_thresh,
@@ -781,6 +830,11 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                     job.keff = keff;
                     job.tx0 = tx0; job.ty0 = by0; job.nx = tx1 - tx0 + 1;
                 }
+                // Row-band frames (multi-GPU): a Gaussian without candidate tiles in this
+                // rank's band emits no pair here, so nothing reads its colour or splat row --
+                // skip both (every rank walks all P Gaussians; this is most of them).  A
+                // template flag: the whole-frame kernel is the same code as without it.
+                if (!BANDED || by0 <= by1) {
                 // binning.py:230-233 view direction, render.py:52-86 colour
                 const float d0 = fs(x, cam.pos[0]), d1 = fs(y, cam.pos[1]), d2 = fs(z, cam.pos[2]);
                 float nrm = fsq(fa(fa(fm(d0, d0), fm(d1, d1)), fm(d2, d2)));
@@ -821,6 +875,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                 row[0] = make_float4(px, py, ca, cb);
                 row[1] = make_float4(cc, op, k, rgb[0]);
                 row[2] = make_float4(rgb[1], rgb[2], hx, hy);
+                }
             }
             asm volatile("cp.async.wait_group 0;" ::: "memory");       // culled after the frustum test
         }
@@ -955,17 +1010,21 @@ int fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, cons
     int attr_dev = 0;
     if (attr_once.need(&attr_dev)) {
         cudaError_t ea = cudaSuccess;
-#define FGS_ATTR(S, B) if (ea == cudaSuccess) ea = cudaFuncSetAttribute(k_preprocess<S, B>, \
+#define FGS_ATTR1(S, B, N) if (ea == cudaSuccess) ea = cudaFuncSetAttribute(k_preprocess<S, B, N>, \
         cudaFuncAttributeMaxDynamicSharedMemorySize, kShBytes)
+#define FGS_ATTR(S, B) FGS_ATTR1(S, B, false); FGS_ATTR1(S, B, true)
         FGS_ATTR(FGS_PRECISE, true); FGS_ATTR(FGS_PRECISE, false);
         FGS_ATTR(FGS_TIGHT_AABB, true); FGS_ATTR(FGS_TIGHT_AABB, false);
         FGS_ATTR(FGS_BASELINE_CIRCLE_AABB, true); FGS_ATTR(FGS_BASELINE_CIRCLE_AABB, false);
 #undef FGS_ATTR
+#undef FGS_ATTR1
         if (ea != cudaSuccess) { fgs_set_cuda_error(ea); return FGS_E_CUDA; }
         attr_once.mark(attr_dev);
     }
-#define FGS_K1(S, B) k_preprocess<S, B><<<blocks, FGS_PRE_THREADS, kShBytes, st>>>( \
+    const bool banded = band0 > 0 || band1 < cam.grid_h - 1;
+#define FGS_K1N(S, B, N) k_preprocess<S, B, N><<<blocks, FGS_PRE_THREADS, kShBytes, st>>>( \
         sc, kcut, (int)P, cam, tau32, fth, sh_degree, band0, band1, f)
+#define FGS_K1(S, B) do { if (banded) FGS_K1N(S, B, true); else FGS_K1N(S, B, false); } while (0)
     switch (strategy) {
     case FGS_PRECISE:
         if (bucket) FGS_K1(FGS_PRECISE, true); else FGS_K1(FGS_PRECISE, false);

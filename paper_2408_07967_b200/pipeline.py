@@ -311,6 +311,22 @@ class Pipeline:
         from .scene_io import load_ply_device
         return cls(load_ply_device(path, kw.get("device")), **kw)
 
+    def row_weights(self, camera, tau=TAU_DEFAULT):
+        """Load estimate per tile row for the multi-GPU row-band split:
+        in-frustum Gaussians whose projected centre lies in the row (``fgs_row_histogram``),
+        as a NumPy int64 array of ``ceil(height / 16)`` counts.  Exact integers: every rank
+        of a band job gets the same array and hence the same
+        ``sharding.balanced_band_partition``."""
+        torch = _torch()
+        gh = -(-int(camera.height) // TILE_SIZE)
+        cam = _capi.camera_struct(camera)
+        with torch.cuda.device(self.device):
+            hist = torch.empty(gh, dtype=torch.int32, device=self.device)
+            _capi.check(_capi.lib().fgs_row_histogram(self.packed.data_ptr(), self.count, C.byref(cam),
+                                                      float(tau), hist.data_ptr(),
+                                                      _stream_ptr(torch, self.device)))
+            return hist.cpu().numpy().view(np.uint32).astype(np.int64)
+
     # -- per-tau cutoff table (extent.py:19-30), cached -------------------------
     def _cutoffs(self, torch, tau):
         key = float(tau)
@@ -745,6 +761,8 @@ def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, worke
             .view(np.uint16).reshape(P, 4).astype(np.int32)
         counts = ws.view(torch, lay.off_counts, P * 4, torch.int32).cpu().numpy().view(np.uint32).copy()
         keys = ws.view(torch, lay.off_keys[0], M * 8, torch.int64).cpu().numpy().view(np.uint64).copy()
+        # a band frame writes splat rows only for Gaussians with candidate tiles in the band
+        splat[(rects[:, 3] < b0) | (rects[:, 1] > b1)] = 0.0
         if mode == "tile-bucket":
             # records are (depth bits << 32 | index), bucketed by tile: rebuild the
             # reference's (tile << 32 | depth bits, index) pairs from the range table

@@ -32,6 +32,47 @@ def band_partition(grid_h: int, world: int) -> list:
     return out
 
 
+def balanced_band_partition(row_weights, world: int, fixed_rows: float = 0.0) -> list:
+    """Inclusive tile-row bands [(ty0, ty1)] per rank with (nearly) equal summed weight
+    instead of equal height.  ``row_weights[ty]`` is the load estimate of tile row ``ty``
+    (``Pipeline.row_weights``: in-frustum Gaussians centred in the row -- integers that every
+    rank computes identically, so all ranks cut the same bands without communicating);
+    ``fixed_rows`` adds a per-row cost in the same unit (pixels cost something even where no
+    Gaussian lands).  Band k ends at the first row where the running weight reaches
+    (k+1)/world of the total; every rank gets at least one row while rows remain.  The
+    rendered frame does not depend on the cut (bands are independent)."""
+    w = [float(v) + float(fixed_rows) for v in row_weights]
+    grid_h = len(w)
+    if grid_h < 1 or world < 1:
+        raise ValueError("row_weights must be non-empty and world positive")
+    total = sum(w)
+    if total <= 0.0:
+        return band_partition(grid_h, world)
+    out, y, run = [], 0, 0.0
+    for r in range(world):
+        left = world - r - 1                      # ranks still to be served after this one
+        if y >= grid_h:
+            out.append((grid_h, grid_h - 1))      # empty band
+            continue
+        if left == 0:
+            out.append((y, grid_h - 1))
+            y = grid_h
+            continue
+        target = total * (r + 1) / world
+        y1 = y
+        run += w[y1]
+        # extend while below the target, leaving at least one row for each later rank
+        while run < target and y1 + 1 < grid_h - left:
+            # stop early if adding the next row overshoots by more than stopping undershoots
+            if run + w[y1 + 1] - target > target - run:
+                break
+            y1 += 1
+            run += w[y1]
+        out.append((y, y1))
+        y = y1 + 1
+    return out
+
+
 def band_pixel_rows(band, height: int) -> tuple:
     """Pixel-row slice [y0, y1) covered by an inclusive tile-row band."""
     ty0, ty1 = band

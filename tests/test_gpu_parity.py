@@ -748,3 +748,41 @@ def test_north_star_size_properties():
     assert np.array_equal(k1, keys) and np.array_equal(v1, vals) and np.array_equal(s1, starts)
     f1, _ = pipe1.render(cam)
     assert np.array_equal(f1.image, full.image)
+
+
+def test_row_weights_and_balanced_bands():
+    """fgs_row_histogram counts the in-frustum Gaussians by the tile row of their projected
+    centre (checked against the splat rows the oracle writes), and the union of the
+    work-balanced bands it leads to is bit-identical to the whole frame."""
+    from paper_2408_07967_b200 import sharding
+    act = fgs.activate(fgs.gen_synthetic("mixed", 30000, 17))
+    cam = fgs.orbit_cameras(1, 9.0, 640, 400)[0]            # camera inside the cloud: culling matters
+    pipe = fgs.Pipeline(act)
+    rw = pipe.row_weights(cam)
+    gh = -(-400 // 16)
+    assert rw.shape == (gh,) and rw.dtype == np.int64
+    # host restatement: frustum_mask (projection.py:39-47) + ndc2pix centre row
+    m = np.asarray(act.means, np.float32)
+    v = np.asarray(cam.world_to_camera, np.float32)
+    z = ((v[2, 0] * m[:, 0] + v[2, 1] * m[:, 1]) + v[2, 2] * m[:, 2]) + v[2, 3]
+    keep = (z > np.float32(0.2)) & (np.asarray(act.opacities) > np.float32(1 / 255))
+    fp = np.asarray(cam.full_projection, np.float32)
+    h1 = ((fp[1, 0] * m[:, 0] + fp[1, 1] * m[:, 1]) + fp[1, 2] * m[:, 2]) + fp[1, 3]
+    h3 = ((fp[3, 0] * m[:, 0] + fp[3, 1] * m[:, 1]) + fp[3, 2] * m[:, 2]) + fp[3, 3]
+    den = np.where(np.abs(h3) > np.float32(1e-7), h3, np.float32(1e-7))
+    py = ((h1 / den + np.float32(1)) * np.float32(400) - np.float32(1)) * np.float32(0.5)
+    ty = np.floor(py * np.float32(0.0625))
+    ok = keep & (ty >= -1) & (ty <= gh)
+    want = np.bincount(np.clip(ty[ok], 0, gh - 1).astype(np.int64), minlength=gh)
+    assert np.array_equal(rw, want)
+    full, st = pipe.render(cam)
+    bands = sharding.balanced_band_partition(rw, 4, fixed_rows=0.3 * float(rw.mean()))
+    assert bands != sharding.band_partition(gh, 4)
+    out = np.zeros_like(full.image)
+    total = 0
+    for b in bands:
+        fb, s = pipe.render(cam, band=b)
+        y0, y1 = sharding.band_pixel_rows(b, 400)
+        out[y0:y1] = fb.image[y0:y1]
+        total += s.pairs_emitted
+    assert np.array_equal(out, full.image) and total == st.pairs_emitted

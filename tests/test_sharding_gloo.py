@@ -90,3 +90,32 @@ def test_band_render_union_equals_full_frame_oracle():
         y0, y1 = sharding.band_pixel_rows(b, 100)
         out[y0:y1] = img[y0:y1]
     assert np.array_equal(out, img)
+
+
+def test_balanced_band_partition_properties():
+    """Work-balanced bands: contiguous, cover every row once, every rank gets a row while
+    rows remain, and the heaviest band is never worse than with equal heights."""
+    rng = np.random.default_rng(5)
+    for grid_h, world in [(270, 8), (68, 4), (135, 2), (7, 8), (16, 1), (5, 5)]:
+        for trial in range(20):
+            w = rng.integers(0, 1000, grid_h)
+            if trial % 3 == 0:                      # a bump in the middle, empty borders
+                w = (1000 * np.exp(-0.5 * ((np.arange(grid_h) - grid_h / 2) / (grid_h / 8 + 1)) ** 2)).astype(int)
+            bands = sharding.balanced_band_partition(w, world)
+            assert len(bands) == world
+            rows = [y for a, b in bands for y in range(a, b + 1)]
+            assert rows == list(range(grid_h))
+            nonempty = [b for b in bands if b[1] >= b[0]]
+            assert len(nonempty) == min(world, grid_h)
+            heavy = max(int(w[a:b + 1].sum()) for a, b in nonempty)
+            equal = max(int(w[a:b + 1].sum()) for a, b in sharding.band_partition(grid_h, world) if b >= a)
+            assert heavy <= max(equal, int(w.max()) + int(w.sum()) // world)
+    # the bump: equal heights leave the middle band with most of the work
+    w = np.zeros(270, int)
+    w[100:170] = 100
+    bal = max(int(w[a:b + 1].sum()) for a, b in sharding.balanced_band_partition(w, 8))
+    eq = max(int(w[a:b + 1].sum()) for a, b in sharding.band_partition(270, 8))
+    assert bal <= 900 and eq >= 3300
+    assert sharding.balanced_band_partition([0, 0, 0], 2) == sharding.band_partition(3, 2)
+    with pytest.raises(ValueError):
+        sharding.balanced_band_partition([], 2)
