@@ -1,0 +1,14 @@
+#!/bin/bash
+# compute-sanitizer passes over small frames (run under gpurun): memcheck on a few parity tests,
+# racecheck + synccheck on the smoke frame.  Logs land in gpurun_out/sanitize_*.log.
+export FGS_SANITIZE=1
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 --log-file gpurun_out/sanitize_memcheck.log \
+  python -m pytest tests/test_gpu_parity.py tests/test_scene_io.py -x -q -m gpu \
+  -k "golden_pipeline_render or binning_known_answers or row_weights or empty_scene or forced_regrow or device_ingest or row_bands" \
+  > gpurun_out/sanitize_memcheck.out 2>&1; echo "memcheck rc=$?"
+tail -3 gpurun_out/sanitize_memcheck.out; tail -4 gpurun_out/sanitize_memcheck.log
+for tool in racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 --log-file gpurun_out/sanitize_$tool.log \
+    python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/sanitize_$tool.out 2>&1; echo "$tool rc=$?"
+  tail -1 gpurun_out/sanitize_$tool.out; tail -3 gpurun_out/sanitize_$tool.log
+done
