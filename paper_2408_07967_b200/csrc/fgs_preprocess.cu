@@ -1112,10 +1112,37 @@ int fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream
 // One CTA per 1024 tiles; instead of a second kernel or a spin-wait, CTA b sums
 // the (L2-resident) counts of all tiles before its own -- O(T^2/1024) reads, at
 // most 33 MB for an 8K frame's 129600 tiles, and no inter-CTA dependency at all.
+// For large grids (> FGS_SCAN_DIRECT_CTAS slices) the slices' totals are summed first by this
+// kernel into the spare words 5/6 of the cursor slots, and k_scan_tiles adds up the totals
+// before its slice instead of every count before it (8K frame: 127 slices, the last one would
+// read 129 K counters through one SM: 41 us -> ~10).
+#define FGS_SCAN_DIRECT_CTAS 12
+__global__ void __launch_bounds__(1024)
+k_tile_blocksums(const uint32_t *__restrict__ counts, uint32_t *__restrict__ cursor, int tiles)
+{
+    __shared__ unsigned long long s_w[32];
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
+    const int i = blockIdx.x * 1024 + threadIdx.x;
+    unsigned long long v = i < tiles ? (unsigned long long)counts[(size_t)i * FGS_CTR_STRIDE] +
+                                           counts[(size_t)i * FGS_CTR_STRIDE + 1] : 0ull;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(FGS_FULL, v, o);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) t += s_w[k];
+        cursor[(size_t)blockIdx.x * FGS_CTR_STRIDE + 5] = (uint32_t)t;
+        cursor[(size_t)blockIdx.x * FGS_CTR_STRIDE + 6] = (uint32_t)(t >> 32);
+    }
+}
+
 __global__ void __launch_bounds__(1024)
 k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
              uint32_t *__restrict__ cursor, uint32_t *__restrict__ bincount, int tiles,
-             unsigned long long capacity, fgs_stats *__restrict__ stats)
+             unsigned long long capacity, fgs_stats *__restrict__ stats, int use_sums)
 {
     __shared__ unsigned long long s_w[32];
     __shared__ uint32_t s_bin[FGS_ORDER_BINS];
@@ -1126,8 +1153,14 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     const int first = blockIdx.x * 1024;
     // prefix of everything before this CTA's slice
     unsigned long long before = 0;
-    for (int i = threadIdx.x; i < first; i += 1024)
-        before += counts[(size_t)i * FGS_CTR_STRIDE] + counts[(size_t)i * FGS_CTR_STRIDE + 1];
+    if (use_sums) {
+        for (int j = threadIdx.x; j < (int)blockIdx.x; j += 1024)
+            before += (unsigned long long)cursor[(size_t)j * FGS_CTR_STRIDE + 5] |
+                      ((unsigned long long)cursor[(size_t)j * FGS_CTR_STRIDE + 6] << 32);
+    } else {
+        for (int i = threadIdx.x; i < first; i += 1024)
+            before += counts[(size_t)i * FGS_CTR_STRIDE] + counts[(size_t)i * FGS_CTR_STRIDE + 1];
+    }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) before += __shfl_xor_sync(FGS_FULL, before, o);
     if (lane == 0) s_w[w] = before;
@@ -1191,8 +1224,14 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
 
 int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st)
 {
-    FGS_CHAIN(k_scan_tiles, dim3((unsigned)((tiles + 1023) / 1024)), dim3(1024), 0, st,
-              f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats);
+    const unsigned slices = (unsigned)((tiles + 1023) / 1024);
+    const int use_sums = slices > FGS_SCAN_DIRECT_CTAS ? 1 : 0;
+    if (use_sums)
+        FGS_CHAIN(k_tile_blocksums, dim3(slices), dim3(1024), 0, st, (const uint32_t *)f.tilecount,
+                  f.cursor, tiles);
+    FGS_CHAIN(k_scan_tiles, dim3(slices), dim3(1024), 0, st,
+              f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats,
+              use_sums);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
