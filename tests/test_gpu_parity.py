@@ -786,3 +786,21 @@ def test_row_weights_and_balanced_bands():
         out[y0:y1] = fb.image[y0:y1]
         total += s.pairs_emitted
     assert np.array_equal(out, full.image) and total == st.pairs_emitted
+
+
+def test_sparse_scene_on_a_large_grid():
+    """A few Gaussians on a 4096x2176 frame (34 816 tiles, mostly empty): the tile scan's
+    slice-total path, empty tiles in every size bin of the blend order, ragged last row."""
+    act = fgs.activate(fgs.gen_synthetic("mixed", 3000, 23))
+    cam = fgs.orbit_cameras(1, 18.0, 4096, 2170)[0]
+    pipe = fgs.Pipeline(act)
+    ob = orc.preprocess_and_bin(act, cam)
+    ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, act.count)
+    keys, vals, starts = fgs.sorted_pairs(pipe, cam)
+    assert np.array_equal(keys, ok) and np.array_equal(vals, ov)
+    assert np.array_equal(starts, orc.tile_range_table(ok, ob.grid_w, ob.grid_h))
+    oimg, ost = orc.render(act, cam, "precise", 1 / 255, (0.2, 0.1, 0.3))
+    fb, st = pipe.render(cam, "precise", 1 / 255, (0.2, 0.1, 0.3), exact=True)
+    assert np.array_equal(fb.image.view(np.uint32), oimg.view(np.uint32))
+    assert (st.pairs_emitted, st.tiles_nonempty, st.pairs_contributing) == \
+        (ost["pairs_emitted"], ost["tiles_nonempty"], ost["pairs_contributing"])

@@ -4,7 +4,7 @@
 export FGS_SANITIZE=1
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 --log-file gpurun_out/sanitize_memcheck.log \
   python -m pytest tests/test_gpu_parity.py tests/test_scene_io.py -x -q -m gpu \
-  -k "golden_pipeline_render or binning_known_answers or row_weights or empty_scene or forced_regrow or device_ingest or row_bands" \
+  -k "golden_pipeline_render or binning_known_answers or row_weights or empty_scene or forced_regrow or device_ingest or row_bands or sparse_scene" \
   > gpurun_out/sanitize_memcheck.out 2>&1; echo "memcheck rc=$?"
 tail -3 gpurun_out/sanitize_memcheck.out; tail -4 gpurun_out/sanitize_memcheck.log
 for tool in racecheck synccheck; do
