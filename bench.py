@@ -231,6 +231,7 @@ def main():
     # a view batch: this rank's share of the views (view v -> rank v mod world), cycled
     my_cams = [cams[v] for v in sharding.views_for_rank(ncam, world, rank)] if nviews else [cam]
     gh = -(-H // 16)
+    gw = -(-W // 16)
     band = None
     bands = sharding.band_partition(gh, world)
     if args.mode == "bands" and world > 1:
@@ -531,7 +532,9 @@ def main():
                     "single_call_ms": single_ms},
             # kernels of this library launched inside the timed region: the profiling marks
             # (one per stage kernel) + k_tile_order, which shares the emit stage's mark
-            "gpu_launches": int((n_marks + (1 if bucket else 0)) * K),
+            # and, on grids above 12 slices of 1024 tiles, k_tile_blocksums (scan stage's mark)
+            "gpu_launches": int((n_marks + (1 if bucket else 0)
+                                 + (1 if bucket and (gw * gh + 1023) // 1024 > 12 else 0)) * K),
             "roofline": roof,
             "cpu_baseline": cpu,
             "kernels": kernels,
