@@ -47,6 +47,8 @@
 #define FGS_WORK_LARGE    0
 #define FGS_WORK_MEDIUM_TICKET 2   // (+1: CTAs out) tile tickets of the persistent sort kernels
 #define FGS_WORK_LARGE_TICKET  4   // (+1: CTAs out)
+#define FGS_WORK_SORT_DONE     6   // bit 0: medium class finished, bit 1: large class finished
+#define FGS_WORK_TAIL_OUT      7   // tail-kernel CTAs past their wait on FGS_WORK_SORT_DONE
 // blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
 // empty = last) and the blend's CTAs take them in bin order, so the long tiles start first
 // and the grid's tail is made of short ones

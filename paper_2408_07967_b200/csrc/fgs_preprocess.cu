@@ -1242,7 +1242,7 @@ int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaSt
 // Order inside a bin is arbitrary (every tile's output is independent of it).
 __global__ void __launch_bounds__(1024)
 k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int first_tile,
-             int band_tiles, const fgs_stats *__restrict__ stats)
+             int band_tiles, uint32_t *__restrict__ tile_ctr, const fgs_stats *__restrict__ stats)
 {
     __shared__ uint32_t s_base[FGS_ORDER_BINS], s_cnt[FGS_ORDER_BINS], s_off[FGS_ORDER_BINS];
     fgs_pdl_wait();
@@ -1269,6 +1269,9 @@ k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int
         const int tile = first_tile + i;
         bin = fgs_order_bin((uint32_t)(starts[tile + 1] - starts[tile]));
         rank = atomicAdd(&s_cnt[bin], 1u);
+        // the placement kernel's per-pair fallback cursor (word 2) starts at zero every time
+        // the stage is issued, not only on the frame's first pass (fgs_emit is idempotent)
+        if (tile_ctr[(size_t)tile * FGS_CTR_STRIDE + 1]) tile_ctr[(size_t)tile * FGS_CTR_STRIDE + 2] = 0u;
     }
     __syncthreads();
     if (t < FGS_ORDER_BINS && s_cnt[t]) s_off[t] = atomicAdd(&hdr[FGS_ORDER_BINS + t], s_cnt[t]);
@@ -1290,7 +1293,7 @@ int fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, c
     if (band1 < band0) return FGS_OK;
     const int band_tiles = (band1 - band0 + 1) * grid_w;
     FGS_CHAIN(k_tile_order, dim3((unsigned)((band_tiles + 1023) / 1024)), dim3(1024), 0, st,
-              f.starts, f.tileorder, band0 * grid_w, band_tiles, f.stats);
+              f.starts, f.tileorder, band0 * grid_w, band_tiles, f.tilecount, f.stats);
     FGS_CHECK_LAUNCH();
     return FGS_OK;
 }

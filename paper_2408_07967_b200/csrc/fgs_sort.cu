@@ -735,12 +735,22 @@ struct TileTickets {
         __syncthreads();
         return i;
     }
-    __device__ __forceinline__ void close()
+    // `done_bit`: raised in FGS_WORK_SORT_DONE by the last worker out, after every worker's
+    // output is visible device-wide -- the tail kernel's explicit join with this class.  (The
+    // classes are chained by launch_dependents WITHOUT a griddepcontrol.wait of their own, so
+    // that they overlap; stream order alone then only promises the tail kernel its immediate
+    // predecessor.)  The caller's loop ends with a barrier: every thread's stores precede this.
+    __device__ __forceinline__ void close(fgs_stats *stats, uint32_t done_bit)
     {
         const uint32_t workers = count < gridDim.x ? count : gridDim.x;
-        if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == workers - 1u) {
-            ctr[0] = 0u;
-            ctr[1] = 0u;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(ctr + 1, 1u) == workers - 1u) {
+                ctr[0] = 0u;
+                ctr[1] = 0u;
+                __threadfence();
+                atomicOr(fgs_work(stats) + FGS_WORK_SORT_DONE, done_bit);
+            }
         }
     }
 };
@@ -824,7 +834,7 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
             hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
     }
-    tk.close();
+    tk.close(stats, 1u);
 }
 
 __global__ void __launch_bounds__(FGS_LARGE_NT, FGS_LARGE_MINB)
@@ -849,7 +859,7 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
             dense_list[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
         __syncthreads();
     }
-    tk.close();
+    tk.close(stats, 2u);
 }
 
 // The tail of the tile sort, one launch: the dense list (split path), then the hard list
@@ -859,9 +869,9 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
                  uint32_t *__restrict__ vals_out, uint64_t *__restrict__ keys_out,
                  const int32_t *__restrict__ starts, const uint32_t *__restrict__ dense_list,
                  const uint32_t *__restrict__ hard_list, int write_keys,
-                 const fgs_stats *__restrict__ stats)
+                 fgs_stats *__restrict__ stats)
 {
-    fgs_pdl_trigger();      // plain launch (waits for every size class); the blend may queue up
+    fgs_pdl_trigger();      // plain launch; the blend may queue up behind this grid
 
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Radix = TileSortSmem<256, 16>;
@@ -870,6 +880,30 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
     BucketSmem<256, 16> *B = reinterpret_cast<BucketSmem<256, 16> *>(
         ts_raw + ((sizeof(Radix) + 15) & ~size_t(15)));
     if (stats->overflow) return;
+    // Explicit join with the medium and large classes (see TileTickets::close): they were
+    // launched before this grid's stream predecessor and every CTA of theirs is resident,
+    // so the flags arrive without this grid's help.  The wait is bounded: a frame that
+    // never sees them is reported as unsorted instead of hanging the device.
+    __shared__ uint32_t s_joined;
+    if (threadIdx.x == 0) {
+        uint32_t *work = fgs_work(stats);
+        const uint32_t need = (stats->medium_tiles ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u);
+        volatile uint32_t *done = work + FGS_WORK_SORT_DONE;
+        uint32_t ok = 1u;
+        for (uint32_t spin = 0; (*done & need) != need; ++spin) {
+            if (spin > (1u << 23)) { ok = 0u; stats->unsorted = 1u; break; }
+            __nanosleep(200);
+        }
+        __threadfence();
+        s_joined = ok;
+        // the last CTA past the join rewinds the flags (the stage may be re-issued on the frame)
+        if (atomicAdd(work + FGS_WORK_TAIL_OUT, 1u) == gridDim.x - 1u) {
+            work[FGS_WORK_SORT_DONE] = 0u;
+            work[FGS_WORK_TAIL_OUT] = 0u;
+        }
+    }
+    __syncthreads();
+    if (!s_joined) return;
     const uint32_t ndense = stats->dense_tiles, nhard = stats->hard_tiles;
     for (uint32_t i = blockIdx.x; i < ndense + nhard; i += gridDim.x) {
         const bool dense = i < ndense;
@@ -896,7 +930,6 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
                   "medium capacity = radix capacity = chunk size of split buckets");
     static FgsOncePerDevice attr_once;
     int attr_dev = 0;
-    static int sms = 148;
     if (attr_once.need(&attr_dev)) {
         cudaError_t e = cudaSuccess;
         auto prep = [&](const void *fn, size_t smem) {
@@ -913,11 +946,11 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         prep((const void *)k_tile_sort_large, sizeof(LargeSmem));
         prep((const void *)k_tile_sort_tail, tail_bytes);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         attr_once.mark(attr_dev);
     }
+    int dev = 0, sms = 148;                 // per call: the persistent grids are sized for THIS device
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     // lists in the spare words of the cursor slots: +1 dense, +2 medium, +3 hard
     uint32_t *dense_list = f.cursor + 1, *medium_list = f.cursor + 2, *hard_list = f.cursor + 3;
     uint32_t *large_list = f.cursor + 4;

@@ -86,7 +86,7 @@ def test_golden_pipeline_render(golden):
         assert _psnr_ok(fb.image, ref)
         assert (st.pairs_emitted, st.gaussians_retained, st.gaussians_degenerate,
                 st.tiles_nonempty) == (want[0], want[2], want[3], want[4])
-        assert abs(st.pairs_contributing - want[1]) <= max(2, want[1] // 10000)
+        assert st.pairs_contributing == want[1]      # the packed blend never flips a skip
         assert st.pair_buffer_bytes == 12 * want[0]
         fbx, stx = pipe.render(cam, "precise", g.tau, g.bg, exact=True)
         assert np.array_equal(fbx.image.view(np.uint32), ref.view(np.uint32))
@@ -643,16 +643,21 @@ def test_packed_blend_rows_outside_its_shortcut():
     assert fgs.max_abs_diff(i2, ix) <= 2e-5
 
 
-def test_stages_can_be_repeated_on_one_frame():
-    """fgs_emit (tile order + placement) and fgs_blend are idempotent on a frame: running
-    them again -- another background, a re-issued stage -- gives the same frame."""
+@pytest.mark.parametrize("preset,n,radius,spatial", [
+    ("mixed", 30000, 20.0, True),
+    ("mixed", 30000, 20.0, False),        # caller-order slots: CTA tile tables overflow ->
+    ("isotropic", 600, 9.5, False),       # ... the per-pair fallback cursor must rewind too
+])
+def test_stages_can_be_repeated_on_one_frame(preset, n, radius, spatial):
+    """fgs_emit (tile order + placement), fgs_sort and fgs_blend are idempotent on a frame:
+    running them again -- another background, a re-issued stage -- gives the same frame."""
     import ctypes as C
     import torch
     from paper_2408_07967_b200 import _capi
-    n, w, h = 30000, 400, 240
-    act = fgs.activate(fgs.gen_synthetic("mixed", n, 31))
-    cam = fgs.orbit_cameras(1, 20.0, w, h)[0]
-    pipe = fgs.Pipeline(act)
+    w, h = 400, 240
+    act = fgs.activate(fgs.gen_synthetic(preset, n, 31))
+    cam = fgs.orbit_cameras(1, radius, w, h)[0]
+    pipe = fgs.Pipeline(act, spatial_order=spatial)
     want, _ = pipe.render(cam)
     L = _capi.lib()
     dev = torch.device("cuda", torch.cuda.current_device())
@@ -669,7 +674,8 @@ def test_stages_can_be_repeated_on_one_frame():
     _capi.check(L.fgs_scan(base, lay, st))
     for _ in range(3):
         _capi.check(L.fgs_emit(pipe.packed.data_ptr(), C.byref(camc), 0, 0, gh - 1, base, lay, st))
-    _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
+    for _ in range(2):
+        _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
     _capi.check(L.fgs_ranges(base, lay, st))
     for _ in range(2):
         _capi.check(L.fgs_blend(pipe.packed.data_ptr(), bg, 1 / 255, 2, 0, gh - 1, ws.rgb.data_ptr(),
