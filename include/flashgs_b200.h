@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define FGS_ABI_VERSION 4
+#define FGS_ABI_VERSION 5
 #define FGS_TILE 16              /* constants.py:4  TILE_SIZE */
 
 enum {
@@ -305,6 +305,17 @@ int fgs_blend(const void *packed_scene, const float background[3], double tau, i
               int32_t band_ty0, int32_t band_ty1,
               float *out_rgb, float *out_alpha, float *out_depth,
               void *workspace, const fgs_layout *layout_host, void *stream);
+
+/* Measurement aid (SURVEY.md 8(d), FP32 roofline of the blend): re-blends the frame whose
+ * sorted pairs are in the workspace with the exact-mode kernel and counts the (pixel, pair)
+ * evaluations of the reference's naive loop (render.py:106-129) by outcome.  counts_out
+ * (device, 8 x uint64, zeroed by the call): [0] rejected by the extent rectangle
+ * (render.py:111), [1] by the cutoff s > k/2 (:114), [2] by alpha < tau (:119), [3] blended,
+ * [4] M_proc = sum over tiles of the pairs visited before the tile's last pixel stopped
+ * (:228-229), [5] pixels.  out_rgb receives the exact-mode frame.  Not on the frame path. */
+int fgs_blend_counts(const void *packed_scene, const float background[3], double tau,
+                     int32_t band_ty0, int32_t band_ty1, float *out_rgb, uint64_t *counts_out,
+                     void *workspace, const fgs_layout *layout_host, void *stream);
 
 /* pipeline.py:77-111 Pipeline.render: the six calls above, back to back on
  * `stream`, no host synchronisation in between. */

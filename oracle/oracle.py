@@ -225,6 +225,23 @@ def render_frame(splat, sorted_values, starts, width, height, background, tau,
     return img, contrib, int(n)
 
 
+EVAL_CLASSES = ("rect_rejected", "cutoff_rejected", "alpha_rejected", "blended")
+
+
+def render_counts(splat, sorted_values, starts, width, height, tau):
+    """Instrumented copy of the naive compositing loop (render.py:106-129): evaluation
+    counts by outcome, M_proc and the pixel count, as a dict."""
+    splat = np.ascontiguousarray(splat, dtype=np.float32)
+    vals = np.ascontiguousarray(sorted_values, dtype=np.uint32)
+    st = np.ascontiguousarray(starts, dtype=np.int64)
+    out = np.zeros(8, np.uint64)
+    lib().orc_render_counts(_p(splat), _p(vals), _p(st), C.c_int(width), C.c_int(height),
+                            C.c_double(tau), _p(out))
+    d = {k: int(out[i]) for i, k in enumerate(EVAL_CLASSES)}
+    d["pairs_processed"], d["pixels"] = int(out[4]), int(out[5])
+    return d
+
+
 def render(act, camera, strategy="precise", tau=1.0 / 255.0,
            background=(0.0, 0.0, 0.0), sh_degree=3, extras=False):
     """Whole path with the reference's three stage timers (pipeline.py:84-102).

@@ -7,8 +7,8 @@ the first call that needs it loads ``_lib/libflashgs_b200.so`` and raises if
 it is absent -- there is no CPU fallback.
 """
 
-from .pipeline import (BinOutput, Framebuffer, FrameStats, Pipeline, STRATEGIES,
-                       TAU_DEFAULT, TILE_SIZE, UnsortedPairsError, max_abs_diff,
+from .pipeline import (EVAL_FLOPS, BinOutput, Framebuffer, FrameStats, Pipeline, STRATEGIES,
+                       TAU_DEFAULT, TILE_SIZE, UnsortedPairsError, blend_eval_counts, max_abs_diff,
                        power_cutoffs, preprocess_and_bin, psnr, render_frame,
                        run_frame, sort_pairs, sorted_pairs, tile_range_table)
 from .reports import REPORT_SCHEMA_VERSION, CompareReport, bench_frames, compare_modes
@@ -29,7 +29,7 @@ __all__ = [
     "ActivatedScene", "BinOutput", "Camera", "CameraValidationError", "CompareReport",
     "Framebuffer", "REPORT_SCHEMA_VERSION", "bench_frames", "compare_modes",
     "FrameStats", "Pipeline", "STRATEGIES", "Scene", "TAU_DEFAULT", "TILE_SIZE",
-    "UnsortedPairsError", "activate", "gen_synthetic", "look_at_camera", "make_camera",
+    "UnsortedPairsError", "EVAL_FLOPS", "blend_eval_counts", "activate", "gen_synthetic", "look_at_camera", "make_camera",
     "max_abs_diff", "orbit_cameras", "power_cutoffs", "preprocess_and_bin", "psnr",
     "read_ppm", "write_png", "write_ppm", "images",
     "render_frame", "run_frame", "service", "sort_pairs", "sorted_pairs", "tile_range_table",

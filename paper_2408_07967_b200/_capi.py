@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # FGS_LIB selects another build of the same library (tuning variants, see build.py)
 LIB_PATH = os.environ.get("FGS_LIB") or os.path.join(HERE, "_lib", "libflashgs_b200.so")
 
-ABI_VERSION = 4
+ABI_VERSION = 5
 STRATEGIES = ("baseline-circle-aabb", "tight-aabb", "precise")   # binning.py:38 order
 STRATEGY_ID = {"precise": 0, "tight-aabb": 1, "baseline-circle-aabb": 2}
 BLEND_EXACT, BLEND_CONTRIB, BLEND_SCALAR = 1, 2, 4
@@ -31,7 +31,7 @@ SYMBOLS = (
     "fgs_workspace_init",
     "fgs_preprocess", "fgs_row_histogram", "fgs_scan", "fgs_emit", "fgs_sort", "fgs_ranges", "fgs_blend",
     "fgs_render", "fgs_sort_pairs_scratch_bytes", "fgs_sort_pairs", "fgs_tile_ranges",
-    "fgs_blend_tiles", "fgs_profile_begin", "fgs_profile_end", "fgs_quantize_rgb8",
+    "fgs_blend_tiles", "fgs_blend_counts", "fgs_profile_begin", "fgs_profile_end", "fgs_quantize_rgb8",
 )
 
 
@@ -115,6 +115,7 @@ def _declare(L):
         "fgs_sort": (C.c_int, [vp, lay_p, u32, vp]),
         "fgs_ranges": (C.c_int, [vp, lay_p, vp]),
         "fgs_blend": (C.c_int, [vp, f3, dbl, i32, i32, i32, vp, vp, vp, vp, lay_p, vp]),
+        "fgs_blend_counts": (C.c_int, [vp, f3, dbl, i32, i32, vp, vp, vp, lay_p, vp]),
         "fgs_render": (C.c_int, [vp, vp, i64, cam_p, dbl, i32, i32, f3, i32, i32, i32, u32,
                                  vp, vp, vp, vp, lay_p, vp]),
         "fgs_sort_pairs_scratch_bytes": (C.c_size_t, [i64]),

@@ -117,16 +117,26 @@ struct BlendSmem {
     unsigned long long tab[32];
 };
 
-template <bool EXACT, bool CONTRIB, bool EXTRAS>
+// COUNT (diagnostic, EXACT only): classify every (pixel, pair) evaluation the reference's
+// naive loop performs (render.py:106-129) -- rejected by the extent rectangle (:111),
+// by the cutoff (:114), by alpha < tau (:119), or blended -- and count, per tile, the
+// pairs visited before the tile's last pixel stops (M_proc of SURVEY.md 8(d)).  The
+// warp-level culls are switched off so that every live pixel classifies every pair
+// itself.  evals[0..3] = the four classes, [4] = M_proc, [5] = pixels.
+template <bool EXACT, bool CONTRIB, bool EXTRAS, bool COUNT = false>
 __global__ void __launch_bounds__(256)
 k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
         const int32_t *__restrict__ starts, const uint32_t *__restrict__ order, int width,
         int height, int grid_w, int first_tile, float bg0, float bg1, float bg2, float tau,
         float *__restrict__ rgb, float *__restrict__ alpha_out, float *__restrict__ depth_out,
-        uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
+        uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats,
+        unsigned long long *__restrict__ evals = nullptr)
 {
     __shared__ BlendSmem S;
+    __shared__ uint32_t s_mproc;
+    uint32_t ev_rect = 0, ev_cut = 0, ev_alpha = 0, ev_blend = 0, visited = 0;
+    if (COUNT && threadIdx.x == 0) s_mproc = 0u;
     if (stats != nullptr && stats->overflow) return;   // frame is re-run with a larger buffer
     const int tid = threadIdx.x;
     // CTA i takes the i-th tile of the blend order (heaviest first), or of the band in
@@ -205,7 +215,8 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
             // subtraction is monotone, so testing the block's extreme centres is exact)
             const int jl = c0 + lane;
             bool keep = false;
-            if (jl < cnt) {
+            if (COUNT) keep = jl < cnt;
+            else if (jl < cnt) {
                 const float4 q0 = S.row[cur][jl][0];
                 const float4 q1 = S.row[cur][jl][1];
                 const float4 q2 = S.row[cur][jl][2];
@@ -237,6 +248,11 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                                    fm(fm(r0.w, dx), dy));
                 // render.py:211 extent rectangle (exact float32 compares), :214 cutoff
                 bool on = !(fabsf(dx) > r2.z) && !(fabsf(dy) > r2.w) && !(s > fm(0.5f, r1.z));
+                const bool ev_live = COUNT && fx != kInf;             // render.py:108 pixel still open
+                if (ev_live) {
+                    if (fabsf(dx) > r2.z || fabsf(dy) > r2.w) ++ev_rect;
+                    else if (!on) ++ev_cut;
+                }
                 float al;
                 if (EXACT) {
                     al = on ? fm(r1.y, expf_exact(-s, S.tab)) : 0.0f;
@@ -246,6 +262,7 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                         al = fm(r1.y, expf_exact(-s, S.tab));
                 }
                 al = al > FGS_ALPHA_CAP ? FGS_ALPHA_CAP : al;     // render.py:217-218
+                if (ev_live && on) { if (al < tau) ++ev_alpha; else ++ev_blend; }
                 on = on && !(al < tau);                           // render.py:219
                 al = on ? al : 0.0f;
                 if (EXACT) {
@@ -264,6 +281,7 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
                     T = T * (1.0f - al);
                 }
                 if (CONTRIB && on) S.touched[cur][j] = 1u;
+                if (COUNT && ev_live && T < FGS_T_STOP) visited = (uint32_t)(b * FGS_BLEND_BATCH + j + 1);
                 if (T < FGS_T_STOP) fx = kInf;                    // render.py:228
             }
         }
@@ -301,6 +319,26 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
     if (CONTRIB) {
         ncontrib = __reduce_add_sync(FGS_FULL, ncontrib);
         if ((tid & 31) == 0 && ncontrib) atomicAdd(&stats->pairs_contributing, ncontrib);
+    }
+    if (COUNT && evals != nullptr) {
+        // a pixel that never stopped visited the whole list; pixels outside the image none
+        if (inside && fx != kInf) visited = (uint32_t)n;
+        if (!inside) visited = 0u;
+        __syncthreads();                    // s_mproc's initial zero (an empty tile has no barrier before here)
+        const uint32_t vmax = __reduce_max_sync(FGS_FULL, visited);
+        if ((tid & 31) == 0) atomicMax(&s_mproc, vmax);
+        const uint32_t c0 = __reduce_add_sync(FGS_FULL, ev_rect), c1 = __reduce_add_sync(FGS_FULL, ev_cut);
+        const uint32_t c2 = __reduce_add_sync(FGS_FULL, ev_alpha), c3 = __reduce_add_sync(FGS_FULL, ev_blend);
+        const uint32_t c5 = __reduce_add_sync(FGS_FULL, inside ? 1u : 0u);
+        if ((tid & 31) == 0) {
+            if (c0) atomicAdd(&evals[0], (unsigned long long)c0);
+            if (c1) atomicAdd(&evals[1], (unsigned long long)c1);
+            if (c2) atomicAdd(&evals[2], (unsigned long long)c2);
+            if (c3) atomicAdd(&evals[3], (unsigned long long)c3);
+            if (c5) atomicAdd(&evals[5], (unsigned long long)c5);
+        }
+        __syncthreads();
+        if (tid == 0 && s_mproc) atomicAdd(&evals[4], (unsigned long long)s_mproc);
     }
 }
 
@@ -652,6 +690,25 @@ int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *va
                               grid_w, first_tile, bg, tau32, rgb, alpha, depth, contrib, stats)
     return want_contrib ? FGS_GO2(true) : FGS_GO2(false);
 #undef FGS_GO2
+}
+
+// Diagnostic pass over a finished frame's sorted pairs: the exact-mode blend with the
+// evaluation counters on (see k_blend, COUNT).  `evals` is zeroed here.
+int fgs_launch_blend_counts(const float *splat, const uint32_t *vals, const uint32_t *inv,
+                            const int32_t *starts, int width, int height, const float bg[3],
+                            double tau, int band0, int band1, float *rgb, fgs_stats *stats,
+                            unsigned long long *evals, cudaStream_t st)
+{
+    const int grid_w = (width + FGS_TILE - 1) / FGS_TILE;
+    cudaError_t e = cudaMemsetAsync(evals, 0, 8 * sizeof(unsigned long long), st);
+    if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+    if (band1 < band0) return FGS_OK;
+    const dim3 grid((unsigned)(grid_w * (band1 - band0 + 1)));
+    k_blend<true, false, false, true><<<grid, 256, 0, st>>>(
+        splat, nullptr, vals, inv, starts, nullptr, width, height, grid_w, band0 * grid_w, bg[0],
+        bg[1], bg[2], (float)tau, rgb, nullptr, nullptr, nullptr, stats, evals);
+    FGS_CHECK_LAUNCH();
+    return FGS_OK;
 }
 
 // images.py:12-15 quantize (float64 like the reference); four values per thread

@@ -338,6 +338,19 @@ int fgs_blend(const void *packed, const float bg[3], double tau, int32_t flags, 
                             f.stats, (cudaStream_t)stream);
 }
 
+int fgs_blend_counts(const void *packed, const float bg[3], double tau, int32_t band0, int32_t band1,
+                     float *out_rgb, uint64_t *counts_out, void *ws, const fgs_layout *L, void *stream)
+{
+    if (!bg || !out_rgb || !counts_out || !ws || !L) return FGS_E_ARG;
+    if (band0 < 0 || band1 >= L->grid_h) return FGS_E_ARG;
+    if (L->gaussians && !packed) return FGS_E_ARG;
+    FrameDev f = fgs_frame_view(ws, L);
+    return fgs_launch_blend_counts(f.splat, f.vals[L->sorted_vals_in],
+                                   fgs_scene_view(packed, L->gaussians).inv, f.starts, L->width,
+                                   L->height, bg, tau, band0, band1, out_rgb, f.stats,
+                                   (unsigned long long *)counts_out, (cudaStream_t)stream);
+}
+
 int fgs_render(const void *packed, const float *k_cut, int64_t P, const fgs_camera *cam, double tau,
                int32_t sh_degree, int32_t strategy, const float bg[3], int32_t blend_flags,
                int32_t band0, int32_t band1, uint32_t epoch, float *out_rgb, float *out_alpha,

@@ -204,6 +204,10 @@ int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *v
                       double tau, int flags, int band0, int band1, float *rgb, float *alpha,
                       float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st);
 
+int  fgs_launch_blend_counts(const float *splat, const uint32_t *vals, const uint32_t *inv,
+                             const int32_t *starts, int width, int height, const float bg[3],
+                             double tau, int band0, int band1, float *rgb, fgs_stats *stats,
+                             unsigned long long *evals, cudaStream_t st);
 int  fgs_launch_quantize(const float *rgb, int64_t count, uint8_t *out, cudaStream_t st);
 
 void fgs_set_cuda_error(cudaError_t e);

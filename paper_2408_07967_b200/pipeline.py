@@ -627,6 +627,56 @@ def sorted_pairs(pipe, camera, strategy="precise", tau=TAU_DEFAULT, band=None):
     return keys, vals, starts
 
 
+# FP32 operations of one (pixel, pair) evaluation by where the reference's loop leaves it
+# (render.py:106-129, counted as SURVEY.md 8(d) does): rectangle-rejected 2 sub + 4 compare;
+# cutoff-rejected + 9 for the quadratic form + 1 compare; alpha-rejected + neg, exp, mul, min,
+# compare; blended + alpha*T, 3 FMA (= 6), 1 - alpha, T *=, compare.
+EVAL_FLOPS = {"rect_rejected": 6, "cutoff_rejected": 16, "alpha_rejected": 21, "blended": 31}
+
+
+def blend_eval_counts(pipe, camera, strategy="precise", tau=TAU_DEFAULT):
+    """Measurement aid for the blend's FP32 roofline: renders ``camera`` and re-blends the
+    frame's sorted pairs with the counting variant of the exact kernel (``fgs_blend_counts``).
+    Returns the (pixel, pair) evaluation counts of the reference's naive loop by outcome,
+    ``pairs_processed`` (M_proc: pairs visited before their tile's last pixel stopped),
+    ``pixels``, ``pairs_emitted`` and ``flops`` (EVAL_FLOPS-weighted)."""
+    torch = _torch()
+    sid = _strategy_id(strategy)
+    L = _capi.lib()
+    cam = _capi.camera_struct(camera)
+    W, H = int(camera.width), int(camera.height)
+    gh = -(-H // TILE_SIZE)
+    bg_c = (C.c_float * 3)(0.0, 0.0, 0.0)
+    capacity = pipe._default_capacity()
+    with torch.cuda.device(pipe.device):
+        st = _stream_ptr(torch, pipe.device)
+        kcut = pipe._cutoffs(torch, tau)
+        while True:
+            ws = pipe._take_ws(torch, W, H, capacity)
+            ws.set_mode(_capi.SORT_MODES[pipe.sort_mode])
+            lay, base = C.byref(ws.lay), C.c_void_p(ws.base)
+            _capi.check(L.fgs_render(pipe.packed.data_ptr(), kcut.data_ptr(), pipe.count, C.byref(cam),
+                                     float(tau), _check_sh_degree(pipe.sh_degree), sid, bg_c, 0, 0,
+                                     gh - 1, ws.next_epoch(), ws.rgb.data_ptr(), None, None, base,
+                                     lay, st))
+            s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+            if int(s["overflow"]):
+                capacity = max(int(capacity * 1.5) + 16,
+                               max(int(s["pairs_emitted"]), int(s["list_used"])) + 4096)
+                continue
+            break
+        ev = torch.zeros(8, dtype=torch.int64, device=pipe.device)
+        _capi.check(L.fgs_blend_counts(pipe.packed.data_ptr(), bg_c, float(tau), 0, gh - 1,
+                                       ws.rgb.data_ptr(), ev.data_ptr(), base, lay, st))
+        c = ev.cpu().numpy()
+        pipe._give_ws(ws)
+    out = {k: int(c[i]) for i, k in enumerate(EVAL_FLOPS)}
+    out["flops"] = sum(EVAL_FLOPS[k] * out[k] for k in EVAL_FLOPS)
+    out["pairs_processed"], out["pixels"] = int(c[4]), int(c[5])
+    out["pairs_emitted"] = int(s["pairs_emitted"])
+    return out
+
+
 def run_frame(scene, camera, strategy="precise", tau=TAU_DEFAULT,
               background=(0.0, 0.0, 0.0), workers=1, sh_degree=3, **kwargs):
     """One-shot convenience wrapper (``pipeline.py:114-119``)."""

@@ -162,3 +162,84 @@ def test_integration_doc_structs_match_the_library():
     assert [f[0] for f in ns["Cam"]._fields_] == [f[0] for f in _capi.FgsCamera._fields_]
     assert C.sizeof(ns["Layout"]) == C.sizeof(_capi.FgsLayout)
     assert [f[0] for f in ns["Layout"]._fields_] == [f[0] for f in _capi.FgsLayout._fields_]
+
+
+# ---------------------------------------------------------------------------
+# INTEGRATION.md option A: the reference's own Scene / Camera objects go straight
+# through the host boundary.  Needs the reference tree (this container only); it
+# is imported from a scratch copy so nothing is written under /root/reference.
+# ---------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def tilesplat():
+    src = "/root/reference/pkg/src/tilesplat"
+    if not os.path.isdir(src):
+        pytest.skip("reference tree not present on this box")
+    import importlib
+    import shutil
+    import sys
+    d = tempfile.mkdtemp(prefix="fgs_ref_")
+    shutil.copytree(src, os.path.join(d, "tilesplat"),
+                    ignore=shutil.ignore_patterns("__pycache__"))
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(d, "numba_cache"))
+    old = sys.dont_write_bytecode
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, d)
+    try:
+        mod = importlib.import_module("tilesplat")
+    except Exception as e:                         # numba / pillow missing on this box
+        pytest.skip(f"reference not importable here: {e}")
+    finally:
+        sys.path.remove(d)
+        sys.dont_write_bytecode = old
+    yield mod
+    shutil.rmtree(d, ignore_errors=True)
+
+
+def test_reference_objects_pass_the_boundary_unchanged(tilesplat):
+    """The reference's Scene, ActivatedScene and Camera are accepted as they are: same
+    field names, bit-identical activation, identical flattened camera."""
+    from paper_2408_07967_b200 import scene as sc
+    ts = tilesplat
+    raw_ref = ts.gen_synthetic("mixed", 3000, 5)
+    raw_own = fgs.gen_synthetic("mixed", 3000, 5)
+    assert sc.is_raw_scene(raw_ref) and not sc.is_activated_scene(raw_ref)
+    for f in ("means", "sh", "logit_opacities", "log_scales", "rotations"):
+        assert np.array_equal(np.asarray(getattr(raw_ref, f)), np.asarray(getattr(raw_own, f))), f
+    act_ref = ts.activate(raw_ref)
+    assert sc.is_activated_scene(act_ref) and not sc.is_raw_scene(act_ref)
+    act_own = fgs.activate(raw_ref)                 # our activate on THEIR object
+    for f in ("means", "opacities", "scales", "rotations", "sh"):
+        a, b = np.asarray(getattr(act_ref, f)), np.asarray(getattr(act_own, f))
+        assert a.dtype == b.dtype == np.float32 and np.array_equal(a.view(np.uint32), b.view(np.uint32)), f
+    cams_ref = ts.orbit_cameras(3, 24.0, 640, 360)
+    cams_own = fgs.orbit_cameras(3, 24.0, 640, 360)
+    for cr, co in zip(cams_ref, cams_own):
+        a, b = _capi.camera_struct(cr), _capi.camera_struct(co)
+        assert bytes(a) == bytes(b)
+        assert cr.grid == co.grid
+    # make_camera validation behaves like the reference's
+    with pytest.raises(ts.model_io.CameraValidationError):
+        ts.make_camera(8, 64, (0, 0, 0), np.eye(3), 32.0, 32.0)
+    with pytest.raises(fgs.CameraValidationError):
+        fgs.make_camera(8, 64, (0, 0, 0), np.eye(3), 32.0, 32.0)
+
+
+def test_oracle_matches_the_reference_on_a_fresh_case(tilesplat):
+    """The oracle against the reference run here, on a case that is not a committed fixture
+    (pair list, sorted order, range table, frame bits, contrib flags, counters)."""
+    from oracle import oracle as orc
+    ts = tilesplat
+    act = ts.activate(ts.gen_synthetic("elongated", 2500, 21))
+    cam = ts.orbit_cameras(2, 15.0, 208, 120)[1]
+    for strat in ("precise", "tight-aabb"):
+        b = ts.preprocess_and_bin(act, cam, strat, 1 / 255, workers=2)
+        keys, vals = ts.sort_pairs(b.keys, b.values, 2, b.grid_w * b.grid_h, act.count)
+        ob = orc.preprocess_and_bin(act, cam, strat)
+        ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, act.count)
+        assert np.array_equal(keys, ok) and np.array_equal(vals, ov)
+        assert np.array_equal(b.splat.view(np.uint32), ob.splat.view(np.uint32))
+    fb, st = ts.Pipeline(act).render(cam, "precise", workers=2)
+    oimg, ost = orc.render(act, cam)
+    assert np.array_equal(fb.image.view(np.uint32), oimg.view(np.uint32))
+    assert (st.pairs_emitted, st.pairs_contributing, st.tiles_nonempty) == \
+        (ost["pairs_emitted"], ost["pairs_contributing"], ost["tiles_nonempty"])

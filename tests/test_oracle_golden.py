@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as orc
+from fgs_testlib import GoldenCase
 
 STRATS = ("precise", "tight-aabb", "baseline-circle-aabb")
 
@@ -93,3 +94,58 @@ def test_range_table_examples():
         orc.tile_range_table(keys[::-1].copy(), 2, 2)
     with pytest.raises(ValueError):
         orc.tile_range_table(np.array([9], np.uint64) << np.uint64(32), 2, 2)
+
+
+def test_eval_counts_against_a_numpy_restatement():
+    """The instrumented copy of the compositing loop (orc_render_counts, the source of the
+    blend's FP32 roofline) against a plain NumPy/Python restatement of render.py:106-129 on a
+    small golden case: class counts, M_proc and pixel count."""
+    import math
+    g = GoldenCase("edge3000_70x42")
+    cam = g.camera(0)
+    b = orc.preprocess_and_bin(g.act, cam, "precise", g.tau, g.sh_degree)
+    keys, vals = orc.sort_pairs(b.keys, b.values, b.grid_w * b.grid_h, g.act.count)
+    starts = orc.tile_range_table(keys, b.grid_w, b.grid_h)
+    got = orc.render_counts(b.splat, vals, starts, cam.width, cam.height, g.tau)
+    f32 = np.float32
+    tau = f32(g.tau)
+    want = dict(rect_rejected=0, cutoff_rejected=0, alpha_rejected=0, blended=0,
+                pairs_processed=0, pixels=0)
+    sp = b.splat
+    for t in range(b.grid_w * b.grid_h):
+        ty, tx = divmod(t, b.grid_w)
+        deepest = 0
+        for y in range(ty * 16, min(ty * 16 + 16, cam.height)):
+            for x in range(tx * 16, min(tx * 16 + 16, cam.width)):
+                fx, fy, T, seen = f32(x) + f32(0.5), f32(y) + f32(0.5), f32(1.0), 0
+                for i in range(int(starts[t]), int(starts[t + 1])):
+                    r = sp[vals[i]]
+                    seen += 1
+                    dx, dy = fx - r[0], fy - r[1]
+                    if abs(dx) > r[10] or abs(dy) > r[11]:
+                        want["rect_rejected"] += 1
+                        continue
+                    s = f32(0.5) * (r[2] * dx * dx + r[4] * dy * dy) + r[3] * dx * dy
+                    if s > f32(0.5) * r[6]:
+                        want["cutoff_rejected"] += 1
+                        continue
+                    al = min(f32(0.99), r[5] * f32(math.exp(-float(s))))
+                    if al < tau:
+                        want["alpha_rejected"] += 1
+                        continue
+                    want["blended"] += 1
+                    T = T * (f32(1.0) - al)
+                    if T < f32(1e-4):
+                        break
+                deepest = max(deepest, seen)
+                want["pixels"] += 1
+        want["pairs_processed"] += deepest
+    # exp here is float64-rounded, the oracle's is glibc expf: a verdict can only differ when
+    # alpha sits within an ulp of tau -- allow a handful of evaluations to change class
+    assert got["pixels"] == want["pixels"] == cam.width * cam.height
+    assert got["rect_rejected"] == want["rect_rejected"]
+    assert got["cutoff_rejected"] == want["cutoff_rejected"]
+    assert abs(got["alpha_rejected"] - want["alpha_rejected"]) <= 3
+    assert abs(got["blended"] - want["blended"]) <= 3
+    assert abs(got["pairs_processed"] - want["pairs_processed"]) <= 3
+    assert got["blended"] >= int(np.count_nonzero(g.contrib(0)))
