@@ -2,25 +2,42 @@
 """Benchmark of the rasterizer hot path (contract: see the task's bench.py rules).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-                    [--workload c1|c2|c3|c2-dense] [--mode views|bands]
+                    [--workload c4-4k|c1|c2|c2-dense|c3|c4|c5] [--mode views|bands]
 
-A *step* is one frame: one pass of preprocess -> emit -> sort -> ranges ->
-blend over one camera view of a synthetic scene that is already resident in
-HBM.  Default workload = BASELINE.json configs[1]: 1M Gaussians (generator
-`mixed`, seed 1, density-scaled per SURVEY.md 8(d)), SH degree 3, one
-1920x1080 view.  Metric = views/sec (whole job, all GPUs); ms/frame is
-`ms_per_step`.  With N > 1 (torchrun, one rank per GPU) every rank holds the
-whole scene and renders its own views -- independent units, no data-path
-collective ("scaling": "weak"); `--mode bands` instead splits ONE frame into
-tile-row bands and gathers them with NCCL.
+A *step* is one frame: one pass of preprocess -> tile scan -> emit -> tile sort ->
+blend over one camera view of a synthetic scene that is already resident in HBM.
+Default workload = the north-star frame of BASELINE.json: 10M Gaussians (generator
+`mixed`, seed 1, density-scaled per SURVEY.md 8(d)), SH degree 3, 3840x2160 -- the
+largest configuration the metric ("ms/frame at 1080p & 4K by Gaussian count") is quoted
+on that fits one GPU.  The line also carries a short run of configs[1] (1M Gaussians,
+1920x1080) under `also.c2`.  Metric = views/sec (whole job, all GPUs); `ms_per_step` is
+its inverse per GPU, `ms_per_frame` the latency of one frame issued alone.  The timed
+views are DISTINCT cameras of an orbit (16, or the 64 of configs[4]); with N > 1
+(torchrun, one rank per GPU) every rank holds the whole scene and renders its own views
+-- independent units, no data-path collective ("scaling": "weak"); `--mode bands`
+instead splits ONE frame into tile-row bands whose gather (NCCL) is inside the timed
+region.
 
-One JSON line is printed by rank 0.  `value` is device-timed (CUDA events per
-step, L2 flushed between steps); `e2e` is the same metric through the public
-API `Pipeline.render(camera)` with the frame read back to host memory every
-step; `roofline` is the dominant kernel, timed live with CUDA events recorded
-between the kernel launches of the timed steps; `cpu_baseline` is the CPU
-oracle (a C/OpenMP restatement of the reference algorithm, bit-identical to the
-reference on the golden vectors) on the same workload on this box's host cores.
+One JSON line is printed by rank 0.
+  value      device-timed: K views issued round-robin on 3 CUDA streams, one start event,
+             one end event per stream, longest span, max over ranks.  No L2 flush in this
+             pass: every view re-reads the packed scene (2.4 GB at 10M) and rewrites its
+             own workspace, all far larger than the 126 MB L2.
+  ms_per_frame / kernels / roofline
+             a separate pass, one frame (view 0) at a time with a 256 MiB buffer written
+             between frames (L2 flush, untimed), CUDA events recorded between the kernel
+             launches on the launch stream (fgs_profile_begin).
+  roofline   the longest kernel of the frame against the roof that bounds it: HBM
+             (MEASURED_PEAKS.json) for preprocess / emit / tile sort on algorithmic bytes,
+             FP32 (SMs x 128 lanes x 2 x clock) for the blend on the flops of the
+             reference loop's evaluations, counted by outcome on the device
+             (fgs_blend_counts, equal to the instrumented oracle loop: tests).
+             `rooflines` lists the same for every kernel of the frame.
+  e2e        the same metric through the public API with HOST frames out (float32
+             (H,W,3), pinned D2H inside the timed region): `Pipeline.render_iter` over the
+             views, and `e2e.render_call_*` for blocking `Pipeline.render(camera)` calls.
+  cpu_baseline  the CPU oracle (C/OpenMP restatement of the reference, bit-identical to it
+             on tests/golden) on the same view on this box's host cores.
 
 `--impl reference` times that CPU path alone (rank 0 only).
 """
@@ -58,7 +75,8 @@ WORKLOADS = {
            "BASELINE configs[4]: 64-view batch of a 3M-Gaussian scene (density-scaled), SH3, "
            "1920x1080, views sharded over the ranks"),
 }
-VIEWS = {"c5": 64}       # workloads that are a batch of distinct views (orbit cameras)
+VIEWS = {"c5": 64}       # workloads that are a batch of 64 distinct views (orbit cameras)
+DEFAULT_WORKLOAD = "c4-4k"
 METRIC, UNIT = "views_per_sec", "views/s"
 
 
@@ -168,8 +186,8 @@ def run_reference(args, rank):
         return
     import paper_2408_07967_b200.scene as scene_mod
     act, w, h, desc = make_scene(scene_mod, args.workload)
-    cam = scene_mod.orbit_cameras(1, 24.0, w, h)[0]
-    cb = cpu_arm(act, cam, args.steps, args.warmup, budget_s=150.0)
+    cam = scene_mod.orbit_cameras(1, 24.0, w, h)[0]           # view 0 of the orbit
+    cb = cpu_arm(act, cam, min(args.steps, 20), args.warmup, budget_s=120.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
         "n_gpus": args.gpus, "steps": cb["frames_timed"], "warmup": args.warmup,
@@ -182,19 +200,388 @@ def run_reference(args, rank):
     print(json.dumps(line), flush=True)
 
 
+NVIEWS_DEFAULT = 16      # distinct orbit views the timed steps cycle through
+
+
+def launches_per_frame(bucket, npass, tiles):
+    """Kernels of this library one frame launches (tile-bucket: preprocess, [slice totals on
+    grids above 12 K tiles], tile scan, tile order, place, four sort classes, blend)."""
+    if bucket:
+        return 10 + (1 if (tiles + 1023) // 1024 > 12 else 0)
+    return 6 + npass
+
+
+def measure(env, name, steps, warmup, args, with_cpu, short=False):
+    """All measurements of one workload on this rank; rank 0 returns the JSON record."""
+    torch, dist, fgs, _capi, sharding = env["torch"], env["dist"], env["fgs"], env["_capi"], env["sharding"]
+    dev, rank, world, local_rank = env["dev"], env["rank"], env["world"], env["local_rank"]
+    act, W, H, desc = make_scene(fgs, name)
+    P = act.count
+    nv_total = VIEWS.get(name, NVIEWS_DEFAULT)
+    cams = fgs.orbit_cameras(nv_total, 24.0, W, H)
+    bands_mode = args.mode == "bands"
+    cam0 = cams[0]                          # the "single view" of BASELINE's configs
+    my_ids = [0] if bands_mode else (sharding.views_for_rank(nv_total, world, rank) or [rank % nv_total])
+    my_cams = [cams[v] for v in my_ids]
+    gh, gw = -(-H // 16), -(-W // 16)
+
+    pipe = fgs.Pipeline(act, sort_mode=args.sort_mode,
+                        spatial_order=False if args.no_spatial else None)
+    L = _capi.lib()
+    hbm_peak, peak_src, sm_max = peaks()
+    props = torch.cuda.get_device_properties(dev)
+    sms = props.multi_processor_count
+
+    band, bands = None, sharding.band_partition(gh, world)
+    if bands_mode and world > 1:
+        if args.band_split == "balanced":
+            rw = pipe.row_weights(cam0)
+            bands = sharding.balanced_band_partition(rw, world, fixed_rows=0.3 * float(rw.mean()))
+        band = bands[rank]
+
+    # ---- warm-up through the public API (also sizes the workspace) -------------
+    pairs_by_view = []
+    for i in range(max(warmup, len(my_cams) if not short else 1)):
+        fb, st = pipe.render(my_cams[i % len(my_cams)], exact=args.exact, band=band)
+        pairs_by_view.append(st.pairs_emitted)
+    fb, st = pipe.render(cam0, exact=args.exact, band=band)
+    M, R = st.pairs_emitted, int(st.gaussians_retained)
+    del fb
+    stream = torch.cuda.current_stream(dev)
+    bucket = args.sort_mode == "tile-bucket"
+    nlanes = max(1, args.streams)
+    lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nlanes - 1)]
+    wss = []
+    for _ in range(nlanes):
+        w_ = pipe._take_ws(torch, W, H, pipe._default_capacity())
+        w_.set_mode(_capi.SORT_MODES[args.sort_mode])
+        wss.append(w_)
+    lay = wss[0].lay
+    T_tiles = int(lay.tiles)
+    npass = 0 if bucket else int(lay.sort_passes)
+    n_marks = 8 if bucket else 6 + npass
+    camcs = [_capi.camera_struct(c) for c in my_cams]
+    cam0c = _capi.camera_struct(cam0)
+    kcut = pipe._cutoffs(torch, 1.0 / 255.0)
+    bg = (C.c_float * 3)(0.0, 0.0, 0.0)
+    flags = (_capi.BLEND_EXACT if args.exact else 0) | _capi.BLEND_CONTRIB
+    b0, b1 = band if band is not None else (0, gh - 1)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
+
+    def frame(lane=0, camc=cam0c):
+        w_ = wss[lane]
+        _capi.check(L.fgs_render(pipe.packed.data_ptr(), kcut.data_ptr(), P, C.byref(camc),
+                                 1.0 / 255.0, 3, 0, bg, flags, b0, b1, w_.next_epoch(),
+                                 w_.rgb.data_ptr(), None, None, C.c_void_p(w_.base),
+                                 C.byref(w_.lay), C.c_void_p(lanes[lane].cuda_stream)))
+
+    for i in range(max(warmup, 2 * nlanes)):
+        frame(i % nlanes, camcs[i % len(camcs)])
+    torch.cuda.synchronize(dev)
+
+    # ---- pass A: view 0, one frame at a time, per-kernel CUDA events -------------
+    KA = min(steps, 12 if short else 30)
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(KA)]
+    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(n_marks)] for _ in range(KA)]
+    for e in ev0:
+        e.record(stream)               # materialise the handles
+    for row in marks:
+        for e in row:
+            e.record(stream)
+    handles = [(C.c_void_p * n_marks)(*[e.cuda_event for e in row]) for row in marks]
+    torch.cuda.synchronize(dev)
+    for i in range(KA):
+        flush.fill_(i & 0xff)          # evict L2 between frames (not timed)
+        ev0[i].record(stream)
+        L.fgs_profile_begin(handles[i], n_marks)
+        frame(0)
+        got = L.fgs_profile_end()
+        assert got == n_marks, (got, n_marks)
+    torch.cuda.synchronize(dev)
+    lat_prof_ms = np.array([ev0[i].elapsed_time(marks[i][-1]) for i in range(KA)])
+    # the same, without the per-kernel events: kernels then chain by programmatic dependent
+    # launch and the sort size classes overlap, so this -- not the sum of the kernels -- is
+    # the latency of a frame
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(KA)]
+    eve = [torch.cuda.Event(enable_timing=True) for _ in range(KA)]
+    for i in range(KA):
+        flush.fill_(i & 0xff)
+        evs[i].record(stream)
+        frame(0)
+        eve[i].record(stream)
+    torch.cuda.synchronize(dev)
+    lat_ms = np.array([evs[i].elapsed_time(eve[i]) for i in range(KA)])
+    kern = np.zeros((KA, n_marks))
+    for i in range(KA):
+        prev = ev0[i]
+        for j in range(n_marks):
+            kern[i, j] = prev.elapsed_time(marks[i][j])
+            prev = marks[i][j]
+
+    # ---- pass B: the timed steps.  K frames over this rank's DISTINCT views, round-robin
+    # over `nlanes` streams (each with its own workspace) so consecutive views overlap on the
+    # GPU, exactly like the public batch API.  Bands: every step is the rank's band of the
+    # one frame followed by the gather on rank 0 (NCCL send/recv), all inside the timed region.
+    K = steps
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_ends = [torch.cuda.Event(enable_timing=True) for _ in range(nlanes)]
+    gather_ms = None
+    full_frame = None
+    if bands_mode and world > 1:
+        full_frame = torch.empty((H, W, 3), dtype=torch.float32, device=dev) if rank == 0 else None
+        for _ in range(2):
+            pipe.render_bands(cam0, dist, bands=bands, out=full_frame, exact=args.exact, as_numpy=False)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    torch.cuda.synchronize(dev)
+    t_wall0 = time.perf_counter()
+    t_begin.record(stream)
+    if bands_mode and world > 1:
+        for i in range(K):
+            pipe.render_bands(cam0, dist, bands=bands, out=full_frame, exact=args.exact,
+                              as_numpy=False, sync=False)
+        t_ends[0].record(stream)
+        t_ends = t_ends[:1]
+    else:
+        for ln in lanes[1:]:
+            ln.wait_event(t_begin)
+        for i in range(K):
+            frame(i % nlanes, camcs[i % len(camcs)])
+        for ln, e in zip(lanes, t_ends):
+            e.record(ln)
+    torch.cuda.synchronize(dev)
+    t_wall = time.perf_counter() - t_wall0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    total_ms = max(t_begin.elapsed_time(e) for e in t_ends)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / K
+    views_per_step = 1 if bands_mode else world
+    value = views_per_step * K / (total_ms / 1e3)
+
+    # ---- end to end through the public API (host frame out every step) -----------
+    if band is None:
+        for fb, _ in pipe.render_iter([my_cams[i % len(my_cams)] for i in range(8)],
+                                      exact=args.exact, streams=nlanes):   # warm the pinned pool
+            pass
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    Ke = K if not short else min(K, 32)
+    t0 = time.perf_counter()
+    if band is None:
+        # the batch call a views/s user makes: the views through Pipeline.render_iter
+        # (frame i's read-back overlaps frame i+1's kernels)
+        nfr = 0
+        for fb, st_e in pipe.render_iter([my_cams[i % len(my_cams)] for i in range(Ke)],
+                                         exact=args.exact, streams=nlanes):
+            assert fb.image.shape == (H, W, 3) and isinstance(fb.image, np.ndarray)   # host frame
+            nfr += 1
+        assert nfr == Ke
+    else:
+        for _ in range(Ke):
+            fbb, _ = pipe.render_bands(cam0, dist, bands=bands, exact=args.exact)   # host frame on rank 0
+            assert rank != 0 or fbb.image.shape == (H, W, 3)
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = views_per_step * Ke / e2e_s
+    # the reference's own entry point, one blocking call per view: Pipeline.render(camera)
+    nsingle = min(K, 10 if short else 20)
+    render_call = {}
+    if band is None:
+        for key, kw in (("float32", {}), ("quantized", {"quantized": True})):
+            pipe.render(my_cams[0], exact=args.exact, timing=False, **kw)
+            t1 = time.perf_counter()
+            for i in range(nsingle):
+                pipe.render(my_cams[i % len(my_cams)], exact=args.exact, timing=False, **kw)
+            render_call[key] = (time.perf_counter() - t1) / nsingle * 1e3
+
+    if rank != 0:
+        return None
+
+    # ---- per-kernel records and rooflines ------------------------------------------
+    if bucket:
+        # launch order of the size classes: persistent kernels first (fgs_launch_tile_sort)
+        names = ["preprocess", "scan", "emit", "tile_sort_medium", "tile_sort_large",
+                 "tile_sort", "tile_sort_tail", "blend"]
+    else:
+        names = ["preprocess", "scan", "emit", "sort_hist"] \
+            + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
+    kmean = kern.mean(axis=0)
+    ncu_name = {"preprocess": "k_preprocess", "scan": "k_scan_tiles", "emit": "k_place",
+                "tile_sort": "k_tile_sort", "tile_sort_medium": "k_tile_sort_medium",
+                "tile_sort_large": "k_tile_sort_large", "tile_sort_tail": "k_tile_sort_tail",
+                "blend": "k_blend" if args.exact else "k_blend2"}
+    prof_all = profiled_kernels(name)
+    kernels = []
+    for nme, ms in zip(names, kmean):
+        ent = {"name": nme, "ms": float(ms), "share": float(ms / kmean.sum())}
+        for k, v in prof_all.items():
+            if isinstance(v, dict) and k.split("<")[0] == ncu_name.get(nme):
+                ent["ncu_dram_bytes"] = v["dram_bytes"]
+                ent["ncu_issue_slots_busy_pct"] = v.get("issue_slots_busy_pct")
+        kernels.append(ent)
+
+    # evaluation counts of the compositing loop for this view (device pass, untimed; equal
+    # to the instrumented oracle loop -- tests/test_gpu_parity.py)
+    evals = fgs.blend_eval_counts(pipe, cam0) if band is None else None
+    M_proc = evals["pairs_processed"] if evals else M
+    # algorithmic bytes per launch (SURVEY.md 8(d); DESIGN.md section 1)
+    alg = {
+        "preprocess": 236.0 * P + 52.0 * R,
+        # bucket: rect + mask + depth + count + index in, 8 B record out; onesweep: 12 B pair out
+        "emit": 8.0 * M + 24.0 * P if bucket else 12.0 * M + 4.0 * P,
+        "tile_sort_all": 12.0 * M,          # 8 B record in, 4 B index out, all four classes
+        "sort_pass": 24.0 * M,
+        "blend": 52.0 * M_proc + 12.0 * W * H,
+    }
+    ms_of = {"preprocess": float(kmean[0]), "emit": float(kmean[2]), "blend": float(kmean[-1])}
+    if bucket:
+        ms_of["tile_sort_all"] = float(kmean[3:-1].sum())
+    else:
+        ms_of["sort_pass"] = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass"))) / max(npass, 1)
+    clock_mhz = float(props.clock_rate) / 1e3 if getattr(props, "clock_rate", 0) else sm_max
+    fp32_peak = sms * 128 * 2 * sm_max * 1e6 / 1e12            # TFLOP/s at the max SM clock
+    kname = {"preprocess": "k_preprocess", "emit": "k_place" if bucket else "k_emit",
+             "tile_sort_all": "k_tile_sort{,_medium,_large,_tail}", "sort_pass": "k_sort_pass",
+             "blend": ncu_name["blend"]}
+
+    def roof_of(key):
+        ms = ms_of[key]
+        hit = [v for k, v in prof_all.items()
+               if isinstance(v, dict) and k.split("<")[0] == kname[key]]
+        if key == "blend" and evals is not None:
+            ach = evals["flops"] / (ms * 1e-3) / 1e12
+            r = {"kernel": kname[key], "bound": "fp32", "achieved": ach, "peak": fp32_peak,
+                 "unit": "TFLOP/s", "frac": ach / fp32_peak, "traffic": None,
+                 "launches_per_step": 1, "ms_per_launch": ms,
+                 "flops_per_launch": evals["flops"],
+                 "evaluations": {k: evals[k] for k in fgs.EVAL_FLOPS},
+                 "flops_per_evaluation": dict(fgs.EVAL_FLOPS),
+                 "pairs_processed": M_proc, "alg_bytes_per_launch": alg["blend"],
+                 "hbm_view_gbs": alg["blend"] / (ms * 1e-3) / 1e9,
+                 "peak_source": f"{sms} SMs x 128 FP32 lanes x 2 x {sm_max:.0f} MHz (max SM clock)",
+                 "note": "flops = the reference loop's own operations per (pixel, pair) evaluation "
+                         "(render.py:106-129: 6 / 16 / 21 / 31 by outcome), counted on the device; the "
+                         "kernel culls pairs per 8x8 block and evaluates two pixels per packed "
+                         "instruction, so it executes fewer instructions than that count implies"}
+            if hit:
+                inst = hit[0]["warp_instructions"]
+                peak_issue = 4.0 * sms * (clocks.get("sm_mhz") or sm_max) * 1e6
+                r["issue"] = {"warp_instructions_per_launch": inst,
+                              "achieved_ginst_s": inst / (ms * 1e-3) / 1e9,
+                              "peak_ginst_s": peak_issue / 1e9, "frac": inst / (ms * 1e-3) / peak_issue,
+                              "ncu_issue_slots_busy_pct": hit[0].get("issue_slots_busy_pct"),
+                              "ncu_fma_pipe_busy_pct": hit[0].get("fma_pipe_busy_pct"),
+                              "ncu_alu_pipe_busy_pct": hit[0].get("alu_pipe_busy_pct"),
+                              "ncu_xu_pipe_busy_pct": hit[0].get("xu_pipe_busy_pct")}
+        else:
+            ach = alg[key] / (ms * 1e-3) / 1e9
+            r = {"kernel": kname[key], "bound": "hbm", "achieved": ach, "peak": hbm_peak,
+                 "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
+                 "launches_per_step": {"tile_sort_all": 4, "sort_pass": npass}.get(key, 1),
+                 "ms_per_launch": ms, "alg_bytes_per_launch": alg[key], "peak_source": peak_src}
+        if hit:
+            r["traffic"] = hit[0]["dram_bytes"]
+            r["traffic_source"] = prof_all.get("_file")
+        return r
+
+    rooflines = {k: roof_of(k) for k in ms_of}
+    dom = max(ms_of, key=lambda k: ms_of[k] * ({"sort_pass": npass}.get(k, 1)))
+    roof = rooflines[dom]
+    for ent in kernels:
+        key = ent["name"]
+        if key in rooflines and key != "blend":
+            ent["alg_bytes"], ent["gbs"], ent["frac_hbm"] = alg[key], rooflines[key]["achieved"], rooflines[key]["frac"]
+        elif key == "blend":
+            ent["alg_bytes"], ent["frac_fp32"] = alg["blend"], rooflines["blend"]["frac"] if evals else None
+    if bucket:
+        kernels.append({"name": "tile_sort_all", "ms": ms_of["tile_sort_all"],
+                        "share": float(ms_of["tile_sort_all"] / kmean.sum()),
+                        "alg_bytes": alg["tile_sort_all"], "gbs": rooflines["tile_sort_all"]["achieved"],
+                        "frac_hbm": rooflines["tile_sort_all"]["frac"],
+                        "note": "sum of the four size-class launches"})
+
+    cpu = cpu_arm(act, cam0, 3, 1, budget_s=25.0) if with_cpu else None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": warmup, "ms_per_step": ms_per_step, "ms_per_frame": float(lat_ms.mean()),
+        "higher_is_better": True,
+        "scaling": "weak" if not bands_mode else "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": desc, "mode": args.mode,
+                   "band_split": (args.band_split if bands_mode else None), "strategy": "precise",
+                   "tau": 1.0 / 255.0, "sh_degree": 3, "gaussians": P, "width": W, "height": H,
+                   "pairs": M, "pairs_processed": M_proc, "retained": R, "tiles": T_tiles,
+                   "sort_mode": args.sort_mode, "sort_passes": npass,
+                   "blend": "exact" if args.exact else "ex2.approx+guard",
+                   "streams": nlanes,
+                   "distinct_views": 1 if bands_mode else len(my_cams) * world,
+                   "views": "orbit_cameras(%d, 24.0, %d, %d); rank r times views r, r+N, ...; "
+                            "kernels / roofline / cpu_baseline are view 0" % (nv_total, W, H),
+                   "pairs_by_view": {"min": int(min(pairs_by_view)), "max": int(max(pairs_by_view))},
+                   "l2": "timed steps: inputs larger than L2 -- every view re-reads the %d MB "
+                         "packed scene and rewrites its own workspace, %d views in flight, 126 MB "
+                         "L2, no flush; latency / per-kernel pass: 256 MiB buffer written between "
+                         "frames (flush, untimed)" % (pipe.scene_bytes >> 20, nlanes),
+                   "timing": "CUDA events on the launch streams: one start event, one end event "
+                             "per stream, longest span; max over ranks"},
+        "clocks": clocks,
+        "frame_latency_ms": float(lat_ms.mean()),
+        "frame_latency_profiled_ms": float(lat_prof_ms.mean()),
+        "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / Ke * 1e3, "steps": Ke,
+                "h2d_bytes_per_step": C.sizeof(_capi.FgsCamera) + 12,
+                "d2h_bytes_per_step": W * H * 12 + 64,
+                "d2h_floor_ms": (W * H * 12) / 55e9 * 1e3,
+                "api": ("Pipeline.render_iter(cameras) -> per view a host numpy float32 frame "
+                        "(pinned D2H behind the view's kernels on its stream; views round-robin "
+                        "on %d streams) + FrameStats" % nlanes) if band is None else
+                       "Pipeline.render_bands(camera, dist) -> host frame on rank 0",
+                "render_call_ms": render_call.get("float32"),
+                "render_call_quantized_ms": render_call.get("quantized"),
+                "render_call_api": "blocking Pipeline.render(camera) per view (the reference's entry "
+                                   "point): float32 host frame / uint8 host frame"},
+        "gpu_launches": int(launches_per_frame(bucket, npass, T_tiles) * K),
+        "roofline": roof,
+        "rooflines": rooflines,
+        "cpu_baseline": cpu,
+        "kernels": kernels,
+        "kernels_note": "per-kernel times are from the one-frame-at-a-time pass (%d frames of view "
+                        "0, L2 flushed between frames); `value` overlaps consecutive views" % KA,
+        "stage_ms": {"preprocess_bin": float(kmean[0:3].sum()),
+                     "sort": float(kmean[3:-1].sum()), "render": float(kmean[-1])},
+        "wall_s_timed_region": t_wall,
+    }
+    del wss, pipe, flush
+    torch.cuda.empty_cache()
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS))
     ap.add_argument("--mode", default="views", choices=["views", "bands"])
     ap.add_argument("--band-split", default="balanced", choices=["balanced", "equal"],
                     help="--mode bands: bands of equal estimated work (default) or equal height")
     ap.add_argument("--exact", action="store_true", help="bit-exact blend mode")
     ap.add_argument("--sort-mode", default="tile-bucket", choices=["tile-bucket", "onesweep"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-also", action="store_true", help="skip the extra configs[1] run")
     ap.add_argument("--no-spatial", action="store_true",
                     help="keep the scene in the caller's order (no Morton slot order)")
     ap.add_argument("--streams", type=int, default=3,
@@ -221,331 +608,22 @@ def main():
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+    env = dict(torch=torch, dist=dist, fgs=fgs, _capi=_capi, sharding=sharding, dev=dev,
+               rank=rank, world=world, local_rank=local_rank)
 
-    act, W, H, desc = make_scene(fgs, args.workload)
-    P = act.count
-    nviews = VIEWS.get(args.workload, 0)
-    ncam = nviews if nviews else max(world, 1)
-    cams = fgs.orbit_cameras(ncam, 24.0, W, H)
-    cam = cams[0] if args.mode == "bands" else cams[rank % ncam]
-    # a view batch: this rank's share of the views (view v -> rank v mod world), cycled
-    my_cams = [cams[v] for v in sharding.views_for_rank(ncam, world, rank)] if nviews else [cam]
-    gh = -(-H // 16)
-    gw = -(-W // 16)
-    band = None
-    bands = sharding.band_partition(gh, world)
-    if args.mode == "bands" and world > 1:
-        band = bands[rank]
-
-    pipe = fgs.Pipeline(act, sort_mode=args.sort_mode,
-                        spatial_order=False if args.no_spatial else None)
-    if args.mode == "bands" and world > 1 and args.band_split == "balanced":
-        # work-balanced bands: every rank derives the same edges from the same integer
-        # row histogram (no communication); the frame does not depend on the cut
-        rw = pipe.row_weights(cam)
-        bands = sharding.balanced_band_partition(rw, world, fixed_rows=0.3 * float(rw.mean()))
-        band = bands[rank]
-    L = _capi.lib()
-    hbm_peak, peak_src, sm_max = peaks()
-
-    # ---- warm-up through the public API (also sizes the workspace) -------------
-    for _ in range(args.warmup):
-        fb, st = pipe.render(cam, exact=args.exact, band=band)
-    M = st.pairs_emitted
-    stream = torch.cuda.current_stream(dev)
-    bucket = args.sort_mode == "tile-bucket"
-    nlanes = max(1, args.streams)
-    lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nlanes - 1)]
-    wss = []
-    for _ in range(nlanes):
-        w_ = pipe._take_ws(torch, W, H, pipe._default_capacity())
-        w_.set_mode(_capi.SORT_MODES[args.sort_mode])
-        wss.append(w_)
-    ws = wss[0]
-    lay = ws.lay
-    npass = 0 if bucket else int(lay.sort_passes)
-    # kernels per frame: bucket  K1 K2 K3 tile_sort(small, medium, large, tail) K6 ;
-    #                     onesweep  K1 K2 K3 hist pass*npass K5 K6
-    n_marks = 8 if bucket else 6 + npass
-    camcs = [_capi.camera_struct(c) for c in my_cams]
-    kcut = pipe._cutoffs(torch, 1.0 / 255.0)
-    bg = (C.c_float * 3)(0.0, 0.0, 0.0)
-    flags = (_capi.BLEND_EXACT if args.exact else 0) | _capi.BLEND_CONTRIB
-    b0, b1 = band if band is not None else (0, gh - 1)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)      # > 126 MB L2
-
-    def frame(lane=0, view=0):
-        w_ = wss[lane]
-        _capi.check(L.fgs_render(pipe.packed.data_ptr(), kcut.data_ptr(), P,
-                                 C.byref(camcs[view % len(camcs)]),
-                                 1.0 / 255.0, 3, 0, bg, flags, b0, b1, w_.next_epoch(),
-                                 w_.rgb.data_ptr(), None, None, C.c_void_p(w_.base),
-                                 C.byref(w_.lay), C.c_void_p(lanes[lane].cuda_stream)))
-
-    for i in range(max(args.warmup, 2 * nlanes)):
-        frame(i % nlanes, i)
-    torch.cuda.synchronize(dev)
-
-    # ---- pass A: one frame at a time, per-kernel CUDA events (latency + roofline) --
-    KA = min(args.steps, 30)
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(KA)]
-    marks = [[torch.cuda.Event(enable_timing=True) for _ in range(n_marks)] for _ in range(KA)]
-    for e in ev0:
-        e.record(stream)               # materialise the handles
-    for row in marks:
-        for e in row:
-            e.record(stream)
-    handles = [(C.c_void_p * n_marks)(*[e.cuda_event for e in row]) for row in marks]
-    torch.cuda.synchronize(dev)
-    for i in range(KA):
-        flush.fill_(i & 0xff)          # evict L2 between frames (not timed)
-        ev0[i].record(stream)
-        L.fgs_profile_begin(handles[i], n_marks)
-        frame(0)
-        got = L.fgs_profile_end()
-        assert got == n_marks, (got, n_marks)
-    torch.cuda.synchronize(dev)
-    lat_prof_ms = np.array([ev0[i].elapsed_time(marks[i][-1]) for i in range(KA)])
-    # the same, without the per-kernel events: the sort size classes then overlap
-    # (programmatic dependent launch), so this -- not the sum of the kernels -- is the latency
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(KA)]
-    eve = [torch.cuda.Event(enable_timing=True) for _ in range(KA)]
-    for i in range(KA):
-        flush.fill_(i & 0xff)
-        evs[i].record(stream)
-        frame(0)
-        eve[i].record(stream)
-    torch.cuda.synchronize(dev)
-    lat_ms = np.array([evs[i].elapsed_time(eve[i]) for i in range(KA)])
-    kern = np.zeros((KA, n_marks))
-    for i in range(KA):
-        prev = ev0[i]
-        for j in range(n_marks):
-            kern[i, j] = prev.elapsed_time(marks[i][j])
-            prev = marks[i][j]
-
-    # ---- pass B: the timed steps.  K frames, round-robin over `nlanes` streams (each
-    # with its own workspace) so consecutive views overlap on the GPU, exactly like the
-    # public batch API.  Timed on the device from one start event to the last lane's end.
-    K = args.steps
-    t_begin = torch.cuda.Event(enable_timing=True)
-    t_ends = [torch.cuda.Event(enable_timing=True) for _ in range(nlanes)]
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    torch.cuda.synchronize(dev)
-    t_wall0 = time.perf_counter()
-    t_begin.record(stream)
-    for ln in lanes[1:]:
-        ln.wait_event(t_begin)
-    for i in range(K):
-        frame(i % nlanes, i)
-    for ln, e in zip(lanes, t_ends):
-        e.record(ln)
-    torch.cuda.synchronize(dev)
-    t_wall = time.perf_counter() - t_wall0
-    if world > 1:
-        dist.barrier()
-    clocks = sampler.stop()
-    total_ms = max(t_begin.elapsed_time(e) for e in t_ends)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / K
-    views_per_step = 1 if (args.mode == "bands") else world
-    value = views_per_step * K / (total_ms / 1e3)
-
-    # ---- end to end through the public API (host frame out every step) -----------
-    if band is None:
-        for fb, _ in pipe.render_iter([cam] * 8, exact=args.exact, streams=nlanes):   # warm the pinned pool
-            pass
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    t0 = time.perf_counter()
-    if band is None:
-        # the batch call a views/s user makes: K views through Pipeline.render_many
-        # (frame i's read-back overlaps frame i+1's kernels)
-        nfr = 0
-        for fb, st_e in pipe.render_iter([my_cams[i % len(my_cams)] for i in range(K)],
-                                         exact=args.exact, streams=nlanes):
-            assert fb.image.shape == (H, W, 3)      # frame is in host memory here
-            nfr += 1
-        assert nfr == K
-    else:
-        for _ in range(K):
-            fb, st_e = pipe.render(cam, exact=args.exact, band=band, timing=False)
-            assert fb.image.shape == (H, W, 3)
-    e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = views_per_step * K / e2e_s
-    # latency of one blocking Pipeline.render(camera) call, for reference
-    t1 = time.perf_counter()
-    for _ in range(min(K, 10)):
-        pipe.render(cam, exact=args.exact, band=band, timing=False)
-    single_ms = (time.perf_counter() - t1) / min(K, 10) * 1e3
-
-    # bands: gather the bands on rank 0 with NCCL send/recv (reported separately)
-    gather_ms = None
-    if args.mode == "bands" and world > 1:
-        y0, y1 = sharding.band_pixel_rows(band, H)
-        mine = ws.rgb[y0:y1].contiguous()
-        torch.cuda.synchronize(dev)
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        g0.record()
-        sharding.gather_bands(mine, bands, H, dist, rank, 0)
-        g1.record()
-        torch.cuda.synchronize(dev)
-        gather_ms = g0.elapsed_time(g1)
-
+    line = measure(env, args.workload, args.steps, args.warmup, args,
+                   with_cpu=not args.no_cpu and world == 1)
+    if args.workload == DEFAULT_WORKLOAD and args.mode == "views" and not args.no_also:
+        # BASELINE configs[1] beside the headline, short: value, latency, e2e, kernels
+        c2 = measure(env, "c2", min(args.steps, 64), 3, args, with_cpu=False, short=True)
+        if rank == 0:
+            keep = ("value", "unit", "ms_per_step", "ms_per_frame", "e2e", "kernels", "roofline",
+                    "rooflines", "stage_ms", "steps")
+            line["also"] = {"c2": dict({k: c2[k] for k in keep},
+                                       workload=c2["config"]["workload"], pairs=c2["config"]["pairs"],
+                                       pairs_processed=c2["config"]["pairs_processed"],
+                                       distinct_views=c2["config"]["distinct_views"])}
     if rank == 0:
-        if bucket:
-            # launch order of the size classes: persistent kernels first (fgs_launch_tile_sort)
-            names = ["preprocess", "scan", "emit", "tile_sort_medium", "tile_sort_large",
-                     "tile_sort", "tile_sort_tail", "blend"]
-        else:
-            names = ["preprocess", "scan", "emit", "sort_hist"] \
-                + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
-        kmean = kern.mean(axis=0)
-        R = int(st.gaussians_retained)
-        T_tiles = int(lay.tiles)
-        # algorithmic bytes per launch (packed scene reads 240+4 B/Gaussian)
-        alg = {
-            "preprocess": 236.0 * P + 52.0 * R,
-            # bucket: rect + mask + depth + count in, 8 B record out; onesweep: 12 B pair out
-            "emit": 8.0 * M + 24.0 * P if bucket else 12.0 * M + 4.0 * P,
-            "tile_sort": 12.0 * M,          # 8 B record in, 4 B index out
-            "sort_hist": 8.0 * M,
-            "ranges": 8.0 * M + 4.0 * (T_tiles + 1),
-            "blend": 52.0 * M + 12.0 * W * H,
-        }
-        for p_ in range(npass):
-            alg[f"sort_pass{p_}"] = 24.0 * M
-        kernels = []
-        for nme, ms in zip(names, kmean):
-            ent = {"name": nme, "ms": float(ms), "share": float(ms / kmean.sum())}
-            if nme in alg and ms > 0:
-                ent["alg_bytes"] = alg[nme]
-                ent["gbs"] = alg[nme] / (ms * 1e-3) / 1e9
-                ent["frac_hbm"] = ent["gbs"] / hbm_peak
-            kernels.append(ent)
-        ncu_name = {"preprocess": "k_preprocess", "scan": "k_scan_tiles", "emit": "k_place",
-                    "tile_sort": "k_tile_sort", "tile_sort_medium": "k_tile_sort_medium",
-                    "tile_sort_large": "k_tile_sort_large", "tile_sort_tail": "k_tile_sort_tail",
-                    "blend": "k_blend" if args.exact else "k_blend2"}
-        prof_all = profiled_kernels(args.workload)
-        for ent in kernels:
-            for k, v in prof_all.items():
-                if isinstance(v, dict) and k.split("<")[0] == ncu_name.get(ent["name"]):
-                    ent["ncu_dram_bytes"] = v["dram_bytes"]
-                    ent["ncu_issue_slots_busy_pct"] = v.get("issue_slots_busy_pct")
-        # dominant kernel: sort passes are launches of ONE kernel -> judged together
-        sort_ms = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass")))
-        cand = {"blend": kmean[-1], "sort_pass": sort_ms, "preprocess": kmean[0], "emit": kmean[2]}
-        if bucket:
-            cand["tile_sort"] = float(kmean[3:-1].sum())
-        dom = max(cand, key=cand.get)
-        if dom == "sort_pass":
-            per_launch_ms = sort_ms / npass
-            ach = 24.0 * M / (per_launch_ms * 1e-3) / 1e9
-            roof = {"kernel": "k_sort_pass", "bound": "hbm", "achieved": ach, "peak": hbm_peak,
-                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                    "launches_per_step": npass, "ms_per_launch": per_launch_ms,
-                    "alg_bytes_per_launch": 24.0 * M}
-        elif dom == "blend":
-            # FP32-pipe bound (no dense contraction -> no tensor cores): also report the
-            # HBM view so the schema's fields are filled; `fp32` carries the pipe estimate.
-            ms = float(kmean[-1])
-            ach = alg["blend"] / (ms * 1e-3) / 1e9
-            roof = {"kernel": ncu_name["blend"], "bound": "hbm", "achieved": ach, "peak": hbm_peak,
-                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                    "launches_per_step": 1, "ms_per_launch": ms,
-                    "alg_bytes_per_launch": alg["blend"],
-                    "note": "blend is bound by FP32/ALU instruction issue, not by HBM: `issue` carries "
-                            "the warp-instruction rate against 4 schedulers x SMs x clock and the ncu "
-                            "pipe utilisations (packed FFMA2/FMUL2/FADD2 on the FMA pipe)"}
-        else:
-            idx = {"preprocess": 0, "emit": 2, "tile_sort": 3}[dom]
-            ms = float(kmean[3:-1].sum() if dom == "tile_sort" else kmean[idx])
-            ach = alg[dom] / (ms * 1e-3) / 1e9
-            roof = {"kernel": "k_" + dom, "bound": "hbm", "achieved": ach, "peak": hbm_peak,
-                    "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                    "launches_per_step": 4 if dom == "tile_sort" else 1, "ms_per_launch": ms,
-                    "alg_bytes_per_launch": alg[dom]}
-        roof["peak_source"] = peak_src
-        # traffic / instruction counts of the same kernel from the committed ncu capture of
-        # this workload (profiles/*_traffic.json, written by profiles/extract_traffic.py)
-        prof = profiled_kernels(args.workload)
-        hit = [v for k, v in prof.items() if isinstance(v, dict) and k.split("<")[0] == roof["kernel"]]
-        if hit:
-            roof["traffic"] = hit[0]["dram_bytes"]
-            roof["traffic_source"] = prof.get("_file")
-            if roof["kernel"].startswith("k_blend"):
-                # the bound that applies: warp-instruction issue (4 schedulers x SMs x clock)
-                inst = hit[0]["warp_instructions"]
-                peak_issue = 4.0 * torch.cuda.get_device_properties(dev).multi_processor_count \
-                    * (clocks.get("sm_mhz") or sm_max) * 1e6
-                ach = inst / (roof["ms_per_launch"] * 1e-3)
-                roof["issue"] = {"warp_instructions_per_launch": inst, "achieved_ginst_s": ach / 1e9,
-                                 "peak_ginst_s": peak_issue / 1e9, "frac": ach / peak_issue,
-                                 "ncu_issue_slots_busy_pct": hit[0].get("issue_slots_busy_pct"),
-                                 "ncu_fma_pipe_busy_pct": hit[0].get("fma_pipe_busy_pct"),
-                                 "ncu_alu_pipe_busy_pct": hit[0].get("alu_pipe_busy_pct"),
-                                 "ncu_xu_pipe_busy_pct": hit[0].get("xu_pipe_busy_pct")}
-
-        cpu = None
-        if not args.no_cpu and world == 1:
-            cpu = cpu_arm(act, cam, 3, 1, budget_s=25.0)
-
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak" if args.mode == "views" else "strong",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": desc, "mode": args.mode, "band_split": (args.band_split if args.mode == "bands" else None), "strategy": "precise",
-                       "tau": 1.0 / 255.0, "sh_degree": 3, "gaussians": P, "width": W, "height": H,
-                       "pairs": M, "retained": R, "tiles": T_tiles, "sort_mode": args.sort_mode,
-                       "sort_passes": npass,
-                       "blend": "exact" if args.exact else "ex2.approx+guard",
-                       "streams": nlanes, "distinct_views": len(my_cams) * (world if nviews else 1),
-                       "l2": "timed steps: inputs larger than L2 -- every view re-reads the 240 MB "
-                             "packed scene and rewrites its own ~150 MB workspace, %d views in "
-                             "flight, 126 MB L2; latency/roofline pass: 256 MiB buffer written "
-                             "between frames (flush, untimed)" % nlanes,
-                       "timing": "CUDA events on the launch streams: one start event, one end event "
-                                 "per stream, longest span; max over ranks"},
-            "clocks": clocks,
-            "frame_latency_ms": float(lat_ms.mean()),
-            "frame_latency_profiled_ms": float(lat_prof_ms.mean()),
-            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_s / K * 1e3,
-                    "h2d_bytes_per_step": C.sizeof(_capi.FgsCamera) + 12,
-                    "d2h_bytes_per_step": W * H * 12 + 64,
-                    "api": "Pipeline.render_iter(cameras) -> per view a host numpy frame (pinned "
-                           "D2H behind the view's kernels on its stream; views round-robin on "
-                           "%d streams) + FrameStats" % nlanes,
-                    "single_call_ms": single_ms},
-            # kernels of this library launched inside the timed region: the profiling marks
-            # (one per stage kernel) + k_tile_order, which shares the emit stage's mark
-            # and, on grids above 12 slices of 1024 tiles, k_tile_blocksums (scan stage's mark)
-            "gpu_launches": int((n_marks + (1 if bucket else 0)
-                                 + (1 if bucket and (gw * gh + 1023) // 1024 > 12 else 0)) * K),
-            "roofline": roof,
-            "cpu_baseline": cpu,
-            "kernels": kernels,
-            "kernels_note": "per-kernel times are from the one-frame-at-a-time pass (%d frames, L2 "
-                            "flushed between frames); `value` overlaps consecutive views" % KA,
-            "stage_ms": {"preprocess_bin": float(kmean[0:3].sum()),
-                         "sort": float(kmean[3:-1].sum()), "render": float(kmean[-1])},
-            "wall_s_timed_region": t_wall,
-        }
-        if gather_ms is not None:
-            line["band_gather_ms"] = gather_ms
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

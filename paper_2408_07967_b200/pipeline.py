@@ -82,6 +82,8 @@ class Framebuffer:
     background: np.ndarray         # (3,) float32
     alpha: object = None           # (H, W) = 1 - T_final           (extras=True)
     depth: object = None           # (H, W) = sum blend weight * z  (extras=True)
+    rows: tuple = None             # pixel rows [y0, y1) of the frame the arrays hold
+                                   # (the whole frame unless a band was rendered)
 
     @property
     def width(self) -> int:
@@ -165,12 +167,21 @@ class _Workspace:
         self.depthmap = None
         self.rgb8 = None               # (H, W, 3) uint8, allocated on first quantized render
         self.h_stats = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+        self.h_stats_np = self.h_stats.numpy().view(_capi.STATS_DTYPE)   # same pinned bytes
+        self.kcut_ptr = None
+        self._events = None
         self.epoch = 1
         _capi.check(_capi.lib().fgs_workspace_init(C.c_void_p(self.base), C.byref(self.lay),
                                                    _stream_ptr(torch, device)))
         # The workspace may be used on another stream next (render_iter's lanes): its
         # initialisation must not still be running then.  Creation is rare; wait here.
         torch.cuda.current_stream(device).synchronize()
+
+    def events(self, torch):
+        """The four stage-boundary events of a timed frame, created once per workspace."""
+        if self._events is None:
+            self._events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        return self._events
 
     def set_mode(self, sort_mode, keep_sorted_keys=False):
         _capi.check(_capi.lib().fgs_layout_set_sort_mode(C.byref(self.lay), int(sort_mode)))
@@ -365,6 +376,33 @@ class Pipeline:
                 lst.append(ws)
 
     # -- the hot path -----------------------------------------------------------
+    def _issue(self, torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1, out_ptr, a_ptr, d_ptr,
+               st, timing):
+        """Enqueue one frame on stream ``st``.  Without stage timing it is ONE C call
+        (``fgs_render``: the kernels chain by programmatic dependent launch); with it, the
+        stage entry points with an event at each of the reference's three stage boundaries
+        (pipeline.py:84-102)."""
+        base, lay = C.c_void_p(ws.base), C.byref(ws.lay)
+        if not timing:
+            _capi.check(L.fgs_render(self.packed.data_ptr(), ws.kcut_ptr, self.count, C.byref(cam),
+                                     float(tau), deg, sid, bg_c, flags, b0, b1, ws.next_epoch(),
+                                     out_ptr, a_ptr, d_ptr, base, lay, st))
+            return None
+        ev = ws.events(torch)
+        ev[0].record()
+        _capi.check(L.fgs_preprocess(self.packed.data_ptr(), ws.kcut_ptr, self.count,
+                                     C.byref(cam), float(tau), deg, sid, b0, b1, base, lay, st))
+        _capi.check(L.fgs_scan(base, lay, st))
+        _capi.check(L.fgs_emit(self.packed.data_ptr(), C.byref(cam), sid, b0, b1, base, lay, st))
+        ev[1].record()
+        _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
+        _capi.check(L.fgs_ranges(base, lay, st))
+        ev[2].record()
+        _capi.check(L.fgs_blend(self.packed.data_ptr(), bg_c, float(tau), flags, b0, b1,
+                                out_ptr, a_ptr, d_ptr, base, lay, st))
+        ev[3].record()
+        return ev
+
     def render(self, camera, strategy="precise", tau=TAU_DEFAULT,
                background=(0.0, 0.0, 0.0), workers=1, initial_capacity=None,
                pipelined=True, *, exact=False, extras=False, contrib=True,
@@ -375,10 +413,13 @@ class Pipeline:
         and do not change the result (the reference guarantees the same).
         Keyword-only extras: ``exact`` (bit-identical frame, FP64 expf),
         ``extras`` (alpha + depth maps), ``contrib`` (pairs_contributing),
-        ``as_numpy`` (False: CUDA tensors, no D2H), ``band=(ty0, ty1)`` tile-row
-        band for multi-GPU row splitting, ``quantized`` (the image comes back as
-        uint8, quantised on the device exactly like ``images.py:12-15``; a
-        quarter of the bytes to read back).
+        ``as_numpy`` (False: CUDA tensors, no D2H), ``timing`` (False: no stage
+        times in the stats; the frame is then a single C call), ``quantized`` (the
+        image comes back as uint8, quantised on the device exactly like
+        ``images.py:12-15``; a quarter of the bytes to read back), and
+        ``band=(ty0, ty1)``: only that tile-row band is rendered (multi-GPU row
+        splitting, see ``render_bands``) and the returned image holds just the
+        band's pixel rows, ``Framebuffer.rows = (y0, y1)``.
         """
         torch = _torch()
         t_host0 = time.perf_counter_ns()
@@ -391,6 +432,7 @@ class Pipeline:
         b0, b1 = (0, gh - 1) if band is None else (int(band[0]), int(band[1]))
         if not (0 <= b0 <= b1 < gh):
             raise ValueError(f"band {band!r} outside the {gh} tile rows")
+        y0, y1 = b0 * TILE_SIZE, min((b1 + 1) * TILE_SIZE, H)      # pixel rows rendered
         bg = np.asarray(background, dtype=np.float32).reshape(3)
         bg_c = (C.c_float * 3)(*bg.tolist())
         flags = (_capi.BLEND_EXACT if exact else 0) | (_capi.BLEND_CONTRIB if contrib else 0)
@@ -399,13 +441,13 @@ class Pipeline:
         capacity = max(capacity, 1)
 
         with torch.cuda.device(self.device):
-            st = _stream_ptr(torch, self.device)
+            stream = torch.cuda.current_stream(self.device)
+            st = C.c_void_p(stream.cuda_stream)
             kcut = self._cutoffs(torch, tau)
             while True:
                 ws = self._take_ws(torch, W, H, capacity)
                 ws.set_mode(_capi.SORT_MODES[self.sort_mode])
-                lay = C.byref(ws.lay)
-                base = C.c_void_p(ws.base)
+                ws.kcut_ptr = kcut.data_ptr()
                 if extras:
                     if ws.alpha is None:
                         ws.alpha = torch.empty((H, W), dtype=torch.float32, device=self.device)
@@ -413,43 +455,27 @@ class Pipeline:
                     a_ptr, d_ptr = ws.alpha.data_ptr(), ws.depthmap.data_ptr()
                 else:
                     a_ptr = d_ptr = None
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)] if timing else None
-                if timing:
-                    ev[0].record()
-                _capi.check(L.fgs_preprocess(self.packed.data_ptr(), kcut.data_ptr(), self.count,
-                                             C.byref(cam), float(tau), deg, sid, b0, b1, base, lay, st))
-                _capi.check(L.fgs_scan(base, lay, st))
-                _capi.check(L.fgs_emit(self.packed.data_ptr(), C.byref(cam), sid, b0, b1, base, lay, st))
-                if timing:
-                    ev[1].record()
-                _capi.check(L.fgs_sort(base, lay, ws.next_epoch(), st))
-                _capi.check(L.fgs_ranges(base, lay, st))
-                if timing:
-                    ev[2].record()
-                _capi.check(L.fgs_blend(self.packed.data_ptr(), bg_c, float(tau), flags, b0, b1,
-                                        ws.rgb.data_ptr(),
-                                        a_ptr, d_ptr, base, lay, st))
-                if timing:
-                    ev[3].record()
+                ev = self._issue(torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1,
+                                 ws.rgb.data_ptr(), a_ptr, d_ptr, st, timing)
                 out_img = ws.rgb
                 if quantized:
                     if ws.rgb8 is None:
                         ws.rgb8 = torch.empty((H, W, 3), dtype=torch.uint8, device=self.device)
-                    _capi.check(L.fgs_quantize_rgb8(ws.rgb.data_ptr(), H * W * 3,
-                                                    ws.rgb8.data_ptr(), st))
+                    _capi.check(L.fgs_quantize_rgb8(ws.rgb[y0:y1].data_ptr(), (y1 - y0) * W * 3,
+                                                    ws.rgb8[y0:y1].data_ptr(), st))
                     out_img = ws.rgb8
                 ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
                 h_rgb = None
                 if as_numpy:
-                    h_rgb = _pinned.take(torch, (H, W, 3), out_img.dtype)
-                    h_rgb.copy_(out_img, non_blocking=True)
+                    h_rgb = _pinned.take(torch, (y1 - y0, W, 3), out_img.dtype)
+                    h_rgb.copy_(out_img[y0:y1], non_blocking=True)
                     if extras:
-                        h_a = _pinned.take(torch, (H, W), torch.float32)
-                        h_d = _pinned.take(torch, (H, W), torch.float32)
-                        h_a.copy_(ws.alpha, non_blocking=True)
-                        h_d.copy_(ws.depthmap, non_blocking=True)
-                torch.cuda.current_stream(self.device).synchronize()
-                s = np.frombuffer(ws.h_stats.numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
+                        h_a = _pinned.take(torch, (y1 - y0, W), torch.float32)
+                        h_d = _pinned.take(torch, (y1 - y0, W), torch.float32)
+                        h_a.copy_(ws.alpha[y0:y1], non_blocking=True)
+                        h_d.copy_(ws.depthmap[y0:y1], non_blocking=True)
+                stream.synchronize()
+                s = ws.h_stats_np[0]
                 if int(s["overflow"]):
                     # binning.py:134-143: grow, never truncate; counted in the stats
                     stats.buffer_regrows += 1
@@ -474,10 +500,136 @@ class Pipeline:
                 if extras:
                     fb.alpha, fb.depth = _pinned.as_numpy(h_a), _pinned.as_numpy(h_d)
             else:
-                fb = Framebuffer(out_img.clone(), bg)
+                fb = Framebuffer(out_img[y0:y1].clone(), bg)
                 if extras:
-                    fb.alpha, fb.depth = ws.alpha.clone(), ws.depthmap.clone()
+                    fb.alpha, fb.depth = ws.alpha[y0:y1].clone(), ws.depthmap[y0:y1].clone()
+            fb.rows = (y0, y1)
             self._give_ws(ws)
+        stats.e2e_ns = time.perf_counter_ns() - t_host0
+        return fb, stats
+
+    def render_bands(self, camera, group=None, strategy="precise", tau=TAU_DEFAULT,
+                     background=(0.0, 0.0, 0.0), *, bands=None, dst=0, out=None, exact=False,
+                     contrib=True, as_numpy=True, sync=True):
+        """ONE frame split into tile-row bands over the ranks of ``group`` (a
+        ``torch.distributed`` process group, default: the world), gathered on rank ``dst``
+        (the reference splits a frame's tiles over its worker pool the same
+        way, render.py:293-309).  Call it on every rank with the same arguments.
+
+        Every rank holds the whole scene and renders the band ``bands[rank]`` -- by default
+        the work-balanced bands of ``sharding.balanced_band_partition(self.row_weights(camera))``,
+        which every rank derives identically without communicating.  The blend writes the
+        band straight into the buffer that is sent: on ``dst`` the full ``(H, W, 3)`` frame
+        (``out`` or a fresh tensor) in which the other ranks' rows are received in place, on
+        the other ranks a band-sized buffer.  The receives are posted on a side stream before
+        ``dst``'s own band is rendered, the sends are issued right behind each band's blend;
+        NCCL send/recv over NVLink, no other collective.  The frame is bit-identical to
+        ``render(camera)`` on one GPU (tiles are independent).
+
+        Returns ``(Framebuffer, FrameStats)``: on ``dst`` the whole frame (host array, or the
+        device tensor with ``as_numpy=False``), elsewhere the rank's own band rows
+        (``Framebuffer.rows``).  The counters are those of the rank's band.  ``sync=False``
+        (device tensors only) leaves the gather enqueued on the current stream and skips the
+        stats read-back, for callers that time a sequence of frames on the device."""
+        torch = _torch()
+        import torch.distributed as dist
+        from . import sharding
+        t_host0 = time.perf_counter_ns()
+        if not dist.is_initialized():
+            raise RuntimeError("render_bands needs an initialised torch.distributed process group")
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        sid = _strategy_id(strategy)
+        deg = _check_sh_degree(self.sh_degree)
+        L = _capi.lib()
+        cam = _capi.camera_struct(camera)
+        W, H = int(camera.width), int(camera.height)
+        gh = -(-H // TILE_SIZE)
+        if bands is None:
+            if world == 1:
+                bands = [(0, gh - 1)]
+            else:
+                rw = self.row_weights(camera, tau)
+                bands = sharding.balanced_band_partition(rw, world, fixed_rows=0.3 * float(rw.mean()))
+        if len(bands) != world:
+            raise ValueError(f"{len(bands)} bands for {world} ranks")
+        b0, b1 = int(bands[rank][0]), int(bands[rank][1])
+        y0, y1 = sharding.band_pixel_rows((b0, b1), H)
+        if sync is False and as_numpy:
+            raise ValueError("sync=False needs as_numpy=False")
+        bg = np.asarray(background, dtype=np.float32).reshape(3)
+        bg_c = (C.c_float * 3)(*bg.tolist())
+        flags = (_capi.BLEND_EXACT if exact else 0) | (_capi.BLEND_CONTRIB if contrib else 0)
+        stats = FrameStats(strategy=strategy, tau=float(tau), workers=world)
+        capacity = self._default_capacity()
+        with torch.cuda.device(self.device):
+            stream = torch.cuda.current_stream(self.device)
+            st = C.c_void_p(stream.cuda_stream)
+            kcut = self._cutoffs(torch, tau)
+            if rank == dst:
+                full = out if out is not None else torch.empty((H, W, 3), dtype=torch.float32,
+                                                               device=self.device)
+                if tuple(full.shape) != (H, W, 3) or full.dtype != torch.float32 or not full.is_contiguous():
+                    raise ValueError("out must be a contiguous float32 (H, W, 3) CUDA tensor")
+                rows, frame_ptr = None, full.data_ptr()
+                # the peers' rows land in place while this rank renders its own band: the
+                # receives go on a side stream that does not wait for the render stream
+                side = self._side_streams(torch, 1)[0]
+                side.wait_stream(stream)          # `full` may still be in use by earlier work
+                with torch.cuda.stream(side):
+                    works = sharding.gather_band_rows(full, None, bands, H, rank, dst, group)
+            else:
+                full = None
+                rows = torch.empty((max(y1 - y0, 0), W, 3), dtype=torch.float32, device=self.device)
+                # the blend addresses pixels by their frame row: shift the base so that row y0
+                # of the frame is row 0 of the band buffer (only rows y0..y1 are written)
+                frame_ptr = rows.data_ptr() - y0 * W * 12
+                works = None
+            while True:
+                ws = self._take_ws(torch, W, H, capacity)
+                ws.set_mode(_capi.SORT_MODES[self.sort_mode])
+                ws.kcut_ptr = kcut.data_ptr()
+                if b1 >= b0:
+                    self._issue(torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1,
+                                C.c_void_p(frame_ptr), None, None, st, False)
+                if not sync:
+                    break
+                ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
+                stream.synchronize()
+                s = ws.h_stats_np[0]
+                if b1 >= b0 and int(s["overflow"]):
+                    stats.buffer_regrows += 1
+                    need = max(int(s["pairs_emitted"]), int(s["list_used"]))
+                    capacity = max(int(capacity * 1.5) + 16, need + need // 8 + 4096)
+                    self._give_ws(ws)
+                    continue
+                if b1 >= b0:
+                    if int(s["bad_depth"]):
+                        self._give_ws(ws)
+                        raise ValueError("depths must be positive and finite (cull failed upstream)")
+                    _fill_counters(stats, s)
+                    self._last_pairs = max(self._last_pairs, stats.pairs_emitted)
+                break
+            self._give_ws(ws)
+            if rank != dst:
+                works = sharding.gather_band_rows(None, rows, bands, H, rank, dst, group)
+                for w_ in works:
+                    w_.wait()
+                img = rows
+            else:
+                with torch.cuda.stream(side):
+                    for w_ in works:
+                        w_.wait()
+                stream.wait_stream(side)          # the frame is complete behind this point
+                img = full
+            fb_rows = (0, H) if rank == dst else (y0, y1)
+            if as_numpy:
+                h = _pinned.take(torch, tuple(img.shape), torch.float32)
+                h.copy_(img, non_blocking=True)
+                stream.synchronize()
+                fb = Framebuffer(_pinned.as_numpy(h), bg)
+            else:
+                fb = Framebuffer(img, bg)
+            fb.rows = fb_rows
         stats.e2e_ns = time.perf_counter_ns() - t_host0
         return fb, stats
 

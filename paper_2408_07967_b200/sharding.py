@@ -112,3 +112,26 @@ def gather_bands(local_rows, bands, height: int, dist, rank: int, dst: int = 0):
         for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, local_rows.contiguous(), dst)]):
             w.wait()
     return None
+
+
+def gather_band_rows(full, local_rows, bands, height: int, rank: int, dst: int = 0, group=None):
+    """In-place band gather (what ``Pipeline.render_bands`` issues behind its blend): on
+    ``dst``, ``full`` is the ``(H, W, 3)`` frame whose own band rows are already written and
+    every other rank's rows are received straight into their place (row slices of a
+    contiguous frame are contiguous, so no staging copy); elsewhere ``local_rows`` -- this
+    rank's ``(rows, W, 3)`` band -- is sent to ``dst``.  Point-to-point because bands are
+    unequal.  Returns the work handles; the caller waits on them (on CUDA tensors ``wait``
+    orders the current stream behind the transfer, it does not block the host)."""
+    import torch.distributed as dist
+    world = len(bands)
+    ops = []
+    if rank == dst:
+        for r in range(world):
+            y0, y1 = band_pixel_rows(bands[r], height)
+            if r != dst and y1 > y0:
+                peer = r if group is None else dist.get_global_rank(group, r)
+                ops.append(dist.P2POp(dist.irecv, full[y0:y1], peer, group))
+    elif local_rows is not None and local_rows.shape[0] > 0:
+        peer = dst if group is None else dist.get_global_rank(group, dst)
+        ops.append(dist.P2POp(dist.isend, local_rows, peer, group))
+    return dist.batch_isend_irecv(ops) if ops else []

@@ -375,10 +375,46 @@ def test_row_bands_equal_full_frame():
     for b0, b1 in ((0, 7), (8, 15), (16, gh - 1)):
         fb, s = pipe.render(cam, band=(b0, b1))
         y0, y1 = b0 * 16, min((b1 + 1) * 16, 400)
-        out[y0:y1] = fb.image[y0:y1]
+        assert fb.rows == (y0, y1) and fb.image.shape == (y1 - y0, 512, 3)   # the band's rows only
+        out[y0:y1] = fb.image
         total += s.pairs_emitted
     assert np.array_equal(out, full.image)
     assert total == st.pairs_emitted
+
+
+def test_render_bands_world1_equals_render():
+    """The product row-band API on a one-rank process group: Pipeline.render_bands renders
+    the frame's band(s) into the gather buffer and returns the same bits as render(); the
+    gather itself is covered at world size 2 over gloo (tests/test_sharding_gloo.py)."""
+    import os
+    import tempfile
+    import torch
+    import torch.distributed as dist
+    act = fgs.activate(fgs.gen_synthetic("mixed", 20000, 7))
+    cam = fgs.orbit_cameras(1, 20.0, 512, 400)[0]
+    pipe = fgs.Pipeline(act)
+    full, st = pipe.render(cam, background=(0.1, 0.2, 0.3))
+    with pytest.raises(RuntimeError):
+        pipe.render_bands(cam)                       # no process group yet
+    store = tempfile.NamedTemporaryFile(delete=False)
+    store.close()
+    dist.init_process_group("nccl", init_method="file://" + store.name, rank=0, world_size=1,
+                            device_id=pipe.device)
+    try:
+        fb, s = pipe.render_bands(cam, background=(0.1, 0.2, 0.3))
+        assert fb.rows == (0, 400) and np.array_equal(fb.image, full.image)
+        assert s.pairs_emitted == st.pairs_emitted and s.pairs_contributing == st.pairs_contributing
+        out = torch.zeros((400, 512, 3), dtype=torch.float32, device=pipe.device)
+        fbd, _ = pipe.render_bands(cam, None, "precise", 1 / 255, (0.1, 0.2, 0.3), out=out,
+                                   as_numpy=False, sync=False)
+        torch.cuda.synchronize()
+        assert fbd.image is out and np.array_equal(out.cpu().numpy(), full.image)
+        with pytest.raises(ValueError):
+            pipe.render_bands(cam, bands=[(0, 3), (4, 24)])      # two bands, one rank
+    finally:
+        dist.destroy_process_group()
+        if os.path.exists(store.name):
+            os.unlink(store.name)
 
 
 # ---------------------------------------------------------------------------
@@ -795,7 +831,7 @@ def test_north_star_size_properties():
     total = 0
     for b0, b1 in zip(edges[:-1], edges[1:]):
         fb, s = pipe.render(cam, band=(b0, b1 - 1))
-        out[b0 * 16:min(b1 * 16, h)] = fb.image[b0 * 16:min(b1 * 16, h)]
+        out[b0 * 16:min(b1 * 16, h)] = fb.image
         total += s.pairs_emitted
     assert total == st.pairs_emitted and np.array_equal(out, full.image)
     del pipe
@@ -839,7 +875,7 @@ def test_row_weights_and_balanced_bands():
     for b in bands:
         fb, s = pipe.render(cam, band=b)
         y0, y1 = sharding.band_pixel_rows(b, 400)
-        out[y0:y1] = fb.image[y0:y1]
+        out[y0:y1] = fb.image
         total += s.pairs_emitted
     assert np.array_equal(out, full.image) and total == st.pairs_emitted
 

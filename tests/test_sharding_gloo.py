@@ -51,6 +51,15 @@ def _worker(rank, world, port, height, width, q):
         frame = torch.arange(height * width * 3, dtype=torch.float32).reshape(height, width, 3)
         y0, y1 = sharding.band_pixel_rows(bands[rank], height)
         full = sharding.gather_bands(frame[y0:y1].clone(), bands, height, dist, rank, 0)
+        # the in-place variant render_bands uses: dst's frame already holds its own rows
+        mine = frame[y0:y1].clone()
+        inplace = None
+        if rank == 0:
+            inplace = torch.full_like(frame, -1.0)
+            inplace[y0:y1] = mine
+        for w in sharding.gather_band_rows(inplace, mine, bands, height, rank, 0):
+            w.wait()
+        assert rank != 0 or torch.equal(inplace, frame)
         # views: weak scaling, no collective on the data path; only the max-over-ranks timing
         t = torch.tensor([float(rank + 1)])
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
