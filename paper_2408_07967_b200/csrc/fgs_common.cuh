@@ -49,6 +49,9 @@
 #define FGS_WORK_LARGE_TICKET  4   // (+1: CTAs out)
 #define FGS_WORK_SORT_DONE     6   // bit 0: medium class finished, bit 1: large class finished
 #define FGS_WORK_TAIL_OUT      7   // tail-kernel CTAs past their wait on FGS_WORK_SORT_DONE
+#define FGS_WORK_STAGE_USED    8   // records the preprocess CTAs have reserved in the stage
+#define FGS_WORK_FB_CTAS       9   // preprocess CTAs left to the placement walk (fallback list length)
+#define FGS_CTA_NO_STAGE  0xffffffffu   // ctainfo.w of a CTA whose records were not staged
 // blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
 // empty = last) and the blend's CTAs take them in bin order, so the long tiles start first
 // and the grid's tail is made of short ones
@@ -123,9 +126,14 @@ struct FrameDev {
     fgs_stats *stats;
     uint32_t *tilecount;    // [tiles]
     uint32_t *cursor;       // [tiles]
-    uint4    *tablelist;    // TILE_BUCKET: (tile, range base, pairs, slot | wc offset) per
-                            // (CTA, tile); aliases keys[1] + vals[0] + vals[1]
-    uint4    *ctainfo;      // [preprocess blocks] (list base, entries, staged records, 0)
+    uint4    *tablelist;    // TILE_BUCKET: (tile, range base, pairs, slot | record offset) per
+                            // (CTA, tile); aliases vals[0] + vals[1] (8 B x capacity)
+    uint64_t *stage;        // TILE_BUCKET: every preprocess CTA's records, grouped by table
+                            // entry, between fgs_preprocess and fgs_emit; aliases keys[1]
+    uint32_t *fb_list;      // TILE_BUCKET: preprocess CTAs left to the placement walk; aliases
+                            // blockbase (ONESWEEP's scan output)
+    uint4    *ctainfo;      // [preprocess blocks] (list base, entries, records, stage base or
+                            // FGS_CTA_NO_STAGE)
     uint32_t *tileorder;    // [FGS_ORDER_HDR + tiles]: bin counts, bin cursors, blend tile order
     uint32_t list_capacity;
 };
@@ -154,10 +162,12 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.stats = (fgs_stats *)(b + L->off_stats);
     f.tilecount = (uint32_t *)(b + L->off_tilecount);
     f.cursor = (uint32_t *)(b + L->off_cursor);
-    f.tablelist = (uint4 *)(b + L->off_keys[1]);
+    f.tablelist = (uint4 *)(b + L->off_vals[0]);
+    f.stage = f.keys[1];
+    f.fb_list = f.blockbase;
     f.ctainfo = (uint4 *)(b + L->off_ctainfo);
     f.tileorder = (uint32_t *)(b + L->off_tileorder);
-    f.list_capacity = (uint32_t)L->capacity;
+    f.list_capacity = (uint32_t)(L->capacity / 2);          // 16-byte entries in 8 B x capacity
     return f;
 }
 
@@ -338,6 +348,32 @@ __device__ __forceinline__ uint32_t block_excl_scan_256(uint32_t v, uint32_t *sc
     uint32_t wsum = lane < 8 ? scratch[lane] : 0u;
     uint32_t wincl = warp_incl_scan(wsum, lane);
     uint32_t wbase = __shfl_sync(FGS_FULL, wincl - wsum, w);
+    total = __shfl_sync(FGS_FULL, wincl, 7);
+    __syncthreads();
+    return wbase + incl - v;
+}
+// The same for a 64-bit value (two packed counters share one pair of barriers).
+// `scratch` is 8 uint64 in shared memory.
+__device__ __forceinline__ unsigned long long block_excl_scan64_256(unsigned long long v,
+                                                                    unsigned long long *scratch,
+                                                                    unsigned long long &total)
+{
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned long long incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(FGS_FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    if (lane == 31) scratch[w] = incl;
+    __syncthreads();
+    unsigned long long wsum = lane < 8 ? scratch[lane] : 0ull, wincl = wsum;
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(FGS_FULL, wincl, o);
+        if (lane >= o) wincl += t;
+    }
+    const unsigned long long wbase = __shfl_sync(FGS_FULL, wincl - wsum, w);
     total = __shfl_sync(FGS_FULL, wincl, 7);
     __syncthreads();
     return wbase + incl - v;

@@ -502,11 +502,32 @@ __device__ __forceinline__ int ht_find(const TileTable &T, uint32_t tile)
     return -1;
 }
 
+// K1 (TILE_BUCKET) work area; takes over the SH staging buffer once the colours are done.
+// A "regular" CTA -- every pair found a table entry, at most FGS_WC_CAP pairs, at most
+// FGS_PARK_CAP of them from Gaussians on the cooperative walk -- leaves K1 with its records
+// already grouped by (CTA, tile) run in the frame's stage, and K3 is a streaming copy of those
+// runs into the tile buckets.  Any other CTA is put on the fallback list and placed by the
+// second walk (k_place), exactly as every CTA was before the stage existed.
+#ifndef FGS_PARK_CAP
+#define FGS_PARK_CAP  2048          // pairs of cooperative-walk Gaussians a regular CTA can park
+#endif
+#define FGS_ER_NONE   0xffffffffu
+struct BinSmem {
+    TileTable tab;
+    uint16_t eoff[FGS_HT_SIZE];     // offset of table entry e's run in the CTA's record block
+    uint32_t park[FGS_PARK_CAP];    // entry | rank << 10 | owner thread << 20
+    uint64_t rec_of[FGS_PRE_THREADS];   // each thread's record: depth bits << 32 | Gaussian index
+    uint64_t wc[FGS_WC_CAP];        // the CTA's records in run order
+    uint32_t npark, irregular;
+};
+
 // What WALK_BIN / WALK_PLACE work on.
 struct BinCtx {
     TileTable *table;
     uint32_t *tile_ctr;             // per tile, FGS_CTR_STRIDE words apart: [0] pairs reserved
                                     // through tables, [1] fallback pairs, [2] fallback cursor
+    // WALK_BIN only
+    uint32_t *park, *npark, *irregular;
     // WALK_PLACE only
     const uint32_t *gbase;          // [FGS_HT_SIZE] bucket position of the entry's range
     const uint16_t *wcoff;          // [FGS_HT_SIZE] offset in the write-combining buffer
@@ -597,11 +618,30 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
             }
         }
         if (MODE == WALK_BIN) {
+            // count the pair in the CTA's table; the atomic's return value is its rank in the
+            // (CTA, tile) run, parked with the entry and the owner until the run offsets exist
+            uint32_t word = FGS_ER_NONE;
             if (pass) {
                 const uint32_t tile = (uint32_t)(ty * grid_w + tx);
                 const int e = ht_insert(*bc->table, tile);
-                if (e >= 0) atomicAdd(&bc->table->val[e], 1u);
-                else atomicAdd(&bc->tile_ctr[(size_t)tile * FGS_CTR_STRIDE + 1], 1u);
+                if (e >= 0) {
+                    const uint32_t r = atomicAdd(&bc->table->val[e], 1u);
+                    word = (uint32_t)e | (r << 10) | ((uint32_t)((threadIdx.x & ~31) + o) << 20);
+                } else {
+                    atomicAdd(&bc->tile_ctr[(size_t)tile * FGS_CTR_STRIDE + 1], 1u);
+                    *bc->irregular = 1u;
+                }
+            }
+            const uint32_t parked = __ballot_sync(FGS_FULL, word != FGS_ER_NONE);
+            if (parked) {
+                uint32_t pbase = 0;
+                if (lane == 0) pbase = atomicAdd(bc->npark, (uint32_t)__popc(parked));
+                pbase = __shfl_sync(FGS_FULL, pbase, 0);
+                if (word != FGS_ER_NONE) {
+                    const uint32_t pos = pbase + __popc(parked & lanemask_lt());
+                    if (pos < FGS_PARK_CAP) bc->park[pos] = word;
+                    else *bc->irregular = 1u;
+                }
             }
         }
         if (MODE == WALK_PLACE) {
@@ -645,6 +685,116 @@ __device__ __forceinline__ uint32_t warp_walk_tiles(const TileJob &job, int widt
 }
 
 // ---------------------------------------------------------------------------
+// The lane-local walk for the common case: a Gaussian whose candidate rectangle is at most
+// 3 x 3 tiles (95 % of them at 4-5 pairs per Gaussian) tests its own tiles, with no owner
+// search and no operand shuffles.  What a column of tiles shares (the facing vertical edge
+// ue, a ue^2, b ue, the unclamped minimiser -b ue / c) and what a row shares are evaluated
+// once, so a tile costs two clamps, two Horner steps and the comparison.  Same screen as
+// tile_hits32: the float32 minimum of the form over the tile decides unless it is within the
+// guard band of keff, and then the reference's float64 predicate does.  The band here is
+// 1e-4 of the Gaussian's own bound  a ex^2 + 2|b| ex ey + c ey^2 + |keff|  (ex = hx + 16,
+// ey = hy + 16: every candidate tile lies inside the extent rectangle grown by one tile, so
+// this bounds each tile's term magnitude) -- wider than tile_hits32's per-tile band, never
+// narrower, so the verdict is the reference's all the same.
+// Passing tiles are counted in the CTA's table; er[k] = entry | rank << 16 of tile
+// k = row * 3 + col (FGS_ER_NONE: no pair).  Returns the pair count; `mask` gets the pass bits
+// in the rectangle's own row-major order (what k_place expects).
+// ---------------------------------------------------------------------------
+template <bool PRECISE>
+__device__ __forceinline__ uint32_t small_walk(bool mine, float cx, float cy, float a, float b,
+                                               float c, float keff, float term, int tx0, int ty0,
+                                               int nx, int ny, int width, int height, int grid_w,
+                                               const BinCtx &bc, uint32_t (&er)[9], uint64_t &mask)
+{
+    uint32_t pass = 0;                                    // bit row * 3 + col
+    if (mine) {
+        if (PRECISE) {
+            const float tol = 1e-4f * (term + fabsf(keff));
+            const float klo = keff - tol, khi = keff + tol;
+            const float rc = __fdividef(1.0f, c), ra = __fdividef(1.0f, a);
+            const float xb = (float)(tx0 * FGS_TILE), yb = (float)(ty0 * FGS_TILE);
+            const float wf = (float)width, hf = (float)height;
+            float e0[3], e1[3], q2[3], lin[3], star[3];   // columns: u0 u1 a*ue^2 2*b*ue -b*ue/c
+            bool inu[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const float x0 = xb + (float)(FGS_TILE * i);
+                e0[i] = x0 - cx;
+                e1[i] = fminf(x0 + (float)FGS_TILE, wf) - cx;
+                inu[i] = e0[i] <= 0.0f && e1[i] >= 0.0f;
+                const float ue = e0[i] > 0.0f ? e0[i] : e1[i];   // the edge facing the centre
+                const float bu = b * ue;
+                q2[i] = a * ue * ue;
+                lin[i] = 2.0f * bu;
+                star[i] = -bu * rc;
+            }
+            uint32_t amb = 0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                // the row's own terms: v0 v1, the facing edge ve, c*ve^2, 2*b*ve, -b*ve/a
+                const float y0 = yb + (float)(FGS_TILE * j);
+                const float f0 = y0 - cy, f1 = fminf(y0 + (float)FGS_TILE, hf) - cy;
+                const bool inv = f0 <= 0.0f && f1 >= 0.0f;
+                const float ve = f0 > 0.0f ? f0 : f1;
+                const float bv = b * ve;
+                const float r2 = c * ve * ve, rin = 2.0f * bv, rtar = -bv * ra;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    if (i < nx && j < ny) {
+                        float q = __int_as_float(0x7f800000);
+                        if (!inu[i]) {                    // edge u = ue, v in [v0, v1]
+                            const float vs = fminf(fmaxf(star[i], f0), f1);
+                            q = fmaf(fmaf(c, vs, lin[i]), vs, q2[i]);
+                        }
+                        if (!inv) {                       // edge v = ve, u in [u0, u1]
+                            const float us = fminf(fmaxf(rtar, e0[i]), e1[i]);
+                            q = fminf(q, fmaf(fmaf(a, us, rin), us, r2));
+                        }
+                        const uint32_t bit = 1u << (j * 3 + i);
+                        if ((inu[i] && inv) || q < klo) pass |= bit;        // intersect.py:84-86 / clear hit
+                        else if (!(q > khi)) amb |= bit;                    // too close (or not finite)
+                    }
+                }
+            }
+            while (amb) {                                 // rare: the reference's float64 predicate
+                const int k = __ffs((int)amb) - 1;
+                amb &= amb - 1u;
+                if (tile_hits(tx0 + k % 3, ty0 + k / 3, width, height, cx, cy, a, b, c, keff))
+                    pass |= 1u << k;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    if (i < nx && j < ny) pass |= 1u << (j * 3 + i);
+        }
+    }
+    uint32_t m = 0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+        er[k] = FGS_ER_NONE;
+        if ((pass >> k) & 1u) {
+            const int i = k % 3, j = k / 3;
+            const uint32_t tile = (uint32_t)((ty0 + j) * grid_w + tx0 + i);
+            // (electing one lane per tile with match.any to count its peers with a single
+            // atomic was measured: 951 -> 1075 us on the 10M frame -- the match costs more
+            // than the same-address atomics it saves)
+            const int e = ht_insert(*bc.table, tile);
+            if (e >= 0) {
+                er[k] = (uint32_t)e | (atomicAdd(&bc.table->val[e], 1u) << 16);
+            } else {
+                atomicAdd(&bc.tile_ctr[(size_t)tile * FGS_CTR_STRIDE + 1], 1u);
+                *bc.irregular = 1u;
+            }
+            m |= 1u << (j * nx + i);
+        }
+    }
+    mask = m;
+    return (uint32_t)__popc(pass);
+}
+
+// ---------------------------------------------------------------------------
 // SH colour, render.py:52-86, for one channel triple
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
@@ -677,7 +827,7 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
 #ifndef FGS_SH_STAGED
 #define FGS_SH_STAGED 12          // SH float4 planes staged in shared memory (of 12)
 #endif
-static_assert(FGS_SH_STAGED * FGS_PRE_THREADS * 16 >= (int)sizeof(TileTable), "the tile table aliases the staging buffer");
+static_assert(FGS_SH_STAGED * FGS_PRE_THREADS * 16 >= (int)sizeof(BinSmem), "the binning work area aliases the staging buffer");
 __device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
 {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(smem);
@@ -698,6 +848,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
 {
     __shared__ uint32_t s_red[8], s_red1[8], s_red2[8];
     __shared__ uint32_t s_bin[4], s_scan[8];
+    __shared__ unsigned long long s_scan64[8];
     // SH staging: plane j of thread t at s_sh[j * 256 + t] (48 KB, dynamic).  A thread's 12
     // cp.async gathers are issued as soon as its Gaussian passes the frustum test and land
     // while the covariance chain runs -- no registers held, one DRAM round trip hidden.
@@ -707,10 +858,11 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = g < P;
-    // TILE_BUCKET: this CTA's pairs per tile.  The table takes over the SH staging buffer once
-    // every thread has consumed its coefficients (the CTA then needs 48 KB, not 56).
-    TileTable &s_tab = *reinterpret_cast<TileTable *>(s_sh);
-    if (BUCKET && threadIdx.x == 0) s_bin[2] = 0u;
+    // TILE_BUCKET: this CTA's pairs per tile, their parked ranks and the record block.  The
+    // work area takes over the SH staging buffer once every thread has consumed its
+    // coefficients (the CTA then needs 48 KB, not 92).
+    BinSmem &B = *reinterpret_cast<BinSmem *>(s_sh);
+    TileTable &s_tab = B.tab;
 
     TileJob job;
     job.cand = 0;
@@ -719,11 +871,13 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     job.nx = 1;
     job.mask = 0;
     bool retained = false, degenerate = false;
-    uint32_t full_cand = 0;
-    float zcam = 0.0f;
+    uint32_t full_cand = 0, og = 0;
+    float zcam = 0.0f, job_term = 0.0f;
+    int job_ny = 0;
 
     if (live) {
-        // all four per-Gaussian geometry loads go out together (44 B; the culled ones waste 28)
+        // all per-Gaussian geometry loads go out together (48 B; the culled ones waste 28)
+        if (BUCKET) og = sc.orig[g];
         const float4 m = sc.g0[g];
         const float4 sc4 = sc.g1[g];
         const float4 q = sc.g2[g];
@@ -829,6 +983,8 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                     job.cx = px; job.cy = py; job.a = ca; job.b = cb; job.c = cc;
                     job.keff = keff;
                     job.tx0 = tx0; job.ty0 = by0; job.nx = tx1 - tx0 + 1;
+                    job_ny = by1 - by0 + 1;
+                    job_term = term;
                 }
                 // Row-band frames (multi-GPU): a Gaussian without candidate tiles in this
                 // rank's band emits no pair here, so nothing reads its colour or splat row --
@@ -885,16 +1041,34 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
 
     uint32_t npairs;
     uint64_t passmask = 0;
+    uint32_t er[9];                       // small walk: entry | rank << 16 per tile of the 3 x 3
+    const uint64_t rec = ((uint64_t)__float_as_uint(zcam) << 32) | og;
     if (BUCKET) {
         __syncthreads();                  // every thread is done with the SH staging buffer
         for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) {
             s_tab.key[i] = FGS_HT_EMPTY;
             s_tab.val[i] = 0u;
         }
+        if (threadIdx.x == 0) { B.npark = 0u; B.irregular = 0u; s_bin[2] = 0u; }
+        B.rec_of[threadIdx.x] = rec;
         __syncthreads();
-        const BinCtx bc{&s_tab, f.tilecount, nullptr, nullptr, nullptr, nullptr, nullptr};
-        npairs = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_BIN>(
-            job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, &bc, &passmask);
+        const BinCtx bc{&s_tab, f.tilecount, B.park, &B.npark, &B.irregular,
+                        nullptr, nullptr, nullptr, nullptr, nullptr};
+        // rectangles of at most 3 x 3 tiles: each lane walks its own; the rest of the warp's
+        // candidates (if any) go through the cooperative walk
+        // (measured on the 10M frame: everything through the cooperative walk instead, with
+        // the same parking, is 1021 us against 952)
+        const bool small = job.cand != 0u && job.nx <= 3 && job_ny <= 3;
+        npairs = small_walk<STRAT == FGS_PRECISE>(small, job.cx, job.cy, job.a, job.b, job.c, job.keff,
+                                                  job_term, job.tx0, job.ty0, job.nx, job_ny,
+                                                  cam.width, cam.height, cam.grid_w, bc, er, passmask);
+        if (small) job.cand = 0u;
+        if (__any_sync(FGS_FULL, job.cand != 0u)) {
+            uint64_t bigmask = 0;
+            const uint32_t nbig = warp_walk_tiles<STRAT == FGS_PRECISE, WALK_BIN>(
+                job, cam.width, cam.height, cam.grid_w, 0, 0, 0, nullptr, nullptr, &bc, &bigmask);
+            if (!small) { npairs = nbig; passmask = bigmask; }
+        }
         // binning.py:50-51: depths of emitted pairs must be positive and finite
         if (npairs && !(zcam < __int_as_float(0x7f800000))) f.stats->bad_depth = 1u;
     } else if (STRAT == FGS_PRECISE)
@@ -904,7 +1078,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         npairs = job.cand;
     if (live) {
         f.counts[g] = npairs;
-        if (STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
+        if (!BUCKET && STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
     }
 
     // block totals: pairs (-> blocksums), retained / degenerate / candidates (-> stats)
@@ -937,11 +1111,11 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
 
     // ---- TILE_BUCKET epilogue: one range per (CTA, tile) in the tile's bucket.  Thread t
     // owns table slots 4t .. 4t+3; entries go to the frame's table list in slot order, each
-    // with its offset in K3's write-combining buffer (a prefix of the entries fits).
-    // The two global round trips of this epilogue -- the bucket reservations (one atomic per
-    // table entry, result needed for the list) and the list reservation (thread 0) -- are
-    // issued as early as their operands exist and consumed after the block scans, which
-    // hide them.
+    // with the offset of its run in the CTA's record block.
+    // The global round trips of this epilogue -- the bucket reservations (one atomic per
+    // table entry, result needed for the list), the list reservation and the stage
+    // reservation (thread 0) -- are issued as early as their operands exist and consumed
+    // after the block scans / the placement, which hide them.
     uint32_t cnt[4], tl[4], gb[4], nent = 0, npr = 0;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -954,36 +1128,98 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         // the counters always get the pairs, so M stays exact when the frame overflows
         gb[k] = used ? atomicAdd(&f.tilecount[(size_t)tl[k] * FGS_CTR_STRIDE], cnt[k]) : 0u;
     }
-    uint32_t tot_ent, tot_pr;
-    const uint32_t ent_off = block_excl_scan_256(nent, s_scan, tot_ent);
-    uint32_t lb = 0;
-    if (threadIdx.x == 0 && tot_ent) lb = atomicAdd(&f.stats->list_used, tot_ent);
-    uint32_t pr_off = block_excl_scan_256(npr, s_scan, tot_pr);
+    // entries and pairs before this thread's slots: one scan of the packed pair
+    unsigned long long tot2;
+    const unsigned long long off2 =
+        block_excl_scan64_256(((unsigned long long)nent << 40) | npr, s_scan64, tot2);
+    const uint32_t tot_ent = (uint32_t)(tot2 >> 40), ent_off = (uint32_t)(off2 >> 40);
+    const unsigned long long tot_pr64 = tot2 & ((1ull << 40) - 1ull);
+    uint32_t pr_off = (uint32_t)(off2 & ((1ull << 40) - 1ull));
+    // regular: every pair has a table entry and a parked rank, and the record block fits
+    const bool regular = B.irregular == 0u && tot_pr64 <= (unsigned long long)FGS_WC_CAP;
+    const uint32_t tot_pr = regular ? (uint32_t)tot_pr64 : 0u;
+    uint32_t lb = 0, sb = FGS_CTA_NO_STAGE;
     if (threadIdx.x == 0) {
-        s_bin[0] = lb;
-        s_bin[1] = (lb + tot_ent <= f.list_capacity) ? 1u : 0u;
-        if (tot_ent && lb + tot_ent > f.list_capacity) f.stats->overflow = 1u;   // grow and re-run
+        if (tot_ent) lb = atomicAdd(&f.stats->list_used, tot_ent);
+        if (regular && tot_pr) sb = atomicAdd(&fgs_work(f.stats)[FGS_WORK_STAGE_USED], tot_pr);
+        if (!regular)                           // left to the placement walk (k_place)
+            f.fb_list[atomicAdd(&fgs_work(f.stats)[FGS_WORK_FB_CTAS], 1u)] = blockIdx.x;
     }
-    __syncthreads();
-    const uint32_t list_base = s_bin[0];
-    const bool fits = s_bin[1] != 0u;
-    uint32_t idx = list_base + ent_off, staged_end = 0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int e = threadIdx.x * 4 + k;
-        if (tl[k] != FGS_HT_EMPTY) {
-            const bool wc = pr_off + cnt[k] <= FGS_WC_CAP;
-            if (wc) staged_end = pr_off + cnt[k];
-            if (fits)
-                f.tablelist[idx++] = make_uint4(tl[k], gb[k], cnt[k],
-                                                ((uint32_t)e << 16) | (wc ? pr_off : FGS_WC_NONE));
+    if (!regular) {
+        // ---- the second walk places this CTA's pairs: its list says, per entry, where the
+        // placement walk write-combines the run (a prefix of the runs fits its buffer)
+        if (live && STRAT == FGS_PRECISE && npairs) f.passmask[g] = passmask;
+        if (threadIdx.x == 0) {
+            s_bin[0] = lb;
+            s_bin[1] = (lb + tot_ent <= f.list_capacity) ? 1u : 0u;
+            if (tot_ent && lb + tot_ent > f.list_capacity) f.stats->overflow = 1u;   // grow and re-run
         }
-        pr_off += cnt[k];
+        __syncthreads();
+        const uint32_t list_base = s_bin[0];
+        const bool fits = s_bin[1] != 0u;
+        uint32_t idx = list_base + ent_off, staged_end = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int e = threadIdx.x * 4 + k;
+            if (tl[k] != FGS_HT_EMPTY) {
+                const bool wc = (unsigned long long)pr_off + cnt[k] <= (unsigned long long)FGS_WC_CAP;
+                if (wc) staged_end = pr_off + cnt[k];
+                if (fits)
+                    f.tablelist[idx++] = make_uint4(tl[k], gb[k], cnt[k],
+                                                    ((uint32_t)e << 16) | (wc ? pr_off : FGS_WC_NONE));
+            }
+            pr_off += cnt[k];
+        }
+        if (staged_end) atomicMax(&s_bin[2], staged_end);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            f.ctainfo[blockIdx.x] = make_uint4(list_base, fits ? tot_ent : 0u, s_bin[2], FGS_CTA_NO_STAGE);
+        return;
     }
-    if (staged_end) atomicMax(&s_bin[2], staged_end);
+    // ---- regular: run offsets, then every pair's record to its run, rank-th inside it
+    {
+        uint32_t o = pr_off;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (tl[k] != FGS_HT_EMPTY) B.eoff[threadIdx.x * 4 + k] = (uint16_t)o;
+            o += cnt[k];
+        }
+    }
+    __syncthreads();                      // run offsets are in place
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+        if (er[k] != FGS_ER_NONE) B.wc[B.eoff[er[k] & 0xffffu] + (er[k] >> 16)] = rec;
+    for (uint32_t i = threadIdx.x; i < B.npark; i += FGS_PRE_THREADS) {
+        const uint32_t w = B.park[i];
+        B.wc[B.eoff[w & 1023u] + ((w >> 10) & 1023u)] = B.rec_of[w >> 20];
+    }
+    if (threadIdx.x == 0) {               // the two reservations have had the placement to arrive
+        const bool fits = lb + tot_ent <= f.list_capacity;
+        // M is exact either way (tile counters); a stage that does not fit means the pair
+        // buffer does not either
+        const bool stage_fits = !tot_pr || (uint64_t)sb + tot_pr <= (uint64_t)f.list_capacity * 2u;
+        if ((tot_ent && !fits) || !stage_fits) f.stats->overflow = 1u;             // grow and re-run
+        s_bin[0] = lb;
+        s_bin[1] = fits ? 1u : 0u;
+        s_bin[3] = stage_fits ? sb : FGS_CTA_NO_STAGE;
+        f.ctainfo[blockIdx.x] = make_uint4(lb, fits ? tot_ent : 0u, tot_pr,
+                                           tot_pr && stage_fits ? sb : FGS_CTA_NO_STAGE);
+    }
     __syncthreads();
-    if (threadIdx.x == 0)
-        f.ctainfo[blockIdx.x] = make_uint4(list_base, fits ? tot_ent : 0u, s_bin[2], 0u);
+    if (s_bin[1]) {
+        uint32_t idx = s_bin[0] + ent_off;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (tl[k] != FGS_HT_EMPTY)
+                f.tablelist[idx++] = make_uint4(tl[k], gb[k], cnt[k],
+                                                ((uint32_t)(threadIdx.x * 4 + k) << 16) | pr_off);
+            pr_off += cnt[k];
+        }
+    }
+    const uint32_t stage_base = s_bin[3];
+    if (tot_pr && stage_base != FGS_CTA_NO_STAGE)
+        for (uint32_t i = threadIdx.x; i < tot_pr; i += FGS_PRE_THREADS)
+            f.stage[stage_base + i] = B.wc[i];
 }
 
 static CamDev g_dummy_cam;   // keeps CamDev's layout in one place for sizeof checks
@@ -1352,10 +1588,70 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
 }
 
 // ---------------------------------------------------------------------------
-// K3 (TILE_BUCKET): second walk.  The CTA reloads its tile table from the frame's list
-// (same slots, so lookups probe exactly as K1's inserts did), ranks every pair inside its
+// K3 (TILE_BUCKET): the runs of every regular preprocess CTA, from the stage into the tile
+// buckets.  One CTA per preprocess CTA: its table list gives, per run, the tile, the range
+// reserved in the tile's bucket and the run's offset in the CTA's record block; the range
+// table (k_scan_tiles) turns that into positions.  A pure streaming copy: coalesced reads of
+// the block, runs written as contiguous segments.
+// ---------------------------------------------------------------------------
+#define FGS_SCATTER_THREADS 128
+// One CTA of four warps per preprocess CTA; warp w takes the table entries w, w + 4, ...:
+// lane l fetches entry 4 l + w (tile, bucket range, run offset) and the tile's bucket start --
+// two round trips for up to 32 runs per warp -- and the warp then copies its runs one after
+// the other, 32 records per step (a run of a Morton-ordered scene is ~30 records).  No shared
+// memory, no barrier.
+__global__ void __launch_bounds__(FGS_SCATTER_THREADS)
+k_scatter_runs(const uint4 *__restrict__ ctainfo, const uint4 *__restrict__ tablelist,
+               const int32_t *__restrict__ starts, const uint64_t *__restrict__ stage,
+               uint64_t *__restrict__ rec, const fgs_stats *__restrict__ stats)
+{
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
+    constexpr uint32_t W = FGS_SCATTER_THREADS / 32;
+    const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t over = stats->overflow;
+    const uint4 info = ctainfo[blockIdx.x];              // (list base, entries, records, stage base)
+    if (over || info.w == FGS_CTA_NO_STAGE || info.z == 0u) return;
+    const uint64_t *blk = stage + info.w;
+    for (uint32_t eb = w; eb < info.y; eb += 32u * W) {  // this warp's entries eb, eb + W, ...
+        uint32_t mydst = 0, myoff = 0, mycnt = 0;
+        const uint32_t mine = eb + lane * W;
+        if (mine < info.y) {
+            const uint4 ent = tablelist[info.x + mine];  // (tile, range base, pairs, slot | offset)
+            myoff = ent.w & 0xffffu;
+            mycnt = ent.z;
+            mydst = (uint32_t)starts[ent.x] + ent.y;
+        }
+        const uint32_t left = (info.y - eb + W - 1u) / W;
+        const int n = left < 32u ? (int)left : 32;
+        // four runs per step: their first 32 records are requested together, then stored
+        for (int k0 = 0; k0 < n; k0 += 4) {
+            uint32_t dst[4], off[4], cnt[4];
+            uint64_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                dst[u] = __shfl_sync(FGS_FULL, mydst, (k0 + u) & 31);
+                off[u] = __shfl_sync(FGS_FULL, myoff, (k0 + u) & 31);
+                cnt[u] = k0 + u < n ? __shfl_sync(FGS_FULL, mycnt, (k0 + u) & 31) : 0u;
+                v[u] = lane < cnt[u] ? blk[off[u] + lane] : 0ull;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (lane < cnt[u]) rec[dst[u] + lane] = v[u];
+                for (uint32_t j = lane + 32u; j < cnt[u]; j += 32u) rec[dst[u] + j] = blk[off[u] + j];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3 fallback (TILE_BUCKET): the second walk, for the preprocess CTAs on the fallback list
+// (a pair without a table entry, more pairs than the record block holds: caller-order scenes,
+// huge splats, very dense scenes).  The CTA reloads its tile table from the frame's list (same
+// slots, so lookups probe exactly as K1's inserts did), ranks every pair inside its
 // (CTA, tile) range with a shared-memory atomic, gathers the records by tile in the
-// write-combining buffer and writes them out as contiguous runs.
+// write-combining buffer and writes them out as contiguous runs.  Persistent CTAs over the
+// list; an empty list costs one launch.
 // ---------------------------------------------------------------------------
 struct PlaceSmem {
     TileTable tab;
@@ -1374,11 +1670,14 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
     PlaceSmem &S = *reinterpret_cast<PlaceSmem *>(place_raw);
     fgs_pdl_wait();
     fgs_pdl_trigger();
-    const uint32_t over = f.stats->overflow;             // consumed after the loads below are out
-    const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
+    if (f.stats->overflow) return;                       // uniform: grow and re-run
+    const uint32_t nfb = fgs_work(f.stats)[FGS_WORK_FB_CTAS];
+    for (uint32_t it = blockIdx.x; it < nfb; it += gridDim.x) {
+    const int cta = (int)f.fb_list[it];
+    const int g = cta * FGS_PRE_THREADS + threadIdx.x;
     const bool live = g < P;
     const uint32_t cnt = live ? f.counts[g] : 0u;
-    const uint4 info = f.ctainfo[blockIdx.x];            // (list base, entries, staged records)
+    const uint4 info = f.ctainfo[cta];                   // (list base, entries, staged records)
     // The Gaussian's own inputs are independent of the table: they go out with the first
     // round trip's successors (table list, bucket starts) instead of after the barriers.
     ushort4 r = make_ushort4(0, 0, 0, 0);
@@ -1390,27 +1689,8 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
         bits = __float_as_uint(f.depth[g]);
         og = orig[g];
     }
-    if (over) return;                                    // uniform: grow and re-run
-#if FGS_PLACE_PF_DIST
-    // L2 prefetch one wave ahead (the CTA that will take this one's place): its per-Gaussian
-    // inputs now, its table list at the end of this kernel (the header has arrived by then).
-    const int64_t gp = ((int64_t)blockIdx.x + FGS_PLACE_PF_DIST) * FGS_PRE_THREADS;
-    uint4 info_pf = make_uint4(0u, 0u, 0u, 0u);
-    if (gp < P) {
-        if (threadIdx.x == 0) info_pf = f.ctainfo[blockIdx.x + FGS_PLACE_PF_DIST];
-        const int t = threadIdx.x;                      // 56 lines of 128 B
-        const void *a = nullptr;
-        int64_t first = P;
-        if (t < 8) { a = f.counts + gp + t * 32; first = gp + t * 32; }
-        else if (t < 24) { a = f.rects + gp + (t - 8) * 16; first = gp + (t - 8) * 16; }
-        else if (t < 40) { a = f.passmask + gp + (t - 24) * 16; first = gp + (t - 24) * 16; }
-        else if (t < 48) { a = f.depth + gp + (t - 40) * 32; first = gp + (t - 40) * 32; }
-        else if (t < 56) { a = orig + gp + (t - 48) * 32; first = gp + (t - 48) * 32; }
-        if (first < P && !(STRAT != FGS_PRECISE && t >= 24 && t < 40))
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    }
-#endif
-    if (__syncthreads_or(cnt != 0u) == 0) return;        // uniform per block
+    __syncthreads();                                     // the previous CTA's flush is done
+    if (__syncthreads_or(cnt != 0u) == 0) continue;      // uniform per block
     for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) S.tab.key[i] = FGS_HT_EMPTY;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < info.y; i += FGS_PRE_THREADS) {
@@ -1450,7 +1730,8 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
             }
         }
     }
-    const BinCtx bc{&S.tab, f.tilecount, S.gbase, S.wcoff, S.wcrec, S.wcdst, f.starts};
+    const BinCtx bc{&S.tab, f.tilecount, nullptr, nullptr, nullptr,
+                    S.gbase, S.wcoff, S.wcrec, S.wcdst, f.starts};
     // records carry the caller's Gaussian index: the reference's pair value and tie-break
     // (measured: letting each lane walk the set bits of its own mask instead -- no owner
     // search, no shuffles -- is 13 % slower: the divergence costs more than the walk)
@@ -1458,14 +1739,7 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
                                                       og, f.keys[0], nullptr, &bc);
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < info.z; i += FGS_PRE_THREADS) f.keys[0][S.wcdst[i]] = S.wcrec[i];
-#if FGS_PLACE_PF_DIST
-    if (threadIdx.x < 32 && gp < P) {
-        info_pf.x = __shfl_sync(FGS_FULL, info_pf.x, 0);
-        info_pf.y = __shfl_sync(FGS_FULL, info_pf.y, 0);
-        for (uint32_t l = threadIdx.x; l * 8u < info_pf.y; l += 32u)      // 8 entries per line
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(f.tablelist + info_pf.x + l * 8u));
     }
-#endif
 }
 
 int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
@@ -1491,11 +1765,20 @@ int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strate
             if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
             attr_once.mark(attr_dev);
         }
+        FGS_CHAIN(k_scatter_runs, dim3(blocks), dim3(FGS_SCATTER_THREADS), 0, st,
+                  (const uint4 *)f.ctainfo, (const uint4 *)f.tablelist, (const int32_t *)f.starts,
+                  (const uint64_t *)f.stage, f.keys[0], (const fgs_stats *)f.stats);
+        FGS_CHECK_LAUNCH();
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned pgrid = blocks < (unsigned)(FGS_PLACE_MINBLOCKS * sms) ? blocks
+                                                                              : (unsigned)(FGS_PLACE_MINBLOCKS * sms);
         if (strategy == FGS_PRECISE)
-            FGS_CHAIN(k_place<FGS_PRECISE>, dim3(blocks), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,
+            FGS_CHAIN(k_place<FGS_PRECISE>, dim3(pgrid), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,
                       (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
         else
-            FGS_CHAIN(k_place<FGS_TIGHT_AABB>, dim3(blocks), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,
+            FGS_CHAIN(k_place<FGS_TIGHT_AABB>, dim3(pgrid), dim3(FGS_PRE_THREADS), sizeof(PlaceSmem), st,
                       (int)P, cam.width, cam.height, cam.grid_w, band0, band1, sc.orig, f);
     } else if (strategy == FGS_PRECISE) {
         k_emit<FGS_PRECISE><<<blocks, FGS_PRE_THREADS, 0, st>>>(

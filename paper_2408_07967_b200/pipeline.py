@@ -479,7 +479,7 @@ class Pipeline:
                 if int(s["overflow"]):
                     # binning.py:134-143: grow, never truncate; counted in the stats
                     stats.buffer_regrows += 1
-                    need = max(int(s["pairs_emitted"]), int(s["list_used"]))
+                    need = max(int(s["pairs_emitted"]), 2 * int(s["list_used"]))
                     capacity = max(int(capacity * 1.5) + 16, need + need // 8 + 4096)
                     if h_rgb is not None:
                         _pinned.give(h_rgb)
@@ -598,7 +598,7 @@ class Pipeline:
                 s = ws.h_stats_np[0]
                 if b1 >= b0 and int(s["overflow"]):
                     stats.buffer_regrows += 1
-                    need = max(int(s["pairs_emitted"]), int(s["list_used"]))
+                    need = max(int(s["pairs_emitted"]), 2 * int(s["list_used"]))
                     capacity = max(int(capacity * 1.5) + 16, need + need // 8 + 4096)
                     self._give_ws(ws)
                     continue
@@ -765,7 +765,7 @@ def sorted_pairs(pipe, camera, strategy="precise", tau=TAU_DEFAULT, band=None):
             s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
             if int(s["overflow"]):
                 capacity = max(int(capacity * 1.5) + 16,
-                               max(int(s["pairs_emitted"]), int(s["list_used"])) + 4096)
+                               max(int(s["pairs_emitted"]), 2 * int(s["list_used"])) + 4096)
                 continue
             break
         M, lay = int(s["pairs_emitted"]), ws.lay
@@ -814,7 +814,7 @@ def blend_eval_counts(pipe, camera, strategy="precise", tau=TAU_DEFAULT):
             s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
             if int(s["overflow"]):
                 capacity = max(int(capacity * 1.5) + 16,
-                               max(int(s["pairs_emitted"]), int(s["list_used"])) + 4096)
+                               max(int(s["pairs_emitted"]), 2 * int(s["list_used"])) + 4096)
                 continue
             break
         ev = torch.zeros(8, dtype=torch.int64, device=pipe.device)
@@ -946,7 +946,7 @@ def preprocess_and_bin(scene, camera, strategy="precise", tau=TAU_DEFAULT, worke
             s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
             if int(s["overflow"]):
                 regrows += 1
-                need = max(int(s["pairs_emitted"]), int(s["list_used"]))
+                need = max(int(s["pairs_emitted"]), 2 * int(s["list_used"]))
                 capacity = max(int(capacity * 1.5) + 16, need)
                 continue
             break
