@@ -43,17 +43,29 @@ def write_ppm(image, path) -> None:
 
 
 def read_ppm(path) -> np.ndarray:
-    """Reads back a P6 file written by ``write_ppm`` (``images.py:27-39``)."""
+    """A binary P6 file with maxval 255, as ``write_ppm`` writes it, back as an
+    ``(H, W, 3)`` uint8 array (the reference's reader: ``images.py:27-39``)."""
     with open(path, "rb") as f:
-        magic = f.readline().strip()
-        if magic != b"P6":
-            raise ValueError(f"not a P6 PPM: {magic!r}")
-        w, h = (int(v) for v in f.readline().split()[:2])
-        maxval = int(f.readline())
-        if maxval != 255:
-            raise ValueError(f"unsupported maxval {maxval}")
-        data = f.read(w * h * 3)
-    return np.frombuffer(data, dtype=np.uint8).reshape(h, w, 3)
+        blob = f.read()
+    # header = three whitespace-separated fields after the magic, then ONE whitespace byte
+    fields, pos = [], 0
+    while len(fields) < 4:
+        while pos < len(blob) and blob[pos:pos + 1].isspace():
+            pos += 1
+        end = pos
+        while end < len(blob) and not blob[end:end + 1].isspace():
+            end += 1
+        fields.append(blob[pos:end])
+        pos = end
+    if fields[0] != b"P6":
+        raise ValueError(f"not a P6 PPM: {fields[0]!r}")
+    width, height, maxval = (int(v) for v in fields[1:])
+    if maxval != 255:
+        raise ValueError(f"unsupported maxval {maxval}")
+    body = blob[pos + 1:pos + 1 + width * height * 3]
+    if len(body) != width * height * 3:
+        raise ValueError("truncated PPM body")
+    return np.frombuffer(body, dtype=np.uint8).reshape(height, width, 3)
 
 
 def png_bytes(image) -> bytes:
