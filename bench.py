@@ -205,9 +205,10 @@ NVIEWS_DEFAULT = 16      # distinct orbit views the timed steps cycle through
 
 def launches_per_frame(bucket, npass, tiles):
     """Kernels of this library one frame launches (tile-bucket: preprocess, [slice totals on
-    grids above 12 K tiles], tile scan, tile order, place, four sort classes, blend)."""
+    grids above 12 K tiles], tile scan, tile order, run scatter, fallback placement, four sort
+    classes, blend)."""
     if bucket:
-        return 10 + (1 if (tiles + 1023) // 1024 > 12 else 0)
+        return 11 + (1 if (tiles + 1023) // 1024 > 12 else 0)
     return 6 + npass
 
 
@@ -418,7 +419,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
         names = ["preprocess", "scan", "emit", "sort_hist"] \
             + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
     kmean = kern.mean(axis=0)
-    ncu_name = {"preprocess": "k_preprocess", "scan": "k_scan_tiles", "emit": "k_place",
+    ncu_name = {"preprocess": "k_preprocess", "scan": "k_scan_tiles", "emit": "k_scatter_runs",
                 "tile_sort": "k_tile_sort", "tile_sort_medium": "k_tile_sort_medium",
                 "tile_sort_large": "k_tile_sort_large", "tile_sort_tail": "k_tile_sort_tail",
                 "blend": "k_blend" if args.exact else "k_blend2"}
@@ -438,9 +439,11 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     M_proc = evals["pairs_processed"] if evals else M
     # algorithmic bytes per launch
     alg = {
-        "preprocess": 236.0 * P + 52.0 * R,
-        # bucket: rect + mask + depth + count + index in, 8 B record out; onesweep: 12 B pair out
-        "emit": 8.0 * M + 24.0 * P if bucket else 12.0 * M + 4.0 * P,
+        # scene in, splat row + depth out; tile-bucket: + the 8 B record of every pair, staged
+        # by run
+        "preprocess": 236.0 * P + 52.0 * R + (8.0 * M if bucket else 0.0),
+        # bucket: the staged records in, the bucketed records out (a copy); onesweep: 12 B pair out
+        "emit": 16.0 * M if bucket else 12.0 * M + 4.0 * P,
         "tile_sort_all": 12.0 * M,          # 8 B record in, 4 B index out, all four classes
         "sort_pass": 24.0 * M,
         "blend": 52.0 * M_proc + 12.0 * W * H,
@@ -452,7 +455,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
         ms_of["sort_pass"] = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass"))) / max(npass, 1)
     clock_mhz = float(props.clock_rate) / 1e3 if getattr(props, "clock_rate", 0) else sm_max
     fp32_peak = sms * 128 * 2 * sm_max * 1e6 / 1e12            # TFLOP/s at the max SM clock
-    kname = {"preprocess": "k_preprocess", "emit": "k_place" if bucket else "k_emit",
+    kname = {"preprocess": "k_preprocess", "emit": "k_scatter_runs" if bucket else "k_emit",
              "tile_sort_all": "k_tile_sort{,_medium,_large,_tail}", "sort_pass": "k_sort_pass",
              "blend": ncu_name["blend"]}
 

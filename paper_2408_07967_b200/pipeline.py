@@ -510,7 +510,7 @@ class Pipeline:
 
     def render_bands(self, camera, group=None, strategy="precise", tau=TAU_DEFAULT,
                      background=(0.0, 0.0, 0.0), *, bands=None, dst=0, out=None, exact=False,
-                     contrib=True, as_numpy=True, sync=True):
+                     contrib=True, as_numpy=True, sync=True, quantized=False):
         """ONE frame split into tile-row bands over the ranks of ``group`` (a
         ``torch.distributed`` process group, default: the world), gathered on rank ``dst``
         (the reference splits a frame's tiles over its worker pool the same
@@ -524,7 +524,10 @@ class Pipeline:
         the other ranks a band-sized buffer.  The receives are posted on a side stream before
         ``dst``'s own band is rendered, the sends are issued right behind each band's blend;
         NCCL send/recv over NVLink, no other collective.  The frame is bit-identical to
-        ``render(camera)`` on one GPU (tiles are independent).
+        ``render(camera)`` on one GPU (tiles are independent).  ``quantized=True`` gathers the
+        frame as uint8 (each rank quantises its band on the device, ``images.py:12-15``):
+        a quarter of the bytes into ``dst``, whose NVLink ingress is what bounds a frame of
+        many bands.
 
         Returns ``(Framebuffer, FrameStats)``: on ``dst`` the whole frame (host array, or the
         device tensor with ``as_numpy=False``), elsewhere the rank's own band rows
@@ -565,12 +568,18 @@ class Pipeline:
             stream = torch.cuda.current_stream(self.device)
             st = C.c_void_p(stream.cuda_stream)
             kcut = self._cutoffs(torch, tau)
+            fdt = torch.uint8 if quantized else torch.float32
+            band_f32 = None
             if rank == dst:
-                full = out if out is not None else torch.empty((H, W, 3), dtype=torch.float32,
-                                                               device=self.device)
-                if tuple(full.shape) != (H, W, 3) or full.dtype != torch.float32 or not full.is_contiguous():
-                    raise ValueError("out must be a contiguous float32 (H, W, 3) CUDA tensor")
-                rows, frame_ptr = None, full.data_ptr()
+                full = out if out is not None else torch.empty((H, W, 3), dtype=fdt, device=self.device)
+                if tuple(full.shape) != (H, W, 3) or full.dtype != fdt or not full.is_contiguous():
+                    raise ValueError(f"out must be a contiguous {fdt} (H, W, 3) CUDA tensor")
+                rows = None
+                if quantized:      # blend into a float band, quantise it into the frame's rows
+                    band_f32 = torch.empty((max(y1 - y0, 0), W, 3), dtype=torch.float32, device=self.device)
+                    frame_ptr = band_f32.data_ptr() - y0 * W * 12
+                else:
+                    frame_ptr = full.data_ptr()
                 # the peers' rows land in place while this rank renders its own band: the
                 # receives go on a side stream that does not wait for the render stream
                 side = self._side_streams(torch, 1)[0]
@@ -579,10 +588,11 @@ class Pipeline:
                     works = sharding.gather_band_rows(full, None, bands, H, rank, dst, group)
             else:
                 full = None
-                rows = torch.empty((max(y1 - y0, 0), W, 3), dtype=torch.float32, device=self.device)
+                rows = torch.empty((max(y1 - y0, 0), W, 3), dtype=fdt, device=self.device)
+                band_f32 = torch.empty_like(rows, dtype=torch.float32) if quantized else rows
                 # the blend addresses pixels by their frame row: shift the base so that row y0
                 # of the frame is row 0 of the band buffer (only rows y0..y1 are written)
-                frame_ptr = rows.data_ptr() - y0 * W * 12
+                frame_ptr = band_f32.data_ptr() - y0 * W * 12
                 works = None
             while True:
                 ws = self._take_ws(torch, W, H, capacity)
@@ -591,6 +601,10 @@ class Pipeline:
                 if b1 >= b0:
                     self._issue(torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1,
                                 C.c_void_p(frame_ptr), None, None, st, False)
+                    if quantized:
+                        q_dst = full[y0:y1] if rank == dst else rows
+                        _capi.check(L.fgs_quantize_rgb8(band_f32.data_ptr(), (y1 - y0) * W * 3,
+                                                        q_dst.data_ptr(), st))
                 if not sync:
                     break
                 ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
@@ -623,7 +637,7 @@ class Pipeline:
                 img = full
             fb_rows = (0, H) if rank == dst else (y0, y1)
             if as_numpy:
-                h = _pinned.take(torch, tuple(img.shape), torch.float32)
+                h = _pinned.take(torch, tuple(img.shape), img.dtype)
                 h.copy_(img, non_blocking=True)
                 stream.synchronize()
                 fb = Framebuffer(_pinned.as_numpy(h), bg)

@@ -409,6 +409,8 @@ def test_render_bands_world1_equals_render():
                                    as_numpy=False, sync=False)
         torch.cuda.synchronize()
         assert fbd.image is out and np.array_equal(out.cpu().numpy(), full.image)
+        fq, _ = pipe.render_bands(cam, background=(0.1, 0.2, 0.3), quantized=True)
+        assert fq.image.dtype == np.uint8 and np.array_equal(fq.image, fgs.images.quantize(full.image))
         with pytest.raises(ValueError):
             pipe.render_bands(cam, bands=[(0, 3), (4, 24)])      # two bands, one rank
     finally:
