@@ -20,6 +20,7 @@
 // alone reproduce the reference's (key, value) order.
 
 #include "fgs_common.cuh"
+#include <type_traits>
 
 // ---------------------------------------------------------------------------
 // per-scene kernels
@@ -456,7 +457,11 @@ struct TileJob {
 enum { WALK_COUNT = 0, WALK_BIN = 1, WALK_EMIT = 2, WALK_PLACE = 3 };
 
 // The CTA's tile table: open addressing, at most FGS_HT_PROBES probes.
-#define FGS_HT_SIZE   1024
+#ifndef FGS_HT_BITS
+#define FGS_HT_BITS   9             // 512 slots: a CTA of a spatially ordered scene fills ~30
+#endif
+#define FGS_HT_SIZE   (1 << FGS_HT_BITS)
+#define FGS_HT_PER    (FGS_HT_SIZE / FGS_PRE_THREADS)   // slots a thread of the epilogue owns
 #define FGS_HT_PROBES 16
 #define FGS_HT_EMPTY  0xffffffffu
 #ifndef FGS_WC_CAP
@@ -473,7 +478,7 @@ struct TileTable {
 
 __device__ __forceinline__ uint32_t ht_hash(uint32_t tile)
 {
-    return (tile * 2654435761u) >> 22;                    // 10 bits
+    return (tile * 2654435761u) >> (32 - FGS_HT_BITS);
 }
 // slot of `tile`, inserting it if absent; -1 when FGS_HT_PROBES slots are taken by others
 __device__ __forceinline__ int ht_insert(TileTable &T, uint32_t tile)
@@ -509,17 +514,26 @@ __device__ __forceinline__ int ht_find(const TileTable &T, uint32_t tile)
 // runs into the tile buckets.  Any other CTA is put on the fallback list and placed by the
 // second walk (k_place), exactly as every CTA was before the stage existed.
 #ifndef FGS_PARK_CAP
-#define FGS_PARK_CAP  2048          // pairs of cooperative-walk Gaussians a regular CTA can park
+#define FGS_PARK_CAP  1920          // pairs of cooperative-walk Gaussians a regular CTA can park
 #endif
 #define FGS_ER_NONE   0xffffffffu
-struct BinSmem {
+// What the walks write: its own shared memory (not the staging buffer), initialised when the
+// CTA starts, so a warp goes from its colours straight into its walk -- no CTA barrier between
+// the geometry and the binning (the warps of a CTA drift apart by then: that barrier held 11 %
+// of the kernel's stall samples).
+struct BinTable {
     TileTable tab;
-    uint16_t eoff[FGS_HT_SIZE];     // offset of table entry e's run in the CTA's record block
     uint32_t park[FGS_PARK_CAP];    // entry | rank << 10 | owner thread << 20
-    uint64_t rec_of[FGS_PRE_THREADS];   // each thread's record: depth bits << 32 | Gaussian index
-    uint64_t wc[FGS_WC_CAP];        // the CTA's records in run order
     uint32_t npark, irregular;
 };
+// What the epilogue adds once every warp's walk is done (and with it every thread's use of the
+// staging buffer, which this aliases).
+struct BinSmem {
+    uint64_t wc[FGS_WC_CAP];        // the CTA's records in run order
+    uint64_t rec_of[FGS_PRE_THREADS];   // each thread's record: depth bits << 32 | Gaussian index
+    uint16_t eoff[FGS_HT_SIZE];     // offset of table entry e's run in the CTA's record block
+};
+struct BinNone {};
 
 // What WALK_BIN / WALK_PLACE work on.
 struct BinCtx {
@@ -825,7 +839,7 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
 }
 
 #ifndef FGS_SH_STAGED
-#define FGS_SH_STAGED 12          // SH float4 planes staged in shared memory (of 12)
+#define FGS_SH_STAGED 11          // SH float4 planes staged in shared memory (of 12)
 #endif
 static_assert(FGS_SH_STAGED * FGS_PRE_THREADS * 16 >= (int)sizeof(BinSmem), "the binning work area aliases the staging buffer");
 __device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
@@ -858,11 +872,21 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     const int g = blockIdx.x * FGS_PRE_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const bool live = g < P;
+    BinSmem &B = *reinterpret_cast<BinSmem *>(s_sh);
+    __shared__ typename std::conditional<BUCKET, BinTable, BinNone>::type s_bt_;
+    BinTable &BT = *reinterpret_cast<BinTable *>(&s_bt_);
+    TileTable &s_tab = BT.tab;
+    if (BUCKET) {
+        for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) {
+            s_tab.key[i] = FGS_HT_EMPTY;
+            s_tab.val[i] = 0u;
+        }
+        if (threadIdx.x == 0) { BT.npark = 0u; BT.irregular = 0u; s_bin[2] = 0u; }
+        __syncthreads();                  // (every warp arrives at once: the CTA has just started)
+    }
     // TILE_BUCKET: this CTA's pairs per tile, their parked ranks and the record block.  The
     // work area takes over the SH staging buffer once every thread has consumed its
     // coefficients (the CTA then needs 48 KB, not 92).
-    BinSmem &B = *reinterpret_cast<BinSmem *>(s_sh);
-    TileTable &s_tab = B.tab;
 
     TileJob job;
     job.cand = 0;
@@ -1044,15 +1068,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     uint32_t er[9];                       // small walk: entry | rank << 16 per tile of the 3 x 3
     const uint64_t rec = ((uint64_t)__float_as_uint(zcam) << 32) | og;
     if (BUCKET) {
-        __syncthreads();                  // every thread is done with the SH staging buffer
-        for (int i = threadIdx.x; i < FGS_HT_SIZE; i += FGS_PRE_THREADS) {
-            s_tab.key[i] = FGS_HT_EMPTY;
-            s_tab.val[i] = 0u;
-        }
-        if (threadIdx.x == 0) { B.npark = 0u; B.irregular = 0u; s_bin[2] = 0u; }
-        B.rec_of[threadIdx.x] = rec;
-        __syncthreads();
-        const BinCtx bc{&s_tab, f.tilecount, B.park, &B.npark, &B.irregular,
+        const BinCtx bc{&s_tab, f.tilecount, BT.park, &BT.npark, &BT.irregular,
                         nullptr, nullptr, nullptr, nullptr, nullptr};
         // rectangles of at most 3 x 3 tiles: each lane walks its own; the rest of the warp's
         // candidates (if any) go through the cooperative walk
@@ -1094,7 +1110,9 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         s_red1[threadIdx.x >> 5] = v1;
         s_red2[threadIdx.x >> 5] = v2;
     }
-    __syncthreads();                      // also: every warp's walk is done, the table is final
+    __syncthreads();                      // also: every warp's walk is done, the table is final,
+                                          // and nobody reads the staging buffer any more
+    if (BUCKET) B.rec_of[threadIdx.x] = rec;      // (read after the run-offset barrier)
     if (threadIdx.x == 0) {
         // one atomic per CTA and counter: every CTA of the grid hits the same three words,
         // and L2 serialises atomics on one address
@@ -1110,16 +1128,16 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     if (!BUCKET) return;
 
     // ---- TILE_BUCKET epilogue: one range per (CTA, tile) in the tile's bucket.  Thread t
-    // owns table slots 4t .. 4t+3; entries go to the frame's table list in slot order, each
+    // owns table slots FGS_HT_PER t .. FGS_HT_PER (t + 1) - 1; entries go to the frame's table list in slot order, each
     // with the offset of its run in the CTA's record block.
     // The global round trips of this epilogue -- the bucket reservations (one atomic per
     // table entry, result needed for the list), the list reservation and the stage
     // reservation (thread 0) -- are issued as early as their operands exist and consumed
     // after the block scans / the placement, which hide them.
-    uint32_t cnt[4], tl[4], gb[4], nent = 0, npr = 0;
+    uint32_t cnt[FGS_HT_PER], tl[FGS_HT_PER], gb[FGS_HT_PER], nent = 0, npr = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const int e = threadIdx.x * 4 + k;
+    for (int k = 0; k < FGS_HT_PER; ++k) {
+        const int e = threadIdx.x * FGS_HT_PER + k;
         tl[k] = s_tab.key[e];
         const bool used = tl[k] != FGS_HT_EMPTY;
         cnt[k] = used ? s_tab.val[e] : 0u;
@@ -1136,7 +1154,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     const unsigned long long tot_pr64 = tot2 & ((1ull << 40) - 1ull);
     uint32_t pr_off = (uint32_t)(off2 & ((1ull << 40) - 1ull));
     // regular: every pair has a table entry and a parked rank, and the record block fits
-    const bool regular = B.irregular == 0u && tot_pr64 <= (unsigned long long)FGS_WC_CAP;
+    const bool regular = BT.irregular == 0u && tot_pr64 <= (unsigned long long)FGS_WC_CAP;
     const uint32_t tot_pr = regular ? (uint32_t)tot_pr64 : 0u;
     uint32_t lb = 0, sb = FGS_CTA_NO_STAGE;
     if (threadIdx.x == 0) {
@@ -1159,8 +1177,8 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         const bool fits = s_bin[1] != 0u;
         uint32_t idx = list_base + ent_off, staged_end = 0;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const int e = threadIdx.x * 4 + k;
+        for (int k = 0; k < FGS_HT_PER; ++k) {
+            const int e = threadIdx.x * FGS_HT_PER + k;
             if (tl[k] != FGS_HT_EMPTY) {
                 const bool wc = (unsigned long long)pr_off + cnt[k] <= (unsigned long long)FGS_WC_CAP;
                 if (wc) staged_end = pr_off + cnt[k];
@@ -1180,8 +1198,8 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     {
         uint32_t o = pr_off;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            if (tl[k] != FGS_HT_EMPTY) B.eoff[threadIdx.x * 4 + k] = (uint16_t)o;
+        for (int k = 0; k < FGS_HT_PER; ++k) {
+            if (tl[k] != FGS_HT_EMPTY) B.eoff[threadIdx.x * FGS_HT_PER + k] = (uint16_t)o;
             o += cnt[k];
         }
     }
@@ -1189,8 +1207,8 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
 #pragma unroll
     for (int k = 0; k < 9; ++k)
         if (er[k] != FGS_ER_NONE) B.wc[B.eoff[er[k] & 0xffffu] + (er[k] >> 16)] = rec;
-    for (uint32_t i = threadIdx.x; i < B.npark; i += FGS_PRE_THREADS) {
-        const uint32_t w = B.park[i];
+    for (uint32_t i = threadIdx.x; i < BT.npark; i += FGS_PRE_THREADS) {
+        const uint32_t w = BT.park[i];
         B.wc[B.eoff[w & 1023u] + ((w >> 10) & 1023u)] = B.rec_of[w >> 20];
     }
     if (threadIdx.x == 0) {               // the two reservations have had the placement to arrive
@@ -1209,10 +1227,10 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     if (s_bin[1]) {
         uint32_t idx = s_bin[0] + ent_off;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
+        for (int k = 0; k < FGS_HT_PER; ++k) {
             if (tl[k] != FGS_HT_EMPTY)
                 f.tablelist[idx++] = make_uint4(tl[k], gb[k], cnt[k],
-                                                ((uint32_t)(threadIdx.x * 4 + k) << 16) | pr_off);
+                                                ((uint32_t)(threadIdx.x * FGS_HT_PER + k) << 16) | pr_off);
             pr_off += cnt[k];
         }
     }
