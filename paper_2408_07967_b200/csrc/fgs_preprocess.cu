@@ -1645,18 +1645,22 @@ k_scatter_runs(const uint4 *__restrict__ ctainfo, const uint4 *__restrict__ tabl
         // four runs per step: their first 32 records are requested together, then stored
         for (int k0 = 0; k0 < n; k0 += 4) {
             uint32_t dst[4], off[4], cnt[4];
-            uint64_t v[4];
+            uint64_t v[4], v2[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 dst[u] = __shfl_sync(FGS_FULL, mydst, (k0 + u) & 31);
                 off[u] = __shfl_sync(FGS_FULL, myoff, (k0 + u) & 31);
                 cnt[u] = k0 + u < n ? __shfl_sync(FGS_FULL, mycnt, (k0 + u) & 31) : 0u;
                 v[u] = lane < cnt[u] ? blk[off[u] + lane] : 0ull;
+                // (a run is ~33 records: its few records beyond 32 go out with the first 32,
+                // not in a dependent second round trip)
+                v2[u] = lane + 32u < cnt[u] ? blk[off[u] + lane + 32u] : 0ull;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (lane < cnt[u]) rec[dst[u] + lane] = v[u];
-                for (uint32_t j = lane + 32u; j < cnt[u]; j += 32u) rec[dst[u] + j] = blk[off[u] + j];
+                if (lane + 32u < cnt[u]) rec[dst[u] + lane + 32u] = v2[u];
+                for (uint32_t j = lane + 64u; j < cnt[u]; j += 32u) rec[dst[u] + j] = blk[off[u] + j];
             }
         }
     }
