@@ -1618,7 +1618,10 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
 // two round trips for up to 32 runs per warp -- and the warp then copies its runs one after
 // the other, 32 records per step (a run of a Morton-ordered scene is ~30 records).  No shared
 // memory, no barrier.
-__global__ void __launch_bounds__(FGS_SCATTER_THREADS)
+#ifndef FGS_SCATTER_MINB
+#define FGS_SCATTER_MINB 12      // 40 registers: the copy is latency-bound, it wants the warps (47 registers: 178 -> 216 us)
+#endif
+__global__ void __launch_bounds__(FGS_SCATTER_THREADS, FGS_SCATTER_MINB)
 k_scatter_runs(const uint4 *__restrict__ ctainfo, const uint4 *__restrict__ tablelist,
                const int32_t *__restrict__ starts, const uint64_t *__restrict__ stage,
                uint64_t *__restrict__ rec, const fgs_stats *__restrict__ stats)
