@@ -51,6 +51,8 @@
 #define FGS_WORK_TAIL_OUT      7   // tail-kernel CTAs past their wait on FGS_WORK_SORT_DONE
 #define FGS_WORK_STAGE_USED    8   // records the preprocess CTAs have reserved in the stage
 #define FGS_WORK_FB_CTAS       9   // preprocess CTAs left to the placement walk (fallback list length)
+#define FGS_WORK_DENSE0       10   // dense tiles the tile scan queued (the medium class splits them; later
+                                   // entries of the dense list -- tiles a class gave up on -- are the tail's)
 #define FGS_CTA_NO_STAGE  0xffffffffu   // ctainfo.w of a CTA whose records were not staged
 // blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
 // empty = last) and the blend's CTAs take them in bin order, so the long tiles start first

@@ -1456,8 +1456,10 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     if (i < tiles) {
         const uint32_t e32 = excl > 0x7fffffffull ? 0x7fffffffu : (uint32_t)excl;
         starts[i] = (int32_t)e32;
-        if (v > FGS_LARGE_TILE)     // queue the bucket for its tile-sort size class
+        if (v > FGS_LARGE_TILE) {   // queue the bucket for its tile-sort size class
             cursor[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE + 1] = (uint32_t)i;
+            atomicAdd(&fgs_work(stats)[FGS_WORK_DENSE0], 1u);
+        }
         else if (v > FGS_DENSE_TILE)
             cursor[(size_t)atomicAdd(&fgs_work(stats)[FGS_WORK_LARGE], 1u) * FGS_CTR_STRIDE + 4] = (uint32_t)i;
         else if (v > FGS_SMALL_TILE)

@@ -705,6 +705,88 @@ __device__ __forceinline__ void ts_sort_tile(TileSortSmem<NT, EMAX> &S, int tile
     }
 }
 
+// A dense bucket (more records than any class's shared memory holds) inside a size-class
+// kernel: the same split as ts_sort_tile's -- one counting pass on the top 8 varying depth bits
+// into `alt` (through L2), consecutive bins grouped into chunks of at most CAP records -- with
+// every chunk sorted by the class's own bucket-rank sort.  Returns false when a chunk cannot
+// be (one bin alone beyond CAP, clustered depths): the caller queues the tile for the tail
+// kernel, which sorts it again from `rec` (untouched here).
+struct SplitSmem {
+    uint32_t sub[257];
+    uint32_t grp[258];
+    uint32_t mm[2];
+    uint32_t ngroups, bad;
+};      // (2 KB: with it the medium class still fits 3 CTAs per SM)
+template <int NT, int EMAX, bool STAGE, int NBDIV>
+__device__ __forceinline__ bool tb_sort_dense(BucketSmem<NT, EMAX, STAGE, NBDIV> &B, SplitSmem &S, int tile,
+                                              const uint64_t *__restrict__ rec, uint64_t *alt,
+                                              uint32_t *__restrict__ vals_out, uint64_t *keys_out,
+                                              const int32_t *__restrict__ starts, int write_keys)
+{
+    constexpr int CAP = BucketSmem<NT, EMAX, STAGE, NBDIV>::CAP;
+    const int tid = threadIdx.x;
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    if (n <= 0) return true;
+    const uint64_t *g = rec + start;
+    uint64_t *a = alt + start;
+    if (tid == 0) { S.mm[0] = 0xffffffffu; S.mm[1] = 0u; S.bad = 0u; }
+    for (int i = tid; i < 257; i += NT) S.sub[i] = 0u;
+    __syncthreads();
+    uint32_t lo = 0xffffffffu, hi = 0u;
+    for (int i = tid; i < n; i += NT) {
+        const uint32_t d = (uint32_t)(g[i] >> 32);
+        lo = d < lo ? d : lo;
+        hi = d > hi ? d : hi;
+    }
+    lo = __reduce_min_sync(FGS_FULL, lo);
+    hi = __reduce_max_sync(FGS_FULL, hi);
+    if ((tid & 31) == 0) { atomicMin(&S.mm[0], lo); atomicMax(&S.mm[1], hi); }
+    __syncthreads();
+    const uint32_t diff = S.mm[0] ^ S.mm[1];
+    const int top = diff ? 31 - __clz((int)diff) : 0;        // highest varying depth bit
+    const int sh = top > 7 ? top - 7 : 0;                     // bin = depth bits [sh, sh+8)
+    for (int i = tid; i < n; i += NT)
+        atomicAdd(&S.sub[1 + (((uint32_t)(g[i] >> 32) >> sh) & 0xffu)], 1u);
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t run = 0;
+        for (int d = 0; d <= 256; ++d) { run += S.sub[d]; S.sub[d] = run; }
+        uint32_t k = 0;
+        S.grp[0] = 0;
+        for (uint32_t d = 0; d < 256; ++d)
+            if (S.sub[d + 1] - S.sub[S.grp[k]] > (uint32_t)CAP && d > S.grp[k]) S.grp[++k] = d;
+        S.grp[++k] = 256;
+        S.ngroups = k;
+        for (uint32_t j = 0; j < k; ++j)
+            if (S.sub[S.grp[j + 1]] - S.sub[S.grp[j]] > (uint32_t)CAP) S.bad = 1u;
+    }
+    __syncthreads();
+    if (S.bad) return false;                                  // uniform
+    uint32_t *cur = B.bin;                                    // scatter cursors (B is idle until the chunks)
+    static_assert(BucketSmem<NT, EMAX, STAGE, NBDIV>::NB >= 256, "cursor array");
+    if (tid < 256) cur[tid] = S.sub[tid];
+    __syncthreads();
+    for (int i = tid; i < n; i += NT) {
+        const uint64_t r = g[i];
+        a[atomicAdd(&cur[((uint32_t)(r >> 32) >> sh) & 0xffu], 1u)] = r;
+    }
+    __syncthreads();
+    const int ngroups = (int)S.ngroups;
+    const uint64_t tile_hi = (uint64_t)(uint32_t)tile << 32;
+    for (int k = 0; k < ngroups; ++k) {
+        const int b0 = (int)S.sub[S.grp[k]];
+        const int m = (int)S.sub[S.grp[k + 1]] - b0;
+        if (m == 0) continue;                                 // uniform
+        // keys_out may alias alt: a chunk is consumed (staged / scattered into shared memory)
+        // before its slice is overwritten
+        if (!tb_sort_range<NT, EMAX, STAGE, NBDIV>(B, a + b0, m, start + b0, tile_hi, vals_out, keys_out,
+                                                   write_keys))
+            return false;
+        __syncthreads();
+    }
+    return true;
+}
+
 // Persistent size-class kernels: CTA b sorts list entry b first and then takes further
 // entries from a ticket counter (the frame's zeroed work block: word `slot` = tickets drawn,
 // word `slot + 1` = CTAs that have left) -- tiles of one class differ 2x in size, and a
@@ -811,9 +893,9 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
 #define FGS_MED_EMAX (4096 / FGS_MED_NT)
 __global__ void __launch_bounds__(FGS_MED_NT, FGS_MED_MINB)
 k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
-                   uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
+                   uint64_t *keys_out, const int32_t *__restrict__ starts,
                    const uint32_t *__restrict__ list, uint32_t *__restrict__ hard_list,
-                   int write_keys, fgs_stats *__restrict__ stats)
+                   uint32_t *dense_list, int write_keys, fgs_stats *__restrict__ stats)
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>;
@@ -824,14 +906,27 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     fgs_pdl_trigger();
     if (stats->overflow) return;
     __shared__ uint32_t s_ticket;
-    const uint32_t count = stats->medium_tiles;
+    __shared__ SplitSmem s_split;
+    // The dense tiles the scan queued come first (the longest jobs of the whole sort: split in
+    // place, chunk by chunk, beside the other classes -- left to the tail kernel they were 61 us
+    // of a mostly idle GPU on the 10M / 4K frame), then the medium list.
+    const uint32_t nd0 = fgs_work(stats)[FGS_WORK_DENSE0];
+    const uint32_t count = nd0 + stats->medium_tiles;
     TileTickets tk;
     if (!tk.open(stats, FGS_WORK_MEDIUM_TICKET, count)) return;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
-        const int tile = (int)list[(size_t)i * FGS_CTR_STRIDE];
-        if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
-            threadIdx.x == 0)
-            hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+        if (i < nd0) {
+            const int tile = (int)dense_list[(size_t)i * FGS_CTR_STRIDE];
+            if (!tb_sort_dense<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>(
+                    S, s_split, tile, rec, keys_out, vals_out, keys_out, starts, write_keys) &&
+                threadIdx.x == 0)      // back of the dense list: the tail kernel's share
+                dense_list[(size_t)atomicAdd(&stats->dense_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+        } else {
+            const int tile = (int)list[(size_t)(i - nd0) * FGS_CTR_STRIDE];
+            if (!tb_sort_tile<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>(S, tile, rec, vals_out, keys_out, starts, write_keys) &&
+                threadIdx.x == 0)
+                hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+        }
         __syncthreads();
     }
     tk.close(stats, 1u);
@@ -887,7 +982,7 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
     __shared__ uint32_t s_joined;
     if (threadIdx.x == 0) {
         uint32_t *work = fgs_work(stats);
-        const uint32_t need = (stats->medium_tiles ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u);
+        const uint32_t need = ((stats->medium_tiles | work[FGS_WORK_DENSE0]) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u);
         volatile uint32_t *done = work + FGS_WORK_SORT_DONE;
         uint32_t ok = 1u;
         for (uint32_t spin = 0; (*done & need) != need; ++spin) {
@@ -904,10 +999,13 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
     }
     __syncthreads();
     if (!s_joined) return;
-    const uint32_t ndense = stats->dense_tiles, nhard = stats->hard_tiles;
+    // (the dense tiles the scan queued were split by the medium class; what it or the large
+    // class could not sort sits behind them in the dense list)
+    const uint32_t nd0 = fgs_work(stats)[FGS_WORK_DENSE0];
+    const uint32_t ndense = stats->dense_tiles - nd0, nhard = stats->hard_tiles;
     for (uint32_t i = blockIdx.x; i < ndense + nhard; i += gridDim.x) {
         const bool dense = i < ndense;
-        const int tile = (int)(dense ? dense_list[(size_t)i * FGS_CTR_STRIDE]
+        const int tile = (int)(dense ? dense_list[(size_t)(nd0 + i) * FGS_CTR_STRIDE]
                                      : hard_list[(size_t)(i - ndense) * FGS_CTR_STRIDE]);
         ts_sort_tile<256, 16, true>(S, tile, rec, alt, vals_out, keys_out, starts, write_keys,
                                     dense ? B : nullptr);
@@ -972,7 +1070,7 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     cfg.attrs = pdl;
     {
         FGS_CHAIN(k_tile_sort_medium, dim3(mgrid), dim3(FGS_MED_NT), sizeof(MediumSmem), st,
-                  f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, write_keys, f.stats);
+                  f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, dense_list, write_keys, f.stats);
         FGS_AFTER_LAUNCH(st);
     }
     {
