@@ -465,8 +465,11 @@ enum { WALK_COUNT = 0, WALK_BIN = 1, WALK_EMIT = 2, WALK_PLACE = 3 };
 #define FGS_HT_PROBES 16
 #define FGS_HT_EMPTY  0xffffffffu
 #ifndef FGS_WC_CAP
-#define FGS_WC_CAP    3072          // records the CTA's write-combining buffer holds
+#define FGS_WC_CAP    3072          // records the placement walk's write-combining buffer holds
 #endif
+#ifndef FGS_BLOCK_CAP
+#define FGS_BLOCK_CAP 5120          // records of a regular preprocess CTA (its block in the stage);
+#endif                              // with rec_of and eoff it fills the 44 KB staging buffer it aliases
 #ifndef FGS_PLACE_MINBLOCKS
 #define FGS_PLACE_MINBLOCKS 4
 #endif
@@ -508,7 +511,7 @@ __device__ __forceinline__ int ht_find(const TileTable &T, uint32_t tile)
 }
 
 // K1 (TILE_BUCKET) work area; takes over the SH staging buffer once the colours are done.
-// A "regular" CTA -- every pair found a table entry, at most FGS_WC_CAP pairs, at most
+// A "regular" CTA -- every pair found a table entry, at most FGS_BLOCK_CAP pairs, at most
 // FGS_PARK_CAP of them from Gaussians on the cooperative walk -- leaves K1 with its records
 // already grouped by (CTA, tile) run in the frame's stage, and K3 is a streaming copy of those
 // runs into the tile buckets.  Any other CTA is put on the fallback list and placed by the
@@ -529,7 +532,7 @@ struct BinTable {
 // What the epilogue adds once every warp's walk is done (and with it every thread's use of the
 // staging buffer, which this aliases).
 struct BinSmem {
-    uint64_t wc[FGS_WC_CAP];        // the CTA's records in run order
+    uint64_t wc[FGS_BLOCK_CAP];     // the CTA's records in run order
     uint64_t rec_of[FGS_PRE_THREADS];   // each thread's record: depth bits << 32 | Gaussian index
     uint16_t eoff[FGS_HT_SIZE];     // offset of table entry e's run in the CTA's record block
 };
@@ -1154,7 +1157,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
     const unsigned long long tot_pr64 = tot2 & ((1ull << 40) - 1ull);
     uint32_t pr_off = (uint32_t)(off2 & ((1ull << 40) - 1ull));
     // regular: every pair has a table entry and a parked rank, and the record block fits
-    const bool regular = BT.irregular == 0u && tot_pr64 <= (unsigned long long)FGS_WC_CAP;
+    const bool regular = BT.irregular == 0u && tot_pr64 <= (unsigned long long)FGS_BLOCK_CAP;
     const uint32_t tot_pr = regular ? (uint32_t)tot_pr64 : 0u;
     uint32_t lb = 0, sb = FGS_CTA_NO_STAGE;
     if (threadIdx.x == 0) {
