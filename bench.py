@@ -181,6 +181,53 @@ def cpu_arm(act, cam, steps, warmup, budget_s=30.0):
                       "tests/golden)"}
 
 
+def tilesplat_arm(scene_mod, names=("c1", "c2"), budget_s=40.0):
+    """The UNMODIFIED reference package (`tilesplat`, pure Python + numba) timed through its own
+    public call, `Pipeline(scene).render(camera, workers=...)`, on BASELINE configs[0] and
+    configs[1] -- when it is installed under baseline/_ref (git-ignored; `python
+    __graft_entry__.py` installs it from /root/reference where that exists, and the directory
+    travels to the GPU box with the snapshot).  Beside each time: the oracle port on the same
+    input, and whether the two frames are bit-identical on this box."""
+    ref_dir = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_dir, "tilesplat")):
+        return {"unavailable": "baseline/_ref/tilesplat is not installed on this box"}
+    try:
+        sys.path.insert(0, ref_dir)
+        import tilesplat
+    except Exception as e:                                   # numba missing, ...
+        return {"unavailable": f"import tilesplat failed: {e!r}"[:200]}
+    from oracle import oracle as orc
+    import dataclasses
+    cores = os.cpu_count() or 1
+    out = {"package": f"tilesplat {getattr(tilesplat, '__version__', '?')} from baseline/_ref",
+           "workers": cores}
+    for name in names:
+        act, w, h, desc = make_scene(scene_mod, name)
+        cam = scene_mod.orbit_cameras(1, 24.0, w, h)[0]
+        r_scene = tilesplat.ActivatedScene(**{f.name: getattr(act, f.name)
+                                              for f in dataclasses.fields(tilesplat.ActivatedScene)})
+        r_cam = tilesplat.Camera(**{f.name: getattr(cam, f.name)
+                                    for f in dataclasses.fields(tilesplat.Camera)})
+        pipe = tilesplat.Pipeline(r_scene)
+        pipe.render(r_cam, workers=cores)                     # numba JIT + warm-up
+        rec = {"workload": desc}
+        for label, wk in (("ms_per_frame", cores), ("ms_per_frame_workers1", 1)):
+            ts, t0 = [], time.perf_counter()
+            while len(ts) < 5 and (not ts or time.perf_counter() - t0 < budget_s / 4):
+                t = time.perf_counter()
+                fb, st = pipe.render(r_cam, workers=wk)
+                ts.append(time.perf_counter() - t)
+            rec[label] = 1e3 * float(np.median(ts))
+        oimg, ost = orc.render(act, cam)
+        _, ost = orc.render(act, cam)
+        rec["oracle_port_ms_per_frame"] = ost["total_ns"] / 1e6
+        rec["port_frame_bit_identical_to_reference"] = bool(
+            np.array_equal(np.asarray(fb.image).view(np.uint32), np.asarray(oimg).view(np.uint32)))
+        rec["pairs_emitted"] = int(st.pairs_emitted)
+        out[name] = rec
+    return out
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -197,6 +244,10 @@ def run_reference(args, rank):
         "cpu_baseline": cb,
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        line["tilesplat"] = tilesplat_arm(scene_mod)
+    except Exception as e:                                   # never lose the arm's own line
+        line["tilesplat"] = {"unavailable": f"{e!r}"[:200]}
     print(json.dumps(line), flush=True)
 
 

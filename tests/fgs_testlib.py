@@ -78,3 +78,43 @@ def identity_camera(width=64, height=64, focal=None, position=(0.0, 0.0, 0.0)):
     from paper_2408_07967_b200.scene import make_camera
     focal = focal if focal is not None else width / 2
     return make_camera(width, height, position, np.eye(3), focal, focal)
+
+
+_TILESPLAT = []
+
+
+def load_tilesplat():
+    """The UNMODIFIED reference package, or None: from a scratch copy of /root/reference (build
+    container; nothing is written under the read-only tree), else from baseline/_ref (the
+    git-ignored `pip install --target` of the same tree that travels to the GPU box)."""
+    if _TILESPLAT:
+        return _TILESPLAT[0]
+    import importlib
+    import shutil
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    src = "/root/reference/pkg/src/tilesplat"
+    mod = None
+    if os.path.isdir(src):
+        d = tempfile.mkdtemp(prefix="fgs_ref_")
+        shutil.copytree(src, os.path.join(d, "tilesplat"), ignore=shutil.ignore_patterns("__pycache__"))
+        os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(d, "numba_cache"))
+        where = d
+    elif os.path.isdir(os.path.join(root, "baseline", "_ref", "tilesplat")):
+        where = os.path.join(root, "baseline", "_ref")
+    else:
+        _TILESPLAT.append(None)
+        return None
+    old = sys.dont_write_bytecode
+    sys.dont_write_bytecode = True
+    sys.path.insert(0, where)
+    try:
+        mod = importlib.import_module("tilesplat")
+    except Exception:                              # numba / pillow missing on this box
+        mod = None
+    finally:
+        sys.path.remove(where)
+        sys.dont_write_bytecode = old
+    _TILESPLAT.append(mod)
+    return mod

@@ -171,28 +171,11 @@ def test_integration_doc_structs_match_the_library():
 # ---------------------------------------------------------------------------
 @pytest.fixture(scope="module")
 def tilesplat():
-    src = "/root/reference/pkg/src/tilesplat"
-    if not os.path.isdir(src):
-        pytest.skip("reference tree not present on this box")
-    import importlib
-    import shutil
-    import sys
-    d = tempfile.mkdtemp(prefix="fgs_ref_")
-    shutil.copytree(src, os.path.join(d, "tilesplat"),
-                    ignore=shutil.ignore_patterns("__pycache__"))
-    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(d, "numba_cache"))
-    old = sys.dont_write_bytecode
-    sys.dont_write_bytecode = True
-    sys.path.insert(0, d)
-    try:
-        mod = importlib.import_module("tilesplat")
-    except Exception as e:                         # numba / pillow missing on this box
-        pytest.skip(f"reference not importable here: {e}")
-    finally:
-        sys.path.remove(d)
-        sys.dont_write_bytecode = old
-    yield mod
-    shutil.rmtree(d, ignore_errors=True)
+    from fgs_testlib import load_tilesplat
+    mod = load_tilesplat()
+    if mod is None:
+        pytest.skip("reference package not present / not importable on this box")
+    return mod
 
 
 def test_reference_objects_pass_the_boundary_unchanged(tilesplat):
