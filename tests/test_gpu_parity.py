@@ -946,3 +946,33 @@ def test_cuda_path_against_the_reference_package(preset, n, seed, w, h, radius, 
     for s in (st, stx):
         assert (s.pairs_emitted, s.pairs_contributing, s.tiles_nonempty, s.gaussians_retained) == \
             (rst.pairs_emitted, rst.pairs_contributing, rst.tiles_nonempty, rst.gaussians_retained)
+
+
+def test_dense_tile_with_a_depth_cluster_falls_back_mid_way():
+    """One tile far above the largest sort class (> 8192 pairs): the medium class splits it by
+    depth and sorts chunk after chunk; here one chunk holds 3000 pairs of a single depth, which
+    the bucket-rank sort gives up on AFTER earlier chunks were written -- the tile goes to the
+    tail kernel and is sorted again from the untouched records.  Order must still be the
+    reference's (depth, then index: sorting.py:3-5)."""
+    rng = np.random.default_rng(77)
+    n_spread, n_same = 9500, 3000
+    n = n_spread + n_same
+    cam = identity_camera(16, 16, focal=8)
+    z = np.concatenate([rng.uniform(5.0, 15.0, n_spread), np.full(n_same, 10.0)])
+    rng.shuffle(z)
+    xy = rng.uniform(-0.6, 0.6, size=(n, 2)) * z[:, None]
+    scene = make_raw_scene(np.concatenate([xy, z[:, None]], axis=1),
+                           rng.uniform(0.05, 0.3, size=(n, 3)), rng.uniform(0.1, 0.9, size=n),
+                           dc=rng.uniform(-1, 1, size=(n, 3)))
+    act = fgs.activate(scene)
+    ob = orc.preprocess_and_bin(act, cam)
+    ok, ov = orc.sort_pairs(ob.keys, ob.values, ob.grid_w * ob.grid_h, n)
+    assert ob.grid_w * ob.grid_h == 1 and ok.size > 8192
+    pipe = fgs.Pipeline(act)
+    for _ in range(2):                                     # the frame's work counters rewind
+        keys, vals, starts = fgs.sorted_pairs(pipe, cam)
+        assert np.array_equal(keys, ok) and np.array_equal(vals, ov)
+    fb, st = pipe.render(cam, exact=True)
+    oimg, ost = orc.render(act, cam)
+    assert np.array_equal(fb.image.view(np.uint32), oimg.view(np.uint32))
+    assert st.pairs_contributing == ost["pairs_contributing"]
