@@ -468,8 +468,8 @@ enum { WALK_COUNT = 0, WALK_BIN = 1, WALK_EMIT = 2, WALK_PLACE = 3 };
 #define FGS_WC_CAP    3072          // records the placement walk's write-combining buffer holds
 #endif
 #ifndef FGS_BLOCK_CAP
-#define FGS_BLOCK_CAP 5120          // records of a regular preprocess CTA (its block in the stage);
-#endif                              // with rec_of and eoff it fills the 44 KB staging buffer it aliases
+#define FGS_BLOCK_CAP 4608          // records of a regular preprocess CTA (its block in the stage);
+#endif                              // with rec_of and eoff it fills the 40 KB staging buffer it aliases
 #ifndef FGS_PLACE_MINBLOCKS
 #define FGS_PLACE_MINBLOCKS 4
 #endif
@@ -517,7 +517,8 @@ __device__ __forceinline__ int ht_find(const TileTable &T, uint32_t tile)
 // runs into the tile buckets.  Any other CTA is put on the fallback list and placed by the
 // second walk (k_place), exactly as every CTA was before the stage existed.
 #ifndef FGS_PARK_CAP
-#define FGS_PARK_CAP  1920          // pairs of cooperative-walk Gaussians a regular CTA can park
+#define FGS_PARK_CAP  2944          // pairs of cooperative-walk Gaussians a regular CTA can park
+                                    // (1920: a quarter of the 8K frame's CTAs overflowed it)
 #endif
 #define FGS_ER_NONE   0xffffffffu
 // What the walks write: its own shared memory (not the staging buffer), initialised when the
@@ -842,7 +843,8 @@ __device__ __forceinline__ void sh_basis(float x, float y, float z, float *bz)
 }
 
 #ifndef FGS_SH_STAGED
-#define FGS_SH_STAGED 11          // SH float4 planes staged in shared memory (of 12)
+#define FGS_SH_STAGED 10          // SH float4 planes staged in shared memory (of 12): 40 KB, which
+                                  // leaves 16 KB of the CTA's 56 for the tile table and the parked ranks
 #endif
 static_assert(FGS_SH_STAGED * FGS_PRE_THREADS * 16 >= (int)sizeof(BinSmem), "the binning work area aliases the staging buffer");
 __device__ __forceinline__ void cp_async16_pre(void *smem, const void *gmem)
