@@ -258,8 +258,9 @@ def launches_per_frame(bucket, npass, tiles):
     """Kernels of this library one frame launches (tile-bucket: preprocess, [slice totals on
     grids above 12 K tiles], tile scan, tile order, run scatter, fallback placement, four sort
     classes, blend)."""
-    if bucket:
-        return 11 + (1 if (tiles + 1023) // 1024 > 12 else 0)
+    if bucket:      # k_preprocess, k_scan_tiles, k_tile_order, k_scatter_runs, k_place, k_tile_sort_medium,
+                    # k_tile_sort_large, k_tile_sort, k_tile_sort_tail, k_blend2 (+ k_tile_blocksums)
+        return 10 + (1 if (tiles + 1023) // 1024 > 12 else 0)
     return 6 + npass
 
 
