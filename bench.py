@@ -200,7 +200,7 @@ def tilesplat_arm(scene_mod, names=("c1", "c2"), budget_s=40.0):
     import dataclasses
     cores = os.cpu_count() or 1
     out = {"package": f"tilesplat {getattr(tilesplat, '__version__', '?')} from baseline/_ref",
-           "workers": cores}
+           "workers": cores, "os_cpu_count": os.cpu_count()}
     for name in names:
         act, w, h, desc = make_scene(scene_mod, name)
         cam = scene_mod.orbit_cameras(1, 24.0, w, h)[0]
@@ -212,12 +212,18 @@ def tilesplat_arm(scene_mod, names=("c1", "c2"), budget_s=40.0):
         pipe.render(r_cam, workers=cores)                     # numba JIT + warm-up
         rec = {"workload": desc}
         for label, wk in (("ms_per_frame", cores), ("ms_per_frame_workers1", 1)):
-            ts, t0 = [], time.perf_counter()
+            ts, best, t0 = [], None, time.perf_counter()
             while len(ts) < 5 and (not ts or time.perf_counter() - t0 < budget_s / 4):
                 t = time.perf_counter()
-                fb, st = pipe.render(r_cam, workers=wk)
+                fb, st = pipe.render(r_cam, "precise", workers=wk)
                 ts.append(time.perf_counter() - t)
+                if best is None or st.total_ns < best.total_ns:
+                    best = st
             rec[label] = 1e3 * float(np.median(ts))
+            # best frame's FrameStats.total_ns and its three stage times
+            rec[label.replace("ms_per_frame", "best_stats_ms")] = {
+                "total": best.total_ns / 1e6, "preprocess_bin": best.preprocess_bin_ns / 1e6,
+                "sort": best.sort_ns / 1e6, "render": best.render_ns / 1e6, "frames": len(ts)}
         oimg, ost = orc.render(act, cam)
         _, ost = orc.render(act, cam)
         rec["oracle_port_ms_per_frame"] = ost["total_ns"] / 1e6
