@@ -127,7 +127,9 @@ class _PinnedPool:
 
     def __init__(self):
         self._free = {}
-        self._lock = threading.Lock()
+        # re-entrant: give() runs from a weakref finalizer, i.e. possibly from a garbage
+        # collection that starts while this very thread holds the lock in take() / give()
+        self._lock = threading.RLock()
 
     def take(self, torch, shape, dtype):
         key = (tuple(shape), str(dtype))
