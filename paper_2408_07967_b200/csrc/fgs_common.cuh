@@ -20,7 +20,7 @@
 // ---- launch shapes ---------------------------------------------------------
 #define FGS_PRE_THREADS   256      // K1 / K3: one Gaussian per thread
 #ifndef FGS_PRE_MINBLOCKS
-#define FGS_PRE_MINBLOCKS 4        // K1 resident CTAs per SM the register budget targets (59 regs, no spills)
+#define FGS_PRE_MINBLOCKS 4        // K1 resident CTAs per SM the register budget targets (64 registers; 5: 48 + 256 B of spills, slower)
 #endif
 #define FGS_SORT_THREADS  256
 #define FGS_SORT_IPT      16
