@@ -260,13 +260,14 @@ def run_reference(args, rank):
 NVIEWS_DEFAULT = 16      # distinct orbit views the timed steps cycle through
 
 
-def launches_per_frame(bucket, npass, tiles):
+def launches_per_frame(bucket, npass, tiles, lazy=False):
     """Kernels of this library one frame launches (tile-bucket: preprocess, [slice totals on
     grids above 12 K tiles], tile scan, tile order, run scatter, fallback placement, four sort
-    classes, blend)."""
+    classes, blend; lazy_sort: + the full sort and the second blend pass of the redo list)."""
     if bucket:      # k_preprocess, k_scan_tiles, k_tile_order, k_scatter_runs, k_place, k_tile_sort_medium,
-                    # k_tile_sort_large, k_tile_sort, k_tile_sort_tail, k_blend2 (+ k_tile_blocksums)
-        return 10 + (1 if (tiles + 1023) // 1024 > 12 else 0)
+                    # k_tile_sort_large | k_tile_front, k_tile_sort, k_tile_sort_tail, k_blend2
+                    # (+ k_tile_blocksums) (+ k_tile_sort_redo, k_blend2<redo>)
+        return 10 + (1 if (tiles + 1023) // 1024 > 12 else 0) + (2 if lazy else 0)
     return 6 + npass
 
 
@@ -285,7 +286,8 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     gh, gw = -(-H // 16), -(-W // 16)
 
     pipe = fgs.Pipeline(act, sort_mode=args.sort_mode,
-                        spatial_order=False if args.no_spatial else None)
+                        spatial_order=False if args.no_spatial else None,
+                        lazy_sort=not args.no_lazy)
     L = _capi.lib()
     hbm_peak, peak_src, sm_max = peaks()
     props = torch.cuda.get_device_properties(dev)
@@ -308,17 +310,19 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     del fb
     stream = torch.cuda.current_stream(dev)
     bucket = args.sort_mode == "tile-bucket"
+    lazy = bool(pipe.lazy_sort)             # (the pipeline drops it when fronts mostly fail)
+    front_tiles, redo_tiles = int(st.front_tiles), int(st.redo_tiles)
     nlanes = max(1, args.streams)
     lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nlanes - 1)]
     wss = []
     for _ in range(nlanes):
         w_ = pipe._take_ws(torch, W, H, pipe._default_capacity())
-        w_.set_mode(_capi.SORT_MODES[args.sort_mode])
+        w_.set_mode(_capi.SORT_MODES[args.sort_mode], lazy_sort=lazy)
         wss.append(w_)
     lay = wss[0].lay
     T_tiles = int(lay.tiles)
     npass = 0 if bucket else int(lay.sort_passes)
-    n_marks = 8 if bucket else 6 + npass
+    n_marks = (10 if lazy else 8) if bucket else 6 + npass
     camcs = [_capi.camera_struct(c) for c in my_cams]
     cam0c = _capi.camera_struct(cam0)
     kcut = pipe._cutoffs(torch, 1.0 / 255.0)
@@ -471,8 +475,9 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     # ---- per-kernel records and rooflines ------------------------------------------
     if bucket:
         # launch order of the size classes: persistent kernels first (fgs_launch_tile_sort)
-        names = ["preprocess", "scan", "emit", "tile_sort_medium", "tile_sort_large",
-                 "tile_sort", "tile_sort_tail", "blend"]
+        names = ["preprocess", "scan", "emit", "tile_sort_medium",
+                 "tile_front" if lazy else "tile_sort_large",
+                 "tile_sort", "tile_sort_tail", "blend"] + (["redo_sort", "redo_blend"] if lazy else [])
     else:
         names = ["preprocess", "scan", "emit", "sort_hist"] \
             + [f"sort_pass{p}" for p in range(npass)] + ["ranges", "blend"]
@@ -480,6 +485,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     ncu_name = {"preprocess": "k_preprocess", "scan": "k_scan_tiles", "emit": "k_scatter_runs",
                 "tile_sort": "k_tile_sort", "tile_sort_medium": "k_tile_sort_medium",
                 "tile_sort_large": "k_tile_sort_large", "tile_sort_tail": "k_tile_sort_tail",
+                "tile_front": "k_tile_front", "redo_sort": "k_tile_sort_redo",
                 "blend": "k_blend" if args.exact else "k_blend2"}
     prof_all = profiled_kernels(name)
     kernels = []
@@ -506,15 +512,19 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
         "sort_pass": 24.0 * M,
         "blend": 52.0 * M_proc + 12.0 * W * H,
     }
-    ms_of = {"preprocess": float(kmean[0]), "emit": float(kmean[2]), "blend": float(kmean[-1])}
+    ib = names.index("blend")
+    # lazy_sort: the redo list's full sort counts with the sort, its second blend pass with the blend
+    ms_of = {"preprocess": float(kmean[0]), "emit": float(kmean[2]),
+             "blend": float(kmean[ib] + (kmean[ib + 2] if lazy and bucket else 0.0))}
     if bucket:
-        ms_of["tile_sort_all"] = float(kmean[3:-1].sum())
+        ms_of["tile_sort_all"] = float(kmean[3:ib].sum() + (kmean[ib + 1] if lazy else 0.0))
     else:
         ms_of["sort_pass"] = float(sum(k["ms"] for k in kernels if k["name"].startswith("sort_pass"))) / max(npass, 1)
     clock_mhz = float(props.clock_rate) / 1e3 if getattr(props, "clock_rate", 0) else sm_max
     fp32_peak = sms * 128 * 2 * sm_max * 1e6 / 1e12            # TFLOP/s at the max SM clock
     kname = {"preprocess": "k_preprocess", "emit": "k_scatter_runs" if bucket else "k_emit",
-             "tile_sort_all": "k_tile_sort{,_medium,_large,_tail}", "sort_pass": "k_sort_pass",
+             "tile_sort_all": "k_tile_sort{,_medium,_tail} + k_tile_front + k_tile_sort_redo" if lazy
+                              else "k_tile_sort{,_medium,_large,_tail}", "sort_pass": "k_sort_pass",
              "blend": ncu_name["blend"]}
 
     def roof_of(key):
@@ -550,7 +560,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
             ach = alg[key] / (ms * 1e-3) / 1e9
             r = {"kernel": kname[key], "bound": "hbm", "achieved": ach, "peak": hbm_peak,
                  "unit": "GB/s", "frac": ach / hbm_peak, "traffic": None,
-                 "launches_per_step": {"tile_sort_all": 4, "sort_pass": npass}.get(key, 1),
+                 "launches_per_step": {"tile_sort_all": 5 if lazy else 4, "sort_pass": npass}.get(key, 1),
                  "ms_per_launch": ms, "alg_bytes_per_launch": alg[key], "peak_source": peak_src}
         if hit:
             r["traffic"] = hit[0]["dram_bytes"]
@@ -586,6 +596,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
                    "tau": 1.0 / 255.0, "sh_degree": 3, "gaussians": P, "width": W, "height": H,
                    "pairs": M, "pairs_processed": M_proc, "retained": R, "tiles": T_tiles,
                    "sort_mode": args.sort_mode, "sort_passes": npass,
+                   "lazy_sort": lazy, "front_tiles": front_tiles, "redo_tiles": redo_tiles,
                    "blend": "exact" if args.exact else "ex2.approx+guard",
                    "streams": nlanes,
                    "distinct_views": 1 if bands_mode else len(my_cams) * world,
@@ -613,7 +624,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
                 "render_call_quantized_ms": render_call.get("quantized"),
                 "render_call_api": "blocking Pipeline.render(camera) per view (the reference's entry "
                                    "point): float32 host frame / uint8 host frame"},
-        "gpu_launches": int(launches_per_frame(bucket, npass, T_tiles) * K),
+        "gpu_launches": int(launches_per_frame(bucket, npass, T_tiles, lazy) * K),
         "roofline": roof,
         "rooflines": rooflines,
         "cpu_baseline": cpu,
@@ -643,6 +654,8 @@ def main():
     ap.add_argument("--sort-mode", default="tile-bucket", choices=["tile-bucket", "onesweep"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-also", action="store_true", help="skip the extra configs[1] run")
+    ap.add_argument("--no-lazy", action="store_true",
+                    help="sort every tile in full (fgs_layout.lazy_sort = 0)")
     ap.add_argument("--no-spatial", action="store_true",
                     help="keep the scene in the caller's order (no Morton slot order)")
     ap.add_argument("--streams", type=int, default=3,

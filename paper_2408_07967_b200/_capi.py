@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 # FGS_LIB selects another build of the same library (tuning variants, see build.py)
 LIB_PATH = os.environ.get("FGS_LIB") or os.path.join(HERE, "_lib", "libflashgs_b200.so")
 
-ABI_VERSION = 5
+ABI_VERSION = 6
 STRATEGIES = ("baseline-circle-aabb", "tight-aabb", "precise")   # binning.py:38 order
 STRATEGY_ID = {"precise": 0, "tight-aabb": 1, "baseline-circle-aabb": 2}
 BLEND_EXACT, BLEND_CONTRIB, BLEND_SCALAR = 1, 2, 4
@@ -51,11 +51,14 @@ class FgsStats(C.Structure):
                 ("unsorted", C.c_uint32), ("tile_out_of_grid", C.c_uint32),
                 ("candidate_tiles_lo", C.c_uint32), ("candidate_tiles_hi", C.c_uint32),
                 ("dense_tiles", C.c_uint32), ("medium_tiles", C.c_uint32),
-                ("hard_tiles", C.c_uint32), ("list_used", C.c_uint32)]
+                ("hard_tiles", C.c_uint32), ("list_used", C.c_uint32),
+                ("front_tiles", C.c_uint32), ("redo_tiles", C.c_uint32),
+                ("reserved_a", C.c_uint32), ("reserved_b", C.c_uint32)]
 
 
 STATS_DTYPE = np.dtype([(n, np.uint32) for n, _ in FgsStats._fields_])
-assert STATS_DTYPE.itemsize == C.sizeof(FgsStats) == 64
+assert STATS_DTYPE.itemsize == C.sizeof(FgsStats) == 80
+STATS_BYTES = STATS_DTYPE.itemsize
 
 
 class FgsLayout(C.Structure):
@@ -75,7 +78,9 @@ class FgsLayout(C.Structure):
                 ("grid_h", C.c_int32), ("tiles", C.c_int32), ("tile_bits", C.c_int32),
                 ("preprocess_blocks", C.c_int32), ("sort_passes", C.c_int32),
                 ("sort_mode", C.c_int32), ("sorted_keys_in", C.c_int32),
-                ("sorted_vals_in", C.c_int32), ("keep_sorted_keys", C.c_int32)]
+                ("sorted_vals_in", C.c_int32), ("keep_sorted_keys", C.c_int32),
+                ("lazy_sort", C.c_int32), ("reserved0", C.c_int32),
+                ("off_front", C.c_uint64)]
 
 
 class FgsError(RuntimeError):

@@ -123,7 +123,32 @@ struct BlendSmem {
 // pairs visited before the tile's last pixel stops (M_proc of SURVEY.md 8(d)).  The
 // warp-level culls are switched off so that every live pixel classifies every pair
 // itself.  evals[0..3] = the four classes, [4] = M_proc, [5] = pixels.
-template <bool EXACT, bool CONTRIB, bool EXTRAS, bool COUNT = false>
+// lazy_sort (both blend kernels).  `limit` (first pass): only the first limit[tile] pairs of
+// the tile's bucket are in order; a tile whose pixels are not all finished when that front is
+// used up is appended to `redo_list` and NOT written (nor counted) -- the second pass, REDO,
+// takes the tiles of that list in full with persistent CTAs after k_tile_sort_redo has sorted
+// them.  The last CTA of the second pass publishes stats->redo_tiles and rewinds the cursor,
+// so the stage can be re-issued on the frame.
+template <typename Body>
+__device__ __forceinline__ void blend_redo_pass(fgs_stats *stats, const uint32_t *redo_list, Body body)
+{
+    uint32_t *work = fgs_work(stats);
+    const uint32_t cnt = work[FGS_WORK_REDO];
+    for (uint32_t it = blockIdx.x; it < cnt; it += gridDim.x) {
+        body((int)redo_list[it]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&work[FGS_WORK_REDO_OUT], 1u) == gridDim.x - 1u) {
+            stats->redo_tiles = cnt;
+            work[FGS_WORK_REDO] = 0u;
+            work[FGS_WORK_REDO_OUT] = 0u;
+        }
+    }
+}
+
+template <bool EXACT, bool CONTRIB, bool EXTRAS, bool COUNT = false, bool REDO = false>
 __global__ void __launch_bounds__(256)
 k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
@@ -131,17 +156,18 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         int height, int grid_w, int first_tile, float bg0, float bg1, float bg2, float tau,
         float *__restrict__ rgb, float *__restrict__ alpha_out, float *__restrict__ depth_out,
         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats,
-        unsigned long long *__restrict__ evals = nullptr)
+        unsigned long long *__restrict__ evals = nullptr,
+        const int32_t *__restrict__ limit = nullptr, uint32_t *__restrict__ redo_list = nullptr)
 {
     __shared__ BlendSmem S;
     __shared__ uint32_t s_mproc;
-    uint32_t ev_rect = 0, ev_cut = 0, ev_alpha = 0, ev_blend = 0, visited = 0;
+    if (REDO) fgs_pdl_wait();
     if (COUNT && threadIdx.x == 0) s_mproc = 0u;
     if (stats != nullptr && stats->overflow) return;   // frame is re-run with a larger buffer
     const int tid = threadIdx.x;
-    // CTA i takes the i-th tile of the blend order (heaviest first), or of the band in
-    // raster order when no order was built
-    const int tile = order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x;
+    if (tid < 32) S.tab[tid] = c_exp2_tab[tid];
+    const auto tile_body = [&](const int tile) {
+    uint32_t ev_rect = 0, ev_cut = 0, ev_alpha = 0, ev_blend = 0, visited = 0;
     const int ty = tile / grid_w, tx = tile - ty * grid_w;
     // each warp owns an 8x4 pixel block (squarer than 16x2, so fewer splat
     // rectangles reach it); lanes run row-major inside the block
@@ -161,8 +187,14 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
     const uint32_t band_lo = __float_as_uint(tau * (1.0f - 1e-5f));
     const uint32_t band_span = __float_as_uint(tau * (1.0f + 1e-5f)) - band_lo;
 
-    const int start = starts[tile], n = starts[tile + 1] - start;
-    if (tid < 32) S.tab[tid] = c_exp2_tab[tid];
+    const int start = starts[tile];
+    int n = starts[tile + 1] - start;
+    bool cut = false, done_all = false;       // lazy_sort: only a sorted front of the tile exists
+    if (!REDO && limit != nullptr) {
+        const int l = limit[tile];
+        cut = l < n;
+        n = cut ? l : n;
+    }
 
     float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f, dz = 0.0f;
     uint32_t ncontrib = 0;
@@ -294,9 +326,14 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
             }
         }
         idx_next = idx_next2;
-        if (all_done) { ++b; break; }
+        if (all_done) { done_all = true; ++b; break; }
     }
     cp_async_wait<0>();
+    if (cut && !done_all) {                   // uniform: the sorted front was not enough
+        if (tid == 0) redo_list[atomicAdd(&fgs_work(stats)[FGS_WORK_REDO], 1u)] = (uint32_t)tile;
+        return;
+    }
+    if (cut) n = starts[tile + 1] - start;
     if (CONTRIB)   // pairs behind a whole-tile early exit never touched a pixel
         for (int i = b * FGS_BLEND_BATCH + tid; i < n; i += FGS_BLEND_BATCH) contrib[start + i] = 0;
 
@@ -339,6 +376,14 @@ k_blend(const float *__restrict__ splat, const float *__restrict__ gdepth,
         }
         __syncthreads();
         if (tid == 0 && s_mproc) atomicAdd(&evals[4], (unsigned long long)s_mproc);
+    }
+    };  // tile_body
+    if (REDO) {
+        blend_redo_pass(stats, redo_list, tile_body);
+    } else {
+        // CTA i takes the i-th tile of the blend order (heaviest first), or of the band in
+        // raster order when no order was built
+        tile_body(order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x);
     }
 }
 
@@ -420,7 +465,7 @@ __device__ __noinline__ float2 alpha_exact_pair(const float4 *row, float fx, flo
                        alpha_exact(r0, r1, r2, fx, fy1, tau, tab));
 }
 
-template <bool CONTRIB, bool EXTRAS>
+template <bool CONTRIB, bool EXTRAS, bool REDO = false>
 __global__ void __launch_bounds__(FGS_B2_THREADS, FGS_B2_MINCTAS)
 k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
          const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
@@ -428,7 +473,8 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
          int height, int grid_w, int first_tile,
          float bg0, float bg1, float bg2, float tau, float *__restrict__ rgb,
          float *__restrict__ alpha_out, float *__restrict__ depth_out,
-         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats)
+         uint8_t *__restrict__ contrib, fgs_stats *__restrict__ stats,
+         const int32_t *__restrict__ limit, uint32_t *__restrict__ redo_list)
 {
     __shared__ Blend2Smem S;
     fgs_pdl_wait();            // (the tail sort kernel before it is launched the plain way and
@@ -439,13 +485,14 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
     const int tid = threadIdx.x;
     const int lane = tid & 31, wq = tid >> 5;
     if (tid < 32) S.tab[tid] = c_exp2_tab[tid];
-    uint32_t ncontrib = 0;
     // CTA i takes the i-th tile of the blend order (heaviest first: longest-first list
     // scheduling by the hardware's in-order CTA dispatch), or of the band in raster order.
     // (Persistent CTAs pulling tiles from a ticket counter were slower: 72 registers, and the
     // per-tile prologue no longer overlaps other CTAs' blending -- 197 us against 177 on C2.)
-    const int tile = order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x;
+    const int tile0 = REDO ? 0 : (order ? (int)order[blockIdx.x] : first_tile + (int)blockIdx.x);
     if (over) return;                                    // uniform: grow and re-run
+    const auto tile_body = [&](const int tile) {
+    uint32_t ncontrib = 0;
     const int ty = tile / grid_w, tx = tile - ty * grid_w;
     const int bx = tx * FGS_TILE + (wq & 1) * 8, by = ty * FGS_TILE + (wq >> 1) * 8;
     const int px = bx + (lane & 7), py0 = by + (lane >> 3), py1 = py0 + 4;
@@ -460,7 +507,14 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
     float fy0 = inside0 ? (float)py0 + 0.5f : kInf, fy1 = inside1 ? (float)py1 + 0.5f : kInf;
     constexpr float kL = -1.4426950408889634f;       // -log2(e)
 
-    const int start = starts[tile], n = starts[tile + 1] - start;
+    const int start = starts[tile];
+    int n = starts[tile + 1] - start;
+    bool cut = false, done_all = false;       // lazy_sort: only a sorted front of the tile exists
+    if (!REDO && limit != nullptr) {
+        const int l = limit[tile];
+        cut = l < n;
+        n = cut ? l : n;
+    }
 
     pk2 T2 = pk(1.0f, 1.0f), cr2 = pk(0.0f, 0.0f), cg2 = cr2, cb2 = cr2, dz2 = cr2;
 
@@ -590,9 +644,14 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
             }
         }
         idx_next = idx_next2;
-        if (all_done) { ++b; break; }
+        if (all_done) { done_all = true; ++b; break; }
     }
     cp_async_wait<0>();
+    if (cut && !done_all) {                   // uniform: the sorted front was not enough
+        if (tid == 0) redo_list[atomicAdd(&fgs_work(stats)[FGS_WORK_REDO], 1u)] = (uint32_t)tile;
+        return;
+    }
+    if (cut) n = starts[tile + 1] - start;
     if (CONTRIB)
         for (int i = b * B + tid; i < n; i += B) contrib[start + i] = 0;
 
@@ -626,40 +685,47 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
         ncontrib = __reduce_add_sync(FGS_FULL, ncontrib);
         if (lane == 0 && ncontrib) atomicAdd(&stats->pairs_contributing, ncontrib);
     }
+    };  // tile_body
+    if (REDO) blend_redo_pass(stats, redo_list, tile_body);
+    else tile_body(tile0);
 }
 
-template <bool CONTRIB>
+template <bool CONTRIB, bool REDO>
 int launch2(bool extras, dim3 grid, cudaStream_t st, const float *splat, const float *gdepth,
             const uint32_t *vals, const uint32_t *inv, const int32_t *starts, const uint32_t *order,
             int width, int height,
             int grid_w, int first_tile, const float bg[3], float tau, float *rgb, float *alpha,
-            float *depth, uint8_t *contrib, fgs_stats *stats)
+            float *depth, uint8_t *contrib, fgs_stats *stats, const int32_t *limit, uint32_t *redo_list)
 {
     if (extras)
-        FGS_CHAIN((k_blend2<CONTRIB, true>), grid, dim3(FGS_B2_THREADS), 0, st, splat, gdepth, vals, inv,
+        FGS_CHAIN((k_blend2<CONTRIB, true, REDO>), grid, dim3(FGS_B2_THREADS), 0, st, splat, gdepth, vals, inv,
                   starts, order, width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha,
-                  depth, contrib, stats);
+                  depth, contrib, stats, limit, redo_list);
     else
-        FGS_CHAIN((k_blend2<CONTRIB, false>), grid, dim3(FGS_B2_THREADS), 0, st, splat, gdepth, vals, inv,
+        FGS_CHAIN((k_blend2<CONTRIB, false, REDO>), grid, dim3(FGS_B2_THREADS), 0, st, splat, gdepth, vals, inv,
                   starts, order, width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha,
-                  depth, contrib, stats);
+                  depth, contrib, stats, limit, redo_list);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
 
-template <bool EXACT, bool CONTRIB>
+template <bool EXACT, bool CONTRIB, bool REDO>
 int launch(bool extras, dim3 grid, cudaStream_t st, const float *splat, const float *gdepth,
            const uint32_t *vals, const uint32_t *inv, const int32_t *starts, const uint32_t *order,
            int width, int height, int grid_w,
            int first_tile, const float bg[3], float tau, float *rgb, float *alpha, float *depth,
-           uint8_t *contrib, fgs_stats *stats)
+           uint8_t *contrib, fgs_stats *stats, const int32_t *limit, uint32_t *redo_list)
 {
+    unsigned long long *no_evals = nullptr;
+    // (the second pass is chained: it starts with griddepcontrol.wait)
     if (extras)
-        k_blend<EXACT, CONTRIB, true><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, order, width,
-            height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+        FGS_CHAIN((k_blend<EXACT, CONTRIB, true, false, REDO>), grid, dim3(256), 0, st, splat, gdepth, vals, inv,
+                  starts, order, width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha,
+                  depth, contrib, stats, no_evals, limit, redo_list);
     else
-        k_blend<EXACT, CONTRIB, false><<<grid, 256, 0, st>>>(splat, gdepth, vals, inv, starts, order, width,
-            height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha, depth, contrib, stats);
+        FGS_CHAIN((k_blend<EXACT, CONTRIB, false, false, REDO>), grid, dim3(256), 0, st, splat, gdepth, vals, inv,
+                  starts, order, width, height, grid_w, first_tile, bg[0], bg[1], bg[2], tau, rgb, alpha,
+                  depth, contrib, stats, no_evals, limit, redo_list);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
@@ -671,25 +737,36 @@ int fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *va
                      int width, int height,
                      const float bg[3], double tau,
                      int flags, int band0, int band1, float *rgb, float *alpha, float *depth,
-                     uint8_t *contrib, fgs_stats *stats, cudaStream_t st)
+                     uint8_t *contrib, fgs_stats *stats, cudaStream_t st,
+                     const int32_t *limit, uint32_t *redo_list, int redo)
 {
     const int grid_w = (width + FGS_TILE - 1) / FGS_TILE;
     if (band1 < band0) return FGS_OK;
-    const dim3 grid((unsigned)(grid_w * (band1 - band0 + 1)));
+    if ((limit != nullptr || redo) && (redo_list == nullptr || stats == nullptr)) return FGS_E_ARG;
+    dim3 grid((unsigned)(grid_w * (band1 - band0 + 1)));
+    if (redo) {
+        // persistent CTAs over the redo list (its length is only known on the device)
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const unsigned want = (unsigned)(4 * sms);
+        grid = dim3(grid.x < want ? grid.x : want);
+    }
     const int first_tile = band0 * grid_w;
     const bool exact = flags & FGS_BLEND_EXACT, want_contrib = (flags & FGS_BLEND_CONTRIB) && contrib;
     const bool extras = (alpha != nullptr) || (depth != nullptr && gdepth != nullptr);
     if (depth != nullptr && gdepth == nullptr) return FGS_E_ARG;
     const float tau32 = (float)tau;
-#define FGS_GO(E, C) launch<E, C>(extras, grid, st, splat, gdepth, vals, inv, starts, order, width, height, \
-                                  grid_w, first_tile, bg, tau32, rgb, alpha, depth, contrib, stats)
+#define FGS_ARGS extras, grid, st, splat, gdepth, vals, inv, starts, order, width, height, \
+                 grid_w, first_tile, bg, tau32, rgb, alpha, depth, contrib, stats, limit, redo_list
+#define FGS_GO(E, C) (redo ? launch<E, C, true>(FGS_ARGS) : launch<E, C, false>(FGS_ARGS))
     if (exact) return want_contrib ? FGS_GO(true, true) : FGS_GO(true, false);
     if (flags & FGS_BLEND_SCALAR) return want_contrib ? FGS_GO(false, true) : FGS_GO(false, false);
 #undef FGS_GO
-#define FGS_GO2(C) launch2<C>(extras, grid, st, splat, gdepth, vals, inv, starts, order, width, height, \
-                              grid_w, first_tile, bg, tau32, rgb, alpha, depth, contrib, stats)
+#define FGS_GO2(C) (redo ? launch2<C, true>(FGS_ARGS) : launch2<C, false>(FGS_ARGS))
     return want_contrib ? FGS_GO2(true) : FGS_GO2(false);
 #undef FGS_GO2
+#undef FGS_ARGS
 }
 
 // Diagnostic pass over a finished frame's sorted pairs: the exact-mode blend with the

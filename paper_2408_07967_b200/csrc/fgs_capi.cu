@@ -48,6 +48,12 @@ static CamDev make_cam(const fgs_camera *c)
     return d;
 }
 
+// lazy_sort as the launchers take it: 0 off, else which tiles get a front only
+static int fgs_lazy(const fgs_layout *L)
+{
+    return (L->lazy_sort && !L->keep_sorted_keys && L->sort_mode == FGS_SORT_TILE_BUCKET) ? FGS_LAZY_LEVEL : 0;
+}
+
 static int check_frame(const fgs_layout *L, const fgs_camera *c)
 {
     if (!L) return FGS_E_ARG;
@@ -222,6 +228,7 @@ int fgs_workspace_layout(int64_t P, int32_t width, int32_t height, int64_t capac
     L->off_hist = take((FGS_SORT_MAXPASS * 256 + FGS_SORT_MAXPASS) * 4);
     L->off_starts = take(((uint64_t)L->tiles + 1) * 4);
     L->off_contrib = take(cap);
+    L->off_front = take((uint64_t)L->tiles * 8);
     L->total_bytes = off;
     return fgs_layout_set_sort_mode(L, FGS_SORT_TILE_BUCKET);
 }
@@ -306,7 +313,7 @@ int fgs_sort(void *ws, const fgs_layout *L, uint32_t epoch, void *stream)
     if (!ws || !L || epoch == 0) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
     if (L->sort_mode == FGS_SORT_TILE_BUCKET)
-        return fgs_launch_tile_sort(f, L->tiles, L->keep_sorted_keys, (cudaStream_t)stream);
+        return fgs_launch_tile_sort(f, L->tiles, L->keep_sorted_keys, fgs_lazy(L), (cudaStream_t)stream);
     const SortPlan plan = fgs_sort_plan(L->tile_bits, 0, 1);
     if (plan.npass != L->sort_passes) return FGS_E_WORKSPACE;
     return fgs_launch_sort(f.keys, f.vals, &f.stats->pairs_in_buffer, L->capacity, plan,
@@ -330,12 +337,19 @@ int fgs_blend(const void *packed, const float bg[3], double tau, int32_t flags, 
     if (band0 < 0 || band1 >= L->grid_h) return FGS_E_ARG;
     if (L->gaussians && !packed) return FGS_E_ARG;
     FrameDev f = fgs_frame_view(ws, L);
-    return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in],
-                            fgs_scene_view(packed, L->gaussians).inv, f.starts,
-                            L->sort_mode == FGS_SORT_TILE_BUCKET ? f.tileorder + FGS_ORDER_HDR : nullptr,
-                            L->width, L->height,
-                            bg, tau, flags, band0, band1, out_rgb, out_alpha, out_depth, f.contrib,
-                            f.stats, (cudaStream_t)stream);
+    const int lazy = fgs_lazy(L);
+    const uint32_t *inv = fgs_scene_view(packed, L->gaussians).inv;
+    const uint32_t *order = L->sort_mode == FGS_SORT_TILE_BUCKET ? f.tileorder + FGS_ORDER_HDR : nullptr;
+    int rc = fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in], inv, f.starts, order,
+                              L->width, L->height, bg, tau, flags, band0, band1, out_rgb, out_alpha,
+                              out_depth, f.contrib, f.stats, (cudaStream_t)stream,
+                              lazy ? f.limit : nullptr, lazy ? f.redo_list : nullptr, 0);
+    if (rc || !lazy) return rc;
+    // the tiles that had not saturated at the end of their sorted front: full sort, blended again
+    if ((rc = fgs_launch_tile_sort_redo(f, L->tiles, (cudaStream_t)stream))) return rc;
+    return fgs_launch_blend(f.splat, f.depth, f.vals[L->sorted_vals_in], inv, f.starts, order,
+                            L->width, L->height, bg, tau, flags, band0, band1, out_rgb, out_alpha,
+                            out_depth, f.contrib, f.stats, (cudaStream_t)stream, nullptr, f.redo_list, 1);
 }
 
 int fgs_blend_counts(const void *packed, const float bg[3], double tau, int32_t band0, int32_t band1,

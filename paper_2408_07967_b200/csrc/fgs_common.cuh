@@ -42,7 +42,7 @@
 #define FGS_DENSE_TILE    4096      // medium: 2049..4096
 #define FGS_LARGE_TILE    8192      // large: 4097..8192; beyond: dense (entry i of the large
                                     // list at cursor[i*FGS_CTR_STRIDE + 4])
-// internal work counters live behind the public 64-byte stats block (the block is 256
+// internal work counters live behind the public 80-byte stats block (the block is 256
 // bytes in the workspace and zeroed with it at the start of every frame)
 #define FGS_WORK_LARGE    0
 #define FGS_WORK_MEDIUM_TICKET 2   // (+1: CTAs out) tile tickets of the persistent sort kernels
@@ -53,6 +53,8 @@
 #define FGS_WORK_FB_CTAS       9   // preprocess CTAs left to the placement walk (fallback list length)
 #define FGS_WORK_DENSE0       10   // dense tiles the tile scan queued (the medium class splits them; later
                                    // entries of the dense list -- tiles a class gave up on -- are the tail's)
+#define FGS_WORK_REDO     11   // lazy_sort: cursor of the redo list (tiles unsaturated at the end of their front)
+#define FGS_WORK_REDO_OUT 12   // lazy_sort: CTAs of the second blend pass that have left
 #define FGS_CTA_NO_STAGE  0xffffffffu   // ctainfo.w of a CTA whose records were not staged
 // blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
 // empty = last) and the blend's CTAs take them in bin order, so the long tiles start first
@@ -137,6 +139,8 @@ struct FrameDev {
     uint4    *ctainfo;      // [preprocess blocks] (list base, entries, records, stage base or
                             // FGS_CTA_NO_STAGE)
     uint32_t *tileorder;    // [FGS_ORDER_HDR + tiles]: bin counts, bin cursors, blend tile order
+    int32_t  *limit;        // [tiles] lazy_sort: sorted pairs at the head of each tile's bucket
+    uint32_t *redo_list;    // [tiles] lazy_sort: tiles to sort in full and blend again
     uint32_t list_capacity;
 };
 
@@ -169,6 +173,8 @@ static inline FrameDev fgs_frame_view(void *ws, const fgs_layout *L)
     f.fb_list = f.blockbase;
     f.ctainfo = (uint4 *)(b + L->off_ctainfo);
     f.tileorder = (uint32_t *)(b + L->off_tileorder);
+    f.limit = (int32_t *)(b + L->off_front);
+    f.redo_list = (uint32_t *)(b + L->off_front) + L->tiles;
     f.list_capacity = (uint32_t)(L->capacity / 2);          // 16-byte entries in 8 B x capacity
     return f;
 }
@@ -194,7 +200,12 @@ int  fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaS
 int  fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st);
 int  fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
                      int band1, int bucket, const FrameDev &f, cudaStream_t st);
-int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st);
+int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, int lazy, cudaStream_t st);
+int  fgs_launch_tile_sort_redo(const FrameDev &f, int tiles, cudaStream_t st);
+// lazy_sort: which tiles get a front only (1: beyond FGS_DENSE_TILE pairs, 2: beyond FGS_SMALL_TILE)
+#ifndef FGS_LAZY_LEVEL
+#define FGS_LAZY_LEVEL 1
+#endif
 
 struct SortPlan {
     int npass;
@@ -209,12 +220,17 @@ int  fgs_launch_sort(uint64_t *keys[2], uint32_t *vals[2], const uint32_t *n_dev
                      uint32_t epoch, cudaStream_t st);
 int  fgs_launch_ranges(const uint64_t *keys, const uint32_t *n_dev, int64_t n_max, int tiles,
                        int32_t *starts, fgs_stats *stats, cudaStream_t st);
+// `limit` / `redo_list` (lazy_sort, both or neither): pairs sorted at the head of each tile;
+// a tile unsaturated at the end of its front is appended to redo_list (cursor:
+// stats->redo_tiles) and left unwritten.  `redo` = the second pass: the tiles of redo_list,
+// in full, by persistent CTAs.
 int  fgs_launch_blend(const float *splat, const float *gdepth, const uint32_t *vals,
                       const uint32_t *inv, const int32_t *starts, const uint32_t *order,
                       int width, int height,
                       const float bg[3],
                       double tau, int flags, int band0, int band1, float *rgb, float *alpha,
-                      float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st);
+                      float *depth, uint8_t *contrib, fgs_stats *stats, cudaStream_t st,
+                      const int32_t *limit = nullptr, uint32_t *redo_list = nullptr, int redo = 0);
 
 int  fgs_launch_blend_counts(const float *splat, const uint32_t *vals, const uint32_t *inv,
                              const int32_t *starts, int width, int height, const float bg[3],

@@ -853,7 +853,8 @@ struct TileTickets {
 __global__ void __launch_bounds__(256, 6)
 k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
             uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
-            uint32_t *__restrict__ hard_list, int write_keys, fgs_stats *__restrict__ stats)
+            uint32_t *__restrict__ hard_list, int write_keys, fgs_stats *__restrict__ stats,
+            int32_t *__restrict__ limit, int front_min)
 {
     // one buffer, two instantiations: up to 1024 records with 4 per thread, up to 2048 with 8
     // (35 KB, still 6 CTAs per SM; the grid's dynamic CTA dispatch balances these tiles
@@ -863,6 +864,9 @@ k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
     const int tile = blockIdx.x;
     const int n = starts[tile + 1] - starts[tile];
     if (over) return;
+    // lazy_sort: this grid visits every tile, so it is the one that marks the tiles sorted in
+    // full (the front kernel writes the entry of every tile beyond front_min itself)
+    if (limit != nullptr && threadIdx.x == 0 && n <= front_min) limit[tile] = 0x7fffffff;
     if (n <= 0 || n > FGS_SMALL_TILE) return;
     const bool ok = n <= BucketSmem<256, 4>::CAP
         ? tb_sort_tile<256, 4, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 4, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
@@ -895,7 +899,7 @@ __global__ void __launch_bounds__(FGS_MED_NT, FGS_MED_MINB)
 k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
                    uint64_t *keys_out, const int32_t *__restrict__ starts,
                    const uint32_t *__restrict__ list, uint32_t *__restrict__ hard_list,
-                   uint32_t *dense_list, int write_keys, fgs_stats *__restrict__ stats)
+                   uint32_t *dense_list, int write_keys, fgs_stats *__restrict__ stats, int lazy)
 {
     extern __shared__ __align__(16) unsigned char ts_raw[];
     using Smem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>;
@@ -910,8 +914,10 @@ k_tile_sort_medium(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals
     // The dense tiles the scan queued come first (the longest jobs of the whole sort: split in
     // place, chunk by chunk, beside the other classes -- left to the tail kernel they were 61 us
     // of a mostly idle GPU on the 10M / 4K frame), then the medium list.
-    const uint32_t nd0 = fgs_work(stats)[FGS_WORK_DENSE0];
-    const uint32_t count = nd0 + stats->medium_tiles;
+    // (lazy_sort: the dense tiles -- and with lazy == 2 the medium ones too -- are the front
+    // kernel's; this kernel still opens the chain for the classes launched behind it)
+    const uint32_t nd0 = lazy ? 0u : fgs_work(stats)[FGS_WORK_DENSE0];
+    const uint32_t count = nd0 + (lazy == 2 ? 0u : stats->medium_tiles);
     TileTickets tk;
     if (!tk.open(stats, FGS_WORK_MEDIUM_TICKET, count)) return;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
@@ -957,6 +963,219 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
     tk.close(stats, 2u);
 }
 
+
+// ---- lazy_sort: the front of a heavy tile ------------------------------------------------
+// Front-to-back compositing stops once every pixel of a tile is opaque (render.py:154, 178,
+// 228-229), and a tile holding thousands of pairs is opaque after a few hundred of them
+// (measured on every benchmark frame: the last pair any pixel consumes sits at position
+// 200-400 in the median heavy tile, beyond 1024 in at most 2 % of them -- tools/lazy_probe.py
+// -- while heavy tiles hold 75-97 % of a frame's pairs).  So of a heavy tile only the nearest
+// pairs are put in order: every record whose depth bin lies at or below the bin that takes the
+// cumulative count past FGS_FRONT_MIN.  Bins are a monotone function of the depth bits, so this
+// front is exactly the head of the tile's fully sorted list, F records long; limit[tile] = F
+// tells the blend where the sorted part ends.  A tile that has not saturated by then goes on
+// the redo list: k_tile_sort_redo sorts it in full and the blend composites it again from
+// scratch (fgs_launch_blend_redo), so the frame never depends on the guess.
+//
+// Per tile: the depth range from a strided sample of 512 records (depths outside it clamp to
+// the end bins, which keeps the map monotone), one pass that counts every record into 2048
+// linear depth bins (shared-memory RED, no return value needed), a scan, one pass that
+// scatters the front's records bin-contiguously into shared memory, and the in-bin ranking of
+// those F records only.  Two reads of the bucket, ~17 instructions per record, against three
+// reads and ~60 for the full bucket-rank sort; 33 KB of shared memory and 32 registers, so
+// four 512-thread CTAs per SM hide the reads.
+#ifndef FGS_FRONT_NT
+#define FGS_FRONT_NT   512
+#endif
+#ifndef FGS_FRONT_MINB
+#define FGS_FRONT_MINB 3         // 42 registers: 16 of them hold the thread's depth words
+#endif
+#ifndef FGS_FRONT_CAP
+#define FGS_FRONT_CAP  3072      // records a front may hold (24 KB)
+#endif
+#ifndef FGS_FRONT_MIN
+#define FGS_FRONT_MIN  1024      // the front ends with the bin that takes it to at least this many
+#endif
+#ifndef FGS_FRONT_E
+#define FGS_FRONT_E    16        // depth words a thread keeps in registers (one chunk = 8192 records)
+#endif
+#define FGS_FRONT_LOW  256       // a front cut short of a clustered bin must still hold this many
+#define FGS_FRONT_NB   2048
+struct FrontSmem {
+    uint64_t b[FGS_FRONT_CAP];
+    uint32_t bin[FGS_FRONT_NB + 1];
+    uint32_t red[64];
+    int32_t  pick[2];
+};
+
+// Returns F, the number of sorted records now at vals_out[start, start + F); 0 = gave up
+// (one depth bin alone overflows the front: clustered depths -- the redo path sorts the tile).
+// Every thread of the CTA calls it with the same arguments; n >= FGS_FRONT_NT.
+//
+// A bucket of up to NT * FGS_FRONT_E records (8192: the large class, 3/4 of the pairs of the
+// 10M / 4K frame) is read ONCE: every thread keeps the depth words of its FGS_FRONT_E records
+// in registers -- all their loads in flight together -- takes the exact depth range from them,
+// counts them, and after the scan fetches the full record only of those that made the front.
+// Larger buckets go through the same code chunk by chunk, twice (range from a strided sample).
+__device__ __forceinline__ int front_sort_tile(FrontSmem &S, int tile, const uint64_t *__restrict__ rec,
+                                               uint32_t *__restrict__ vals_out,
+                                               const int32_t *__restrict__ starts)
+{
+    constexpr int NT = FGS_FRONT_NT, NB = FGS_FRONT_NB, E = FGS_FRONT_E, CH = NT * E;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int start = starts[tile], n = starts[tile + 1] - start;
+    const uint64_t *g = rec + start;
+    const uint32_t *gd = reinterpret_cast<const uint32_t *>(g) + 1;     // depth word of record i: gd[2 i]
+    const bool one = n <= CH;                                 // uniform
+    uint32_t dreg[E];
+    const auto load_chunk = [&](int c0) {
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const int i = c0 + tid + k * NT;
+            dreg[k] = i < n ? gd[2 * i] : 0xffffffffu;
+        }
+    };
+
+    // 1. depth range: exact from the registers, or of a strided sample (depths outside it
+    // clamp to the end bins, which keeps the map monotone)
+    {
+        uint32_t lo = 0xffffffffu, hi = 0u;
+        if (one) {
+            load_chunk(0);
+#pragma unroll
+            for (int k = 0; k < E; ++k) {
+                if (tid + k * NT < n) {
+                    lo = dreg[k] < lo ? dreg[k] : lo;
+                    hi = dreg[k] > hi ? dreg[k] : hi;
+                }
+            }
+        } else {
+            lo = hi = gd[2 * (int)(((int64_t)tid * n) / NT)];
+        }
+        lo = __reduce_min_sync(FGS_FULL, lo);
+        hi = __reduce_max_sync(FGS_FULL, hi);
+        if (lane == 0) { S.red[w] = lo; S.red[32 + w] = hi; }
+    }
+    for (int i = tid; i <= NB; i += NT) S.bin[i] = 0u;
+    __syncthreads();
+    uint32_t lo = 0xffffffffu, hi = 0u;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) {
+        lo = S.red[i] < lo ? S.red[i] : lo;
+        hi = S.red[32 + i] > hi ? S.red[32 + i] : hi;
+    }
+    // bin = (depth bits - lo) >> sh with the smallest shift that maps the range below NB:
+    // monotone, one instruction, and between NB / 2 and NB bins in use
+    const uint32_t range = hi - lo;
+    const int sh = range < (uint32_t)NB ? 0 : 32 - __clz((int)(range >> 11));
+    static_assert(FGS_FRONT_NB == 2048, "shift = bits of (range >> log2 NB)");
+    const auto bin_of = [&](uint32_t d) -> uint32_t {
+        return ((d < lo ? lo : (d > hi ? hi : d)) - lo) >> sh;
+    };
+
+    // 2. count every record into its bin
+    for (int c0 = 0; c0 < n; c0 += CH) {
+        if (!one) load_chunk(c0);
+#pragma unroll
+        for (int k = 0; k < E; ++k)
+            if (c0 + tid + k * NT < n) atomicAdd(&S.bin[1 + bin_of(dreg[k])], 1u);
+    }
+    __syncthreads();
+
+    // 3. bin offsets: inclusive scan of bin[1..NB] in place (bin[0] = 0), and the front's last bin
+    {
+        constexpr int PER = NB / NT;                          // consecutive bins per thread
+        uint32_t v[PER], sum = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            v[k] = S.bin[1 + tid * PER + k];
+            sum += v[k];
+        }
+        const uint32_t incl = warp_incl_scan(sum, lane);
+        if (lane == 31) S.red[w] = incl;
+        __syncthreads();
+        const uint32_t wsum = lane < NT / 32 ? S.red[lane] : 0u;
+        const uint32_t wincl = warp_incl_scan(wsum, lane);
+        uint32_t run = __shfl_sync(FGS_FULL, wincl - wsum, w) + incl - sum;
+        const uint32_t want = (uint32_t)(n < FGS_FRONT_MIN ? n : FGS_FRONT_MIN);
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int bn = tid * PER + k;                     // bin bn = [run, run + v[k])
+            const uint32_t end = run + v[k];
+            if (run < want && end >= want) {                  // exactly one bin of the tile
+                int bf = bn, F = (int)end;
+                if (end > (uint32_t)FGS_FRONT_CAP) {
+                    if (run >= (uint32_t)FGS_FRONT_LOW) { bf = bn - 1; F = (int)run; }
+                    else { bf = -1; F = 0; }
+                }
+                S.pick[0] = bf;
+                S.pick[1] = F;
+            }
+            S.bin[1 + bn] = end;
+            run = end;
+        }
+    }
+    __syncthreads();
+    const int bf = S.pick[0], F = S.pick[1];
+    if (bf < 0) return 0;                                      // uniform
+
+    // 4. the front's records, bin-contiguous: bin[bn] is bin bn's cursor, and its end afterwards
+    for (int c0 = 0; c0 < n; c0 += CH) {
+        if (!one) load_chunk(c0);
+#pragma unroll
+        for (int k = 0; k < E; ++k) {
+            const int i = c0 + tid + k * NT;
+            if (i < n) {
+                const uint32_t bn = bin_of(dreg[k]);
+                if (bn <= (uint32_t)bf)
+                    S.b[atomicAdd(&S.bin[bn], 1u)] = ((uint64_t)dreg[k] << 32) | (uint32_t)g[i];
+            }
+        }
+    }
+    __syncthreads();
+
+    // 5. rank inside the bin by full-word comparison (settles equal depths by index)
+    for (int i = tid; i < F; i += NT) {
+        const uint64_t r = S.b[i];
+        const uint32_t bn = bin_of((uint32_t)(r >> 32));
+        const int b0 = bn ? (int)S.bin[bn - 1] : 0, b1 = (int)S.bin[bn];
+        int rank = 0;
+        for (int j = b0; j < b1; ++j) rank += S.b[j] < r ? 1 : 0;
+        vals_out[start + b0 + rank] = (uint32_t)r;
+    }
+    return F;
+}
+
+__global__ void __launch_bounds__(FGS_FRONT_NT, FGS_FRONT_MINB)
+k_tile_front(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
+             const int32_t *__restrict__ starts, const uint32_t *__restrict__ dense_list,
+             const uint32_t *__restrict__ large_list, const uint32_t *__restrict__ medium_list,
+             int take_medium, int32_t *__restrict__ limit, fgs_stats *__restrict__ stats)
+{
+    extern __shared__ __align__(16) unsigned char ts_raw[];
+    FrontSmem &S = *reinterpret_cast<FrontSmem *>(ts_raw);
+    fgs_pdl_trigger();      // no wait, as the large class it stands in for: released only after
+                            // the medium kernel's wait returned
+    if (stats->overflow) return;
+    __shared__ uint32_t s_ticket;
+    const uint32_t nd0 = fgs_work(stats)[FGS_WORK_DENSE0], nl = fgs_work(stats)[FGS_WORK_LARGE];
+    const uint32_t count = nd0 + nl + (take_medium ? stats->medium_tiles : 0u);
+    TileTickets tk;
+    if (!tk.open(stats, FGS_WORK_LARGE_TICKET, count)) return;
+    uint32_t mine = 0;
+    for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
+        const int tile = (int)(i < nd0 ? dense_list[(size_t)i * FGS_CTR_STRIDE]
+                               : i < nd0 + nl ? large_list[(size_t)(i - nd0) * FGS_CTR_STRIDE]
+                                              : medium_list[(size_t)(i - nd0 - nl) * FGS_CTR_STRIDE]);
+        const int F = front_sort_tile(S, tile, rec, vals_out, starts);
+        if (threadIdx.x == 0) limit[tile] = F;
+        ++mine;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && mine) atomicAdd(&stats->front_tiles, mine);
+    tk.close(stats, 2u);
+}
+
 // The tail of the tile sort, one launch: the dense list (split path), then the hard list
 // (small / medium buckets the bucket-rank sort gave up on: radix path, no second try).
 __global__ void __launch_bounds__(256, 2)
@@ -964,7 +1183,7 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
                  uint32_t *__restrict__ vals_out, uint64_t *__restrict__ keys_out,
                  const int32_t *__restrict__ starts, const uint32_t *__restrict__ dense_list,
                  const uint32_t *__restrict__ hard_list, int write_keys,
-                 fgs_stats *__restrict__ stats)
+                 fgs_stats *__restrict__ stats, int lazy)
 {
     fgs_pdl_trigger();      // plain launch; the blend may queue up behind this grid
 
@@ -982,7 +1201,11 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
     __shared__ uint32_t s_joined;
     if (threadIdx.x == 0) {
         uint32_t *work = fgs_work(stats);
-        const uint32_t need = ((stats->medium_tiles | work[FGS_WORK_DENSE0]) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u);
+        // (lazy_sort: bit 1 is the front kernel's, which takes the dense and large tiles and
+        // with lazy == 2 the medium ones; the medium kernel keeps what is left)
+        const uint32_t nmed = lazy == 2 ? 0u : stats->medium_tiles, nd = work[FGS_WORK_DENSE0];
+        const uint32_t need = lazy ? ((nmed ? 1u : 0u) | ((nd | work[FGS_WORK_LARGE] | (stats->medium_tiles - nmed)) ? 2u : 0u))
+                                   : (((nmed | nd) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u));
         volatile uint32_t *done = work + FGS_WORK_SORT_DONE;
         uint32_t ok = 1u;
         for (uint32_t spin = 0; (*done & need) != need; ++spin) {
@@ -1013,9 +1236,34 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
     }
 }
 
+
+// lazy_sort: the tiles the blend found unsaturated at the end of their sorted front, sorted in
+// full by the tail kernel's general path (any size: split on the top varying depth bits,
+// bucket-rank per chunk, radix / bitonic fallbacks).  Rare by construction; rec is untouched
+// by everything before, so the sort starts from the tile's bucket as the scatter left it.
+__global__ void __launch_bounds__(256, 2)
+k_tile_sort_redo(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
+                 uint32_t *__restrict__ vals_out, const int32_t *__restrict__ starts,
+                 const uint32_t *__restrict__ redo_list, fgs_stats *__restrict__ stats)
+{
+    fgs_pdl_wait();
+    fgs_pdl_trigger();
+    extern __shared__ __align__(16) unsigned char ts_raw[];
+    using Radix = TileSortSmem<256, 16>;
+    Radix &S = *reinterpret_cast<Radix *>(ts_raw);
+    BucketSmem<256, 16> *B = reinterpret_cast<BucketSmem<256, 16> *>(
+        ts_raw + ((sizeof(Radix) + 15) & ~size_t(15)));
+    if (stats->overflow) return;
+    const uint32_t n = fgs_work(stats)[FGS_WORK_REDO];
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        ts_sort_tile<256, 16, true>(S, (int)redo_list[i], rec, alt, vals_out, alt, starts, 0, B);
+        __syncthreads();
+    }
+}
+
 }  // namespace
 
-int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStream_t st)
+int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, int lazy, cudaStream_t st)
 {
     if (tiles <= 0) return FGS_OK;
     using MediumSmem = BucketSmem<FGS_MED_NT, FGS_MED_EMAX, FGS_MED_STAGE, FGS_MED_NBDIV>;
@@ -1043,6 +1291,8 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         prep((const void *)k_tile_sort_medium, sizeof(MediumSmem));
         prep((const void *)k_tile_sort_large, sizeof(LargeSmem));
         prep((const void *)k_tile_sort_tail, tail_bytes);
+        prep((const void *)k_tile_front, sizeof(FrontSmem));
+        prep((const void *)k_tile_sort_redo, tail_bytes);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         attr_once.mark(attr_dev);
     }
@@ -1070,10 +1320,23 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
     cfg.attrs = pdl;
     {
         FGS_CHAIN(k_tile_sort_medium, dim3(mgrid), dim3(FGS_MED_NT), sizeof(MediumSmem), st,
-                  f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, dense_list, write_keys, f.stats);
+                  f.keys[0], f.vals[0], f.keys[1], f.starts, medium_list, hard_list, dense_list, write_keys, f.stats,
+                  lazy);
         FGS_AFTER_LAUNCH(st);
     }
-    {
+    if (lazy) {
+        // the front kernel stands in for the large class (same place in the chain, same ticket
+        // and done-flag words) and also takes the dense tiles
+        cfg.gridDim = dim3((unsigned)(tiles < FGS_FRONT_MINB * sms ? tiles : FGS_FRONT_MINB * sms));
+        cfg.blockDim = dim3(FGS_FRONT_NT);
+        cfg.dynamicSmemBytes = sizeof(FrontSmem);
+        cfg.numAttrs = overlap ? 1 : 0;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_tile_front, (const uint64_t *)f.keys[0], f.vals[0],
+            (const int32_t *)f.starts, (const uint32_t *)dense_list, (const uint32_t *)large_list,
+            (const uint32_t *)medium_list, lazy == 2 ? 1 : 0, f.limit, f.stats);
+        if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
+        FGS_AFTER_LAUNCH(st);
+    } else {
         cfg.gridDim = dim3(dgrid);
         cfg.blockDim = dim3(FGS_LARGE_NT);
         cfg.dynamicSmemBytes = sizeof(LargeSmem);
@@ -1090,13 +1353,30 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, cudaStrea
         cfg.dynamicSmemBytes = 0;
         cfg.numAttrs = overlap ? 1 : 0;
         const cudaError_t e = cudaLaunchKernelEx(&cfg, k_tile_sort, (const uint64_t *)f.keys[0],
-            f.vals[0], f.keys[1], (const int32_t *)f.starts, hard_list, write_keys, f.stats);
+            f.vals[0], f.keys[1], (const int32_t *)f.starts, hard_list, write_keys, f.stats,
+            lazy ? f.limit : (int32_t *)nullptr, lazy == 2 ? FGS_SMALL_TILE : FGS_DENSE_TILE);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         FGS_AFTER_LAUNCH(st);
     }
     k_tile_sort_tail<<<tgrid, 256, tail_bytes, st>>>(f.keys[0], f.keys[1], f.vals[0], f.keys[1],
                                                      f.starts, dense_list, hard_list, write_keys,
-                                                     f.stats);
+                                                     f.stats, lazy);
+    FGS_AFTER_LAUNCH(st);
+    return FGS_OK;
+}
+
+// lazy_sort: full sort of the tiles on the redo list (behind the first blend pass)
+int fgs_launch_tile_sort_redo(const FrameDev &f, int tiles, cudaStream_t st)
+{
+    if (tiles <= 0) return FGS_OK;
+    using TailRadix = TileSortSmem<256, 16>;
+    constexpr size_t tail_bytes = ((sizeof(TailRadix) + 15) & ~size_t(15)) + sizeof(BucketSmem<256, 16>);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)(tiles < 2 * sms ? tiles : 2 * sms);
+    FGS_CHAIN(k_tile_sort_redo, dim3(grid), dim3(256), tail_bytes, st, f.keys[0], f.keys[1], f.vals[0],
+              (const int32_t *)f.starts, (const uint32_t *)f.redo_list, f.stats);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }

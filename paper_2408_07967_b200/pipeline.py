@@ -71,6 +71,8 @@ class FrameStats:
     # extras (not in the reference)
     candidate_tiles: int = 0
     e2e_ns: int = 0                # host wall clock of the call incl. the D2H copy
+    front_tiles: int = 0           # lazy_sort: heavy tiles whose nearest pairs only were sorted
+    redo_tiles: int = 0            # ... of which sorted in full and blended again (not saturated)
 
     def to_dict(self) -> dict:
         return asdict(self)
@@ -119,6 +121,8 @@ def _fill_counters(stats, s):
     stats.tiles_nonempty = int(s["tiles_nonempty"])
     stats.pair_buffer_bytes = 12 * stats.pairs_emitted
     stats.candidate_tiles = int(s["candidate_tiles_lo"]) | (int(s["candidate_tiles_hi"]) << 32)
+    stats.front_tiles = int(s["front_tiles"])
+    stats.redo_tiles = int(s["redo_tiles"])
 
 
 class _PinnedPool:
@@ -168,7 +172,7 @@ class _Workspace:
         self.alpha = None
         self.depthmap = None
         self.rgb8 = None               # (H, W, 3) uint8, allocated on first quantized render
-        self.h_stats = torch.empty(64, dtype=torch.uint8, pin_memory=True)
+        self.h_stats = torch.empty(_capi.STATS_BYTES, dtype=torch.uint8, pin_memory=True)
         self.h_stats_np = self.h_stats.numpy().view(_capi.STATS_DTYPE)   # same pinned bytes
         self.kcut_ptr = None
         self._events = None
@@ -185,9 +189,10 @@ class _Workspace:
             self._events = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
         return self._events
 
-    def set_mode(self, sort_mode, keep_sorted_keys=False):
+    def set_mode(self, sort_mode, keep_sorted_keys=False, lazy_sort=False):
         _capi.check(_capi.lib().fgs_layout_set_sort_mode(C.byref(self.lay), int(sort_mode)))
         self.lay.keep_sorted_keys = 1 if keep_sorted_keys else 0
+        self.lay.lazy_sort = 1 if lazy_sort else 0
 
     def next_epoch(self):
         e = self.epoch
@@ -200,7 +205,7 @@ class _Workspace:
         return self.buf[int(off):int(off) + int(nbytes)].view(dtype)
 
     def stats_tensor(self):
-        return self.buf[int(self.lay.off_stats):int(self.lay.off_stats) + 64]
+        return self.buf[int(self.lay.off_stats):int(self.lay.off_stats) + _capi.STATS_BYTES]
 
 
 class Pipeline:
@@ -217,7 +222,7 @@ class Pipeline:
     """
 
     def __init__(self, scene, sh_degree=3, device=None, sort_mode="tile-bucket",
-                 spatial_order=None, device_activate=False):
+                 spatial_order=None, device_activate=False, lazy_sort=True):
         if sort_mode not in _capi.SORT_MODES:
             raise ValueError(f"unknown sort_mode {sort_mode!r}, expected one of {tuple(_capi.SORT_MODES)}")
         self.sort_mode = sort_mode
@@ -230,6 +235,14 @@ class Pipeline:
         if spatial_order and sort_mode != "tile-bucket":
             raise ValueError("spatial_order needs sort_mode='tile-bucket'")
         self.spatial_order = bool(spatial_order)
+        # ``lazy_sort`` (tile-bucket only): a heavy tile is opaque long before its pair list
+        # ends, so the sort orders only the nearest ~1024 pairs of each tile beyond 4096 and
+        # the blend falls back to a full sort of the tiles that were not saturated by then
+        # (fgs_layout.lazy_sort).  Frames and counters are unchanged.  A scene whose heavy
+        # tiles mostly do NOT saturate (translucent clouds) pays the front for nothing:
+        # when more than a quarter of a frame's fronts had to be redone, the pipeline
+        # switches the option off for its later frames.
+        self.lazy_sort = bool(lazy_sort) and sort_mode == "tile-bucket"
         # ``device_activate``: a raw Scene is activated by the library (fgs_scene_activate)
         # instead of on the host.  Opacities / scales may then differ from the reference's
         # NumPy activation by 1 ulp (see the header), so frames agree within the pixel
@@ -377,6 +390,11 @@ class Pipeline:
             if len(lst) < 4:
                 lst.append(ws)
 
+    def _note_fronts(self, stats):
+        """lazy_sort pays only while heavy tiles saturate inside their sorted front."""
+        if self.lazy_sort and stats.front_tiles >= 16 and 4 * stats.redo_tiles > stats.front_tiles:
+            self.lazy_sort = False
+
     # -- the hot path -----------------------------------------------------------
     def _issue(self, torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1, out_ptr, a_ptr, d_ptr,
                st, timing):
@@ -448,7 +466,7 @@ class Pipeline:
             kcut = self._cutoffs(torch, tau)
             while True:
                 ws = self._take_ws(torch, W, H, capacity)
-                ws.set_mode(_capi.SORT_MODES[self.sort_mode])
+                ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=self.lazy_sort)
                 ws.kcut_ptr = kcut.data_ptr()
                 if extras:
                     if ws.alpha is None:
@@ -496,6 +514,7 @@ class Pipeline:
                 stats.render_ns = int(ev[2].elapsed_time(ev[3]) * 1e6)
                 stats.total_ns = int(ev[0].elapsed_time(ev[3]) * 1e6)
             _fill_counters(stats, s)
+            self._note_fronts(stats)
             self._last_pairs = max(self._last_pairs, stats.pairs_emitted)
             if as_numpy:
                 fb = Framebuffer(_pinned.as_numpy(h_rgb), bg)
@@ -598,7 +617,7 @@ class Pipeline:
                 works = None
             while True:
                 ws = self._take_ws(torch, W, H, capacity)
-                ws.set_mode(_capi.SORT_MODES[self.sort_mode])
+                ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=self.lazy_sort)
                 ws.kcut_ptr = kcut.data_ptr()
                 if b1 >= b0:
                     self._issue(torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1,
@@ -701,6 +720,7 @@ class Pipeline:
                                    contrib=contrib, timing=False, quantized=quantized)
             st = FrameStats(strategy=strategy, tau=float(tau), workers=1)
             _fill_counters(st, s)
+            self._note_fronts(st)
             self._last_pairs = max(self._last_pairs, st.pairs_emitted)
             st.e2e_ns = time.perf_counter_ns() - t0
             return Framebuffer(_pinned.as_numpy(h_rgb), bg), st
@@ -723,7 +743,7 @@ class Pipeline:
                     W, H = int(cam_obj.width), int(cam_obj.height)
                     gh = -(-H // TILE_SIZE)
                     ws = self._take_ws(torch, W, H, self._default_capacity())
-                    ws.set_mode(_capi.SORT_MODES[self.sort_mode])
+                    ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=self.lazy_sort)
                     lane = lanes[issued % nstreams]
                     issued += 1
                     _capi.check(L.fgs_render(self.packed.data_ptr(), kcut.data_ptr(), self.count,
@@ -1056,7 +1076,7 @@ def tile_range_table(sorted_keys, grid_w, grid_h) -> np.ndarray:
     dev = torch.device("cuda", torch.cuda.current_device())
     k = torch.from_numpy(keys.view(np.int64)).to(dev)
     starts = torch.empty(tiles + 1, dtype=torch.int32, device=dev)
-    stats = torch.zeros(64, dtype=torch.uint8, device=dev)
+    stats = torch.zeros(_capi.STATS_BYTES, dtype=torch.uint8, device=dev)
     _capi.check(_capi.lib().fgs_tile_ranges(k.data_ptr() if keys.size else None, keys.shape[0],
                                             tiles, starts.data_ptr(), stats.data_ptr(),
                                             _stream_ptr(torch, dev)))
@@ -1084,7 +1104,7 @@ def render_frame(splat, sorted_values, starts, width, height, background, tau,
     bg_c = (C.c_float * 3)(*bg.tolist())
     rgb = torch.empty((height, width, 3), dtype=torch.float32, device=dev)
     contrib = torch.zeros(max(vals_np.shape[0], 1), dtype=torch.uint8, device=dev)
-    stats = torch.zeros(64, dtype=torch.uint8, device=dev)
+    stats = torch.zeros(_capi.STATS_BYTES, dtype=torch.uint8, device=dev)
     extras = gaussian_depth is not None
     if extras:
         gd = torch.from_numpy(np.ascontiguousarray(gaussian_depth, dtype=np.float32)).to(dev)

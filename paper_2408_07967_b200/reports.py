@@ -52,7 +52,7 @@ class CompareReport:
 def _reference_stats_dict(st) -> dict:
     """FrameStats -> exactly the reference's frame-stats object (report-schema.md:11-28)."""
     d = st.to_dict()
-    for extra in ("candidate_tiles", "e2e_ns"):
+    for extra in ("candidate_tiles", "e2e_ns", "front_tiles", "redo_tiles"):
         d.pop(extra, None)
     return d
 

@@ -33,6 +33,9 @@ for cub in glob.glob(os.path.join(tmp, "*.cubin")):
         if m:
             if chain:
                 own = [c for c in chain if "/csrc/" in c[0]]
+                if os.environ.get("SRCPROF_CALLSITE"):      # attribute inlined fgs_common.cuh helpers to their call site
+                    cu = [c for c in own if c[0].endswith(".cu")]
+                    own = cu or own
                 last = own[0] if own else chain[0]
                 chain = []
             tab.append((int(m.group(1), 16), last, m.group(2).strip()))
@@ -70,6 +73,12 @@ def src(f, l):
         src_cache[f] = open(p).read().splitlines() if os.path.exists(p) else []
     L = src_cache[f]
     return L[l - 1].strip()[:100] if 0 < l <= len(L) else ""
+if os.environ.get("SRCPROF_RANGES"):                # e.g. "geometry:907-1069,walk:722-813": sums per line range
+    for spec in os.environ["SRCPROF_RANGES"].split(","):
+        name, r = spec.split(":"); lo, hi = map(int, r.split("-"))
+        ii = sum(a[0] for (f, l), a in agg.items() if f.endswith(".cu") and lo <= l <= hi)
+        ss = sum(a[1] for (f, l), a in agg.items() if f.endswith(".cu") and lo <= l <= hi)
+        print(f"range {name:12s} {lo:5d}-{hi:5d}: {100*ii/ti:5.1f}% inst {100*ss/ts:5.1f}% smp")
 print(f"{kern}: {ti} warp instructions, {ts} samples, {unk} unmatched SASS rows")
 tot_st = {}
 for a in agg.values():
