@@ -988,7 +988,8 @@ k_tile_sort_large(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_
 #define FGS_FRONT_NT   512
 #endif
 #ifndef FGS_FRONT_MINB
-#define FGS_FRONT_MINB 3         // 42 registers: 16 of them hold the thread's depth words
+#define FGS_FRONT_MINB 4         // 32 registers (the 16 depth words of a thread partly in local
+                                 // memory, L1-resident): 134 us on the 10M / 4K frame against 138 at 3
 #endif
 #ifndef FGS_FRONT_CAP
 #define FGS_FRONT_CAP  3072      // records a front may hold (24 KB)
@@ -1162,17 +1163,14 @@ k_tile_front(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
     const uint32_t count = nd0 + nl + (take_medium ? stats->medium_tiles : 0u);
     TileTickets tk;
     if (!tk.open(stats, FGS_WORK_LARGE_TICKET, count)) return;
-    uint32_t mine = 0;
     for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
         const int tile = (int)(i < nd0 ? dense_list[(size_t)i * FGS_CTR_STRIDE]
                                : i < nd0 + nl ? large_list[(size_t)(i - nd0) * FGS_CTR_STRIDE]
                                               : medium_list[(size_t)(i - nd0 - nl) * FGS_CTR_STRIDE]);
         const int F = front_sort_tile(S, tile, rec, vals_out, starts);
         if (threadIdx.x == 0) limit[tile] = F;
-        ++mine;
         __syncthreads();
     }
-    if (threadIdx.x == 0 && mine) atomicAdd(&stats->front_tiles, mine);
     tk.close(stats, 2u);
 }
 
@@ -1204,6 +1202,11 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
         // (lazy_sort: bit 1 is the front kernel's, which takes the dense and large tiles and
         // with lazy == 2 the medium ones; the medium kernel keeps what is left)
         const uint32_t nmed = lazy == 2 ? 0u : stats->medium_tiles, nd = work[FGS_WORK_DENSE0];
+        // the frame's heavy tiles -- those lazy_sort orders a front of -- reported either way:
+        // the host arms lazy_sort only for frames that have enough of them to pay for its two
+        // extra launches
+        if (blockIdx.x == 0)
+            stats->front_tiles = nd + work[FGS_WORK_LARGE] + (FGS_LAZY_LEVEL == 2 ? stats->medium_tiles : 0u);
         const uint32_t need = lazy ? ((nmed ? 1u : 0u) | ((nd | work[FGS_WORK_LARGE] | (stats->medium_tiles - nmed)) ? 2u : 0u))
                                    : (((nmed | nd) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u));
         volatile uint32_t *done = work + FGS_WORK_SORT_DONE;

@@ -125,6 +125,9 @@ def _fill_counters(stats, s):
     stats.redo_tiles = int(s["redo_tiles"])
 
 
+LAZY_MIN_TILES = 512     # heavy tiles a frame must have for lazy_sort to be armed for the next one
+
+
 class _PinnedPool:
     """Recycles pinned host frames: a frame handed to the caller returns to the
     pool when the caller's ndarray is garbage-collected."""
@@ -241,8 +244,10 @@ class Pipeline:
         # (fgs_layout.lazy_sort).  Frames and counters are unchanged.  A scene whose heavy
         # tiles mostly do NOT saturate (translucent clouds) pays the front for nothing:
         # when more than a quarter of a frame's fronts had to be redone, the pipeline
-        # switches the option off for its later frames.
-        self.lazy_sort = bool(lazy_sort) and sort_mode == "tile-bucket"
+        # switches the option off for its later frames; and a frame with fewer than
+        # LAZY_MIN_TILES heavy tiles leaves it off for the next one (nothing to gain).
+        self._lazy_allowed = bool(lazy_sort) and sort_mode == "tile-bucket"
+        self.lazy_sort = self._lazy_allowed         # the next frame's setting (see _note_fronts)
         # ``device_activate``: a raw Scene is activated by the library (fgs_scene_activate)
         # instead of on the host.  Opacities / scales may then differ from the reference's
         # NumPy activation by 1 ulp (see the header), so frames agree within the pixel
@@ -391,9 +396,17 @@ class Pipeline:
                 lst.append(ws)
 
     def _note_fronts(self, stats):
-        """lazy_sort pays only while heavy tiles saturate inside their sorted front."""
-        if self.lazy_sort and stats.front_tiles >= 16 and 4 * stats.redo_tiles > stats.front_tiles:
-            self.lazy_sort = False
+        """lazy_sort pays only while heavy tiles saturate inside their sorted front, and only
+        on frames with enough heavy tiles to cover its two extra kernel launches (~10 us): the
+        next frame follows what this one showed (``fgs_stats.front_tiles`` counts the frame's
+        heavy tiles whether or not the option was on)."""
+        if not self._lazy_allowed:
+            return
+        heavy, redo = stats.front_tiles, stats.redo_tiles
+        if self.lazy_sort and heavy >= 16 and 4 * redo > heavy:
+            self._lazy_allowed = self.lazy_sort = False        # fronts mostly fail: stop guessing
+        else:
+            self.lazy_sort = heavy >= LAZY_MIN_TILES
 
     # -- the hot path -----------------------------------------------------------
     def _issue(self, torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1, out_ptr, a_ptr, d_ptr,

@@ -71,8 +71,9 @@ def test_lazy_fronts_give_the_full_sort_frame(kind):
         lazy.lazy_sort = True            # (a frame of failed fronts switches it off: keep it on)
         fl, sl = lazy.render(cam, exact=exact)
         ff, sf = full.render(cam, exact=exact)
-        assert sf.front_tiles == 0 and sf.redo_tiles == 0
-        assert sl.front_tiles == int((per_tile > 4096).sum())
+        # (front_tiles counts the frame's heavy tiles with the option on or off)
+        assert sf.redo_tiles == 0
+        assert sl.front_tiles == sf.front_tiles == int((per_tile > 4096).sum())
         if kind == "opaque":
             assert sl.redo_tiles == 0
         elif kind == "mixed":
@@ -86,10 +87,13 @@ def test_lazy_fronts_give_the_full_sort_frame(kind):
         if exact:                        # ... and the reference's
             assert np.array_equal(fl.image.view(np.uint32), oimg.view(np.uint32))
             assert sl.pairs_contributing == ost["pairs_contributing"]
-    if kind in ("translucent", "near cluster", "late cluster"):
-        lazy.lazy_sort = True
-        lazy.render(cam)
-        assert lazy.lazy_sort is False   # most fronts failed: the pipeline stops guessing
+    fresh = fgs.Pipeline(act)
+    assert fresh.lazy_sort is True
+    fresh.render(cam)
+    # the next frame's setting follows this one: most fronts failed -> the pipeline stops
+    # guessing for good; and 16 heavy tiles are too few to pay for the two extra launches
+    assert fresh.lazy_sort is False
+    assert fresh._lazy_allowed is (kind == "opaque")          # (mixed: half of the fronts failed)
 
 
 def test_lazy_extras_and_bands():
