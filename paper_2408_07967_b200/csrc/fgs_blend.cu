@@ -597,7 +597,8 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
                 const float4 f1 = S.fast[j][1];
                 const float4 f2 = S.fast[j][2];
                 const float dx = fx - f0.x;
-                const float adx2 = (f0.z * dx) * dx, bdx = f0.w * dx;
+                const pk2 ab = mul2(pk(f0.z, f0.w), bc(dx));         // (a2 dx, b2 dx): one FMUL2
+                const float adx2 = ab.x * dx, bdx = ab.y;
                 const pk2 dy2 = sub2(pk(fy0, fy1), bc(f0.y));
                 const pk2 h2 = fma2(bc(f1.x), dy2, bc(bdx));
                 const pk2 m2 = fma2(dy2, h2, bc(adx2));              // -log2(e) * s
@@ -609,8 +610,14 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
                 upk(d2, d0, d1);
                 upk(al2, al0, al1);
                 bool on0 = d0 >= 0.0f, on1 = d1 >= 0.0f;
-                const bool band = !(fabsf(d0) > f1.w) | !(fabsf(d1) > f1.w);
-                if (band) {
+                // one FMNMX with |.| on both operands + one compare for the two pixels (a NaN in
+                // either means a NaN in both: the row's centre or conic is NaN, and eps = inf
+                // sends rows with a degenerate conic here anyway).  The branch is taken by the
+                // whole warp when any lane is in the band: a uniform branch needs no
+                // reconvergence bookkeeping around the call, and the exact path gives the lanes
+                // outside the band the verdict they already had.
+                const bool band = !(fminf(fabsf(d0), fabsf(d1)) > f1.w);
+                if (__any_sync(FGS_FULL, band)) {
                     // within eps of the threshold (or a row the shortcut does not cover):
                     // the reference's own evaluation decides, for both pixels
                     const float2 ax = alpha_exact_pair(&S.row[cur][j][0], fx, fy0, fy1, tau, S.tab);
@@ -627,8 +634,9 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
                 cg2 = fma2(bc(f2.y), w2, cg2);
                 cb2 = fma2(bc(f2.z), w2, cb2);
                 if (EXTRAS) dz2 = fma2(bc(f2.w), w2, dz2);
-                T2 = mul2(T2, sub2(pk(1.0f, 1.0f), al2));
-                if (CONTRIB && (on0 || on1)) S.touched[j] = 1u;
+                T2 = sub2(T2, w2);                                   // T (1 - alpha) = T - alpha T
+                // (any non-zero word marks the pair: fx's bits are at hand, a constant 1 is not)
+                if (CONTRIB && (on0 || on1)) S.touched[j] = __float_as_uint(fx);
                 float t0, t1;
                 upk(T2, t0, t1);
                 if (t0 < FGS_T_STOP) fy0 = kInf;                     // render.py:228
@@ -638,7 +646,7 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
         const bool all_done = __syncthreads_and(fy0 == kInf && fy1 == kInf);
         if (CONTRIB) {
             if (tid < cnt) {
-                const uint32_t t = S.touched[tid];
+                const uint32_t t = S.touched[tid] != 0u ? 1u : 0u;
                 contrib[start + b * B + tid] = (uint8_t)t;
                 ncontrib += t;
             }
