@@ -310,7 +310,7 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     del fb
     stream = torch.cuda.current_stream(dev)
     bucket = args.sort_mode == "tile-bucket"
-    lazy = bool(pipe.lazy_sort)             # (the pipeline drops it when fronts mostly fail)
+    lazy = int(pipe.lazy_sort)              # level the pipeline settled on during the warm-up frames
     front_tiles, redo_tiles = int(st.front_tiles), int(st.redo_tiles)
     nlanes = max(1, args.streams)
     lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nlanes - 1)]

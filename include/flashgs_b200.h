@@ -107,7 +107,8 @@ typedef struct fgs_stats {
     uint32_t hard_tiles;           /* TILE_BUCKET: tiles sent to the radix fallback */
     uint32_t list_used;            /* TILE_BUCKET: (CTA, tile) table entries of the frame;
                                       at most M, so it fits whenever M fits          */
-    uint32_t front_tiles;          /* lazy_sort: heavy tiles whose nearest pairs only were sorted */
+    uint32_t front_tiles;          /* tiles with more than 4096 pairs (with medium_tiles: what
+                                      lazy_sort would sort a front of; filled with it on or off) */
     uint32_t redo_tiles;           /* lazy_sort: of those, tiles that had not saturated by the end
                                       of their sorted front -- sorted in full and blended again */
     uint32_t reserved[2];
@@ -155,15 +156,16 @@ typedef struct fgs_layout {
                                   (only the values feed the blend); caller-set  */
     int32_t  lazy_sort;        /* TILE_BUCKET, caller-set, ignored with keep_sorted_keys: front-to-back
                                   compositing stops once a tile is opaque (render.py:154,178,228),
-                                  so of a heavy tile (> 4096 pairs) fgs_sort only orders the nearest
-                                  ~1024 pairs (every pair nearer than a depth threshold, so the
-                                  front IS the head of the tile's sorted list) and fgs_blend
-                                  composites those; a tile that has not saturated by then is
-                                  sorted in full and blended again from scratch inside the same
-                                  fgs_blend call.  The frame, the contrib flags of every pair a
-                                  pixel consumed and all counters are those of the full sort;
-                                  the sorted VALUE buffer is complete only for the tiles that
-                                  needed it.  0 = every tile sorted in full (sorting.py:101-136). */
+                                  so of a heavy tile -- 1: more than 4096 pairs, 2: more than 2048 --
+                                  fgs_sort only orders the nearest ~1024 pairs (every pair nearer
+                                  than a depth threshold, so the front IS the head of the tile's
+                                  sorted list) and fgs_blend composites those; a tile that has not
+                                  saturated by then is sorted in full and blended again from scratch
+                                  inside the same fgs_blend call.  The frame, the contrib flags of
+                                  every pair a pixel consumed and all counters are those of the full
+                                  sort; the sorted VALUE buffer is complete only for the tiles that
+                                  needed it.  0 = every tile sorted in full (sorting.py:101-136).
+                                  Keep the value unchanged between fgs_sort and fgs_blend.  */
     int32_t  reserved0;
     uint64_t off_front;        /* TILE_BUCKET: int32 [tiles] sorted pairs at the head of each tile's
                                   bucket (INT32_MAX = all of them), then uint32 [tiles] redo list */

@@ -635,8 +635,9 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
                 cb2 = fma2(bc(f2.z), w2, cb2);
                 if (EXTRAS) dz2 = fma2(bc(f2.w), w2, dz2);
                 T2 = sub2(T2, w2);                                   // T (1 - alpha) = T - alpha T
-                // (any non-zero word marks the pair: fx's bits are at hand, a constant 1 is not)
-                if (CONTRIB && (on0 || on1)) S.touched[j] = __float_as_uint(fx);
+                // (every lane stores the same word: marking with a register that happens to be
+                // live saves the constant's MOV, but lanes then race with different values)
+                if (CONTRIB && (on0 || on1)) S.touched[j] = 1u;
                 float t0, t1;
                 upk(T2, t0, t1);
                 if (t0 < FGS_T_STOP) fy0 = kInf;                     // render.py:228
@@ -646,7 +647,7 @@ k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
         const bool all_done = __syncthreads_and(fy0 == kInf && fy1 == kInf);
         if (CONTRIB) {
             if (tid < cnt) {
-                const uint32_t t = S.touched[tid] != 0u ? 1u : 0u;
+                const uint32_t t = S.touched[tid];
                 contrib[start + b * B + tid] = (uint8_t)t;
                 ncontrib += t;
             }

@@ -48,10 +48,11 @@ static CamDev make_cam(const fgs_camera *c)
     return d;
 }
 
-// lazy_sort as the launchers take it: 0 off, else which tiles get a front only
+// lazy_sort as the launchers take it: 0 off, 1 / 2 = which tiles get a front only
 static int fgs_lazy(const fgs_layout *L)
 {
-    return (L->lazy_sort && !L->keep_sorted_keys && L->sort_mode == FGS_SORT_TILE_BUCKET) ? FGS_LAZY_LEVEL : 0;
+    if (L->lazy_sort <= 0 || L->keep_sorted_keys || L->sort_mode != FGS_SORT_TILE_BUCKET) return 0;
+    return L->lazy_sort >= 2 ? 2 : 1;
 }
 
 static int check_frame(const fgs_layout *L, const fgs_camera *c)

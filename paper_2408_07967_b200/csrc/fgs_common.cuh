@@ -202,10 +202,7 @@ int  fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strat
                      int band1, int bucket, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, int lazy, cudaStream_t st);
 int  fgs_launch_tile_sort_redo(const FrameDev &f, int tiles, cudaStream_t st);
-// lazy_sort: which tiles get a front only (1: beyond FGS_DENSE_TILE pairs, 2: beyond FGS_SMALL_TILE)
-#ifndef FGS_LAZY_LEVEL
-#define FGS_LAZY_LEVEL 1
-#endif
+// (lazy: 0 off; 1 = tiles beyond FGS_DENSE_TILE pairs get a front only; 2 = beyond FGS_SMALL_TILE)
 
 struct SortPlan {
     int npass;

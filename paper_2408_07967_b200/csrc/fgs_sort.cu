@@ -1206,7 +1206,7 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
         // the host arms lazy_sort only for frames that have enough of them to pay for its two
         // extra launches
         if (blockIdx.x == 0)
-            stats->front_tiles = nd + work[FGS_WORK_LARGE] + (FGS_LAZY_LEVEL == 2 ? stats->medium_tiles : 0u);
+            stats->front_tiles = nd + work[FGS_WORK_LARGE];      // (level 2 adds stats->medium_tiles)
         const uint32_t need = lazy ? ((nmed ? 1u : 0u) | ((nd | work[FGS_WORK_LARGE] | (stats->medium_tiles - nmed)) ? 2u : 0u))
                                    : (((nmed | nd) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u));
         volatile uint32_t *done = work + FGS_WORK_SORT_DONE;

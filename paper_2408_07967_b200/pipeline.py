@@ -126,6 +126,7 @@ def _fill_counters(stats, s):
 
 
 LAZY_MIN_TILES = 512     # heavy tiles a frame must have for lazy_sort to be armed for the next one
+LAZY_REDO_MAX = 8        # fronts of tiles below 4097 pairs redone in a frame before level 2 is given up
 
 
 class _PinnedPool:
@@ -195,7 +196,7 @@ class _Workspace:
     def set_mode(self, sort_mode, keep_sorted_keys=False, lazy_sort=False):
         _capi.check(_capi.lib().fgs_layout_set_sort_mode(C.byref(self.lay), int(sort_mode)))
         self.lay.keep_sorted_keys = 1 if keep_sorted_keys else 0
-        self.lay.lazy_sort = 1 if lazy_sort else 0
+        self.lay.lazy_sort = int(lazy_sort)            # 0 off, 1: tiles > 4096 pairs, 2: > 2048
 
     def next_epoch(self):
         e = self.epoch
@@ -239,15 +240,15 @@ class Pipeline:
             raise ValueError("spatial_order needs sort_mode='tile-bucket'")
         self.spatial_order = bool(spatial_order)
         # ``lazy_sort`` (tile-bucket only): a heavy tile is opaque long before its pair list
-        # ends, so the sort orders only the nearest ~1024 pairs of each tile beyond 4096 and
-        # the blend falls back to a full sort of the tiles that were not saturated by then
-        # (fgs_layout.lazy_sort).  Frames and counters are unchanged.  A scene whose heavy
-        # tiles mostly do NOT saturate (translucent clouds) pays the front for nothing:
-        # when more than a quarter of a frame's fronts had to be redone, the pipeline
-        # switches the option off for its later frames; and a frame with fewer than
-        # LAZY_MIN_TILES heavy tiles leaves it off for the next one (nothing to gain).
-        self._lazy_allowed = bool(lazy_sort) and sort_mode == "tile-bucket"
-        self.lazy_sort = self._lazy_allowed         # the next frame's setting (see _note_fronts)
+        # ends, so the sort orders only the nearest ~1024 pairs of each heavy tile and the
+        # blend falls back to a full sort of the tiles that were not saturated by then
+        # (fgs_layout.lazy_sort; level 1: tiles beyond 4096 pairs, level 2: beyond 2048).
+        # Frames and counters are unchanged.  The level follows the frames (_note_fronts): off
+        # while a frame has too few heavy tiles to pay for the two extra launches, capped at 1
+        # when fronts of the lighter class fail, and off for good when fronts mostly fail
+        # (translucent clouds).
+        self._lazy_cap = 2 if (lazy_sort and sort_mode == "tile-bucket") else 0
+        self.lazy_sort = self._lazy_cap             # the next frame's level (see _note_fronts)
         # ``device_activate``: a raw Scene is activated by the library (fgs_scene_activate)
         # instead of on the host.  Opacities / scales may then differ from the reference's
         # NumPy activation by 1 ulp (see the header), so frames agree within the pixel
@@ -395,18 +396,28 @@ class Pipeline:
             if len(lst) < 4:
                 lst.append(ws)
 
-    def _note_fronts(self, stats):
-        """lazy_sort pays only while heavy tiles saturate inside their sorted front, and only
-        on frames with enough heavy tiles to cover its two extra kernel launches (~10 us): the
-        next frame follows what this one showed (``fgs_stats.front_tiles`` counts the frame's
-        heavy tiles whether or not the option was on)."""
-        if not self._lazy_allowed:
+    def _note_fronts(self, stats, level, s):
+        """What the next frame's ``lazy_sort`` level is, from what this one showed (it was
+        rendered at ``level``; ``s`` = its device stats).  A front pays only while heavy tiles
+        saturate inside it, and only on frames with enough heavy tiles to cover the two extra
+        kernel launches (~10 us).  Level 2 also takes the tiles of 2049..4096 pairs: those that
+        fail are long tiles blended alone at the end of the frame, so a handful of them is
+        already a net loss and caps the level at 1."""
+        if not self._lazy_cap:
             return
-        heavy, redo = stats.front_tiles, stats.redo_tiles
-        if self.lazy_sort and heavy >= 16 and 4 * redo > heavy:
-            self._lazy_allowed = self.lazy_sort = False        # fronts mostly fail: stop guessing
+        heavy1 = stats.front_tiles
+        heavy2 = heavy1 + int(s["medium_tiles"])
+        used, redo = (heavy2 if level >= 2 else heavy1), stats.redo_tiles
+        if level and used >= 16 and 4 * redo > used:
+            self._lazy_cap = 0                          # fronts mostly fail: stop guessing
+        elif level >= 2 and redo > LAZY_REDO_MAX:
+            self._lazy_cap = 1
+        if self._lazy_cap >= 2 and heavy2 >= LAZY_MIN_TILES:
+            self.lazy_sort = 2
+        elif self._lazy_cap >= 1 and heavy1 >= LAZY_MIN_TILES:
+            self.lazy_sort = 1
         else:
-            self.lazy_sort = heavy >= LAZY_MIN_TILES
+            self.lazy_sort = 0
 
     # -- the hot path -----------------------------------------------------------
     def _issue(self, torch, L, ws, cam, tau, deg, sid, bg_c, flags, b0, b1, out_ptr, a_ptr, d_ptr,
@@ -479,7 +490,8 @@ class Pipeline:
             kcut = self._cutoffs(torch, tau)
             while True:
                 ws = self._take_ws(torch, W, H, capacity)
-                ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=self.lazy_sort)
+                lazy_level = int(self.lazy_sort)
+                ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=lazy_level)
                 ws.kcut_ptr = kcut.data_ptr()
                 if extras:
                     if ws.alpha is None:
@@ -527,7 +539,7 @@ class Pipeline:
                 stats.render_ns = int(ev[2].elapsed_time(ev[3]) * 1e6)
                 stats.total_ns = int(ev[0].elapsed_time(ev[3]) * 1e6)
             _fill_counters(stats, s)
-            self._note_fronts(stats)
+            self._note_fronts(stats, lazy_level, s)
             self._last_pairs = max(self._last_pairs, stats.pairs_emitted)
             if as_numpy:
                 fb = Framebuffer(_pinned.as_numpy(h_rgb), bg)
@@ -723,7 +735,7 @@ class Pipeline:
         inflight = deque()
 
         def finish(job):
-            cam_obj, ws, h_rgb, done, t0 = job
+            cam_obj, ws, h_rgb, done, t0, lazy_level = job
             done.synchronize()
             s = np.frombuffer(ws.h_stats.numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
             self._give_ws(ws)
@@ -733,7 +745,7 @@ class Pipeline:
                                    contrib=contrib, timing=False, quantized=quantized)
             st = FrameStats(strategy=strategy, tau=float(tau), workers=1)
             _fill_counters(st, s)
-            self._note_fronts(st)
+            self._note_fronts(st, lazy_level, s)
             self._last_pairs = max(self._last_pairs, st.pairs_emitted)
             st.e2e_ns = time.perf_counter_ns() - t0
             return Framebuffer(_pinned.as_numpy(h_rgb), bg), st
@@ -756,7 +768,8 @@ class Pipeline:
                     W, H = int(cam_obj.width), int(cam_obj.height)
                     gh = -(-H // TILE_SIZE)
                     ws = self._take_ws(torch, W, H, self._default_capacity())
-                    ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=self.lazy_sort)
+                    lazy_level = int(self.lazy_sort)
+                    ws.set_mode(_capi.SORT_MODES[self.sort_mode], lazy_sort=lazy_level)
                     lane = lanes[issued % nstreams]
                     issued += 1
                     _capi.check(L.fgs_render(self.packed.data_ptr(), kcut.data_ptr(), self.count,
@@ -778,7 +791,7 @@ class Pipeline:
                         ws.h_stats.copy_(ws.stats_tensor(), non_blocking=True)
                         done = torch.cuda.Event()
                         done.record(lane)
-                    inflight.append((cam_obj, ws, h_rgb, done, t0))
+                    inflight.append((cam_obj, ws, h_rgb, done, t0, lazy_level))
                 while inflight:
                     yield finish(inflight.popleft())
             finally:

@@ -88,12 +88,40 @@ def test_lazy_fronts_give_the_full_sort_frame(kind):
             assert np.array_equal(fl.image.view(np.uint32), oimg.view(np.uint32))
             assert sl.pairs_contributing == ost["pairs_contributing"]
     fresh = fgs.Pipeline(act)
-    assert fresh.lazy_sort is True
+    assert fresh.lazy_sort == 2
     fresh.render(cam)
-    # the next frame's setting follows this one: most fronts failed -> the pipeline stops
+    # the next frame's level follows this one: most fronts failed -> the pipeline stops
     # guessing for good; and 16 heavy tiles are too few to pay for the two extra launches
-    assert fresh.lazy_sort is False
-    assert fresh._lazy_allowed is (kind == "opaque")          # (mixed: half of the fronts failed)
+    assert fresh.lazy_sort == 0
+    assert fresh._lazy_cap == (2 if kind == "opaque" else 0)  # (mixed: half of the fronts failed)
+
+
+@pytest.mark.parametrize("kind", ["opaque", "translucent", "mixed"])
+def test_lazy_level_2_takes_the_medium_tiles(kind):
+    """Level 2: tiles of 2049..4096 pairs get a front too."""
+    act = _scene(kind, 30000)
+    cam = identity_camera(64, 64, focal=32)
+    ob = orc.preprocess_and_bin(act, cam)
+    per_tile = np.bincount((ob.keys >> np.uint64(32)).astype(np.int64), minlength=16)
+    medium = (per_tile > 2048) & (per_tile <= 4096)
+    assert medium.sum() >= 12, per_tile
+    oimg, ost = orc.render(act, cam)
+    lazy = fgs.Pipeline(act)
+    assert lazy.lazy_sort == 2
+    fl, sl = lazy.render(cam, exact=True)
+    assert sl.front_tiles == int((per_tile > 4096).sum())
+    if kind == "opaque":
+        assert sl.redo_tiles == 0
+    elif kind == "translucent":
+        assert sl.redo_tiles == int((per_tile > 2048).sum())
+    else:
+        assert 0 < sl.redo_tiles < int((per_tile > 2048).sum())
+    assert np.array_equal(fl.image.view(np.uint32), oimg.view(np.uint32))
+    assert sl.pairs_contributing == ost["pairs_contributing"]
+    lazy.lazy_sort = 1                    # level 1 leaves these tiles to the full sort
+    f1, s1 = lazy.render(cam, exact=True)
+    assert s1.redo_tiles == 0 or (per_tile > 4096).any()
+    assert np.array_equal(f1.image.view(np.uint32), oimg.view(np.uint32))
 
 
 def test_lazy_extras_and_bands():

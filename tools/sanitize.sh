@@ -17,3 +17,13 @@ timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 9 --log-file gp
   python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "dense_tile_with or equal_depth_ties_order_by_index and 3000" \
   > gpurun_out/sanitize_racecheck_dense.out 2>&1; echo "racecheck(dense) rc=$?"
 tail -1 gpurun_out/sanitize_racecheck_dense.out; tail -3 gpurun_out/sanitize_racecheck_dense.log
+# lazy_sort: memcheck + racecheck over the front kernel, the redo sort and the second blend pass
+# (mixed scene: half of the fronts are redone; late cluster: fronts cut before a depth cluster)
+timeout 1500 compute-sanitizer --tool memcheck --error-exitcode 9 --log-file gpurun_out/sanitize_memcheck_lazy.log \
+  python -m pytest tests/test_lazy_sort.py -x -q -m gpu -k "mixed or late or extras or repeated" \
+  > gpurun_out/sanitize_memcheck_lazy.out 2>&1; echo "memcheck(lazy) rc=$?"
+tail -1 gpurun_out/sanitize_memcheck_lazy.out; tail -2 gpurun_out/sanitize_memcheck_lazy.log
+timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 9 --log-file gpurun_out/sanitize_racecheck_lazy.log \
+  python -m pytest tests/test_lazy_sort.py -x -q -m gpu -k "mixed or extras" \
+  > gpurun_out/sanitize_racecheck_lazy.out 2>&1; echo "racecheck(lazy) rc=$?"
+tail -1 gpurun_out/sanitize_racecheck_lazy.out; tail -2 gpurun_out/sanitize_racecheck_lazy.log
