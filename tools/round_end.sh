@@ -12,7 +12,7 @@ done
 python tools/benchsum.py gpurun_out/${tag}_bench_c*.json
 cmd="python bench.py --steps 2 --warmup 3 --no-cpu --no-also --workload c4-4k"
 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/${tag}_launches.csv $cmd > gpurun_out/${tag}_ncu_b.log 2>&1
-for k in k_preprocess k_scan_tiles k_tile_order k_scatter_runs k_tile_sort_medium k_tile_sort_large k_blend2; do
+for k in k_preprocess k_scan_tiles k_tile_order k_scatter_runs k_tile_sort_medium k_tile_front k_blend2; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 8 -c 1 -f -o gpurun_out/${tag}_c44k_$k $cmd > gpurun_out/${tag}_ncu_$k.log 2>&1
 done
 cmd="python bench.py --steps 2 --warmup 3 --no-cpu --no-also --workload c2"
