@@ -18,6 +18,10 @@ views are DISTINCT cameras of an orbit (16, or the 64 of configs[4]); with N > 1
 instead splits ONE frame into tile-row bands whose gather (NCCL) is inside the timed
 region.
 
+The frames are rendered the way `Pipeline.render` renders them, i.e. with `lazy_sort` at the
+level the pipeline settled on during the warm-up frames (`config.lazy_sort`; `--no-lazy` = every
+tile sorted in full): same frames, contrib flags and counters either way (tests/test_lazy_sort.py).
+
 One JSON line is printed by rank 0.
   value      device-timed: K views issued round-robin on 3 CUDA streams, one start event,
              one end event per stream, longest span, max over ranks.  No L2 flush in this
