@@ -921,10 +921,12 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
         ushort4 rect = make_ushort4(0, 0, 0, 0);
         // projection.py:39-47 frustum_mask
         if ((t2 > FGS_Z_NEAR) && (op > frustum_thresh)) {
+#ifndef FGS_PROBE_NO_SH     // (timing probe: K1 without the SH colours -- WRONG frames)
 #pragma unroll
             for (int j = 0; j < FGS_SH_STAGED; ++j)
                 cp_async16_pre(&s_sh[j * FGS_PRE_THREADS + threadIdx.x], &sc.sh[(int64_t)j * sc.n + g]);
             asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
             // projection.py:59-85: the 3D covariance, evaluated per scene by fgs_scene_pack
             float S[3][3];
             S[0][0] = sc4.x; S[0][1] = S[1][0] = sc4.y; S[0][2] = S[2][0] = sc4.z;
@@ -1032,6 +1034,7 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                 // are live (no 48-register coefficient array).
                 asm volatile("cp.async.wait_group 0;" ::: "memory");   // own gathers: no barrier needed
                 float rgb[3] = {0.0f, 0.0f, 0.0f};
+#ifndef FGS_PROBE_NO_SH
                 // planes beyond the staged ones come straight from global memory, issued here
                 // and consumed last (the staging buffer is what caps the CTAs per SM)
                 float4 late[12 - FGS_SH_STAGED + 1];
@@ -1053,6 +1056,9 @@ k_preprocess(SceneDev sc, const float *__restrict__ kcut, int P,
                         else { if (sh_degree >= 3) rgb[ch] = fa(rgb[ch], fm(bz[i], v)); }
                     }
                 }
+#else
+                rgb[0] = bz[1]; rgb[1] = bz[2]; rgb[2] = bz[3];
+#endif
 #pragma unroll
                 for (int ch = 0; ch < 3; ++ch) rgb[ch] = fmaxf(fa(rgb[ch], 0.5f), 0.0f);
                 // render.py:34-40 splat row, binning.py:235-241
@@ -1619,7 +1625,9 @@ k_emit(int P, int width, int height, int grid_w, int band0, int band1, FrameDev 
 // table (k_scan_tiles) turns that into positions.  A pure streaming copy: coalesced reads of
 // the block, runs written as contiguous segments.
 // ---------------------------------------------------------------------------
+#ifndef FGS_SCATTER_THREADS
 #define FGS_SCATTER_THREADS 128
+#endif
 // One CTA of four warps per preprocess CTA; warp w takes the table entries w, w + 4, ...:
 // lane l fetches entry 4 l + w (tile, bucket range, run offset) and the tile's bucket start --
 // two round trips for up to 32 runs per warp -- and the warp then copies its runs one after
