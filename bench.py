@@ -315,6 +315,9 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     stream = torch.cuda.current_stream(dev)
     bucket = args.sort_mode == "tile-bucket"
     lazy = int(pipe.lazy_sort)              # level the pipeline settled on during the warm-up frames
+    if args.lazy_level is not None:
+        lazy = pipe.lazy_sort = args.lazy_level
+        pipe._lazy_cap = 0                  # (frozen: _note_fronts leaves the level alone)
     front_tiles, redo_tiles = int(st.front_tiles), int(st.redo_tiles)
     nlanes = max(1, args.streams)
     lanes = [stream] + [torch.cuda.Stream(device=dev) for _ in range(nlanes - 1)]
@@ -660,6 +663,8 @@ def main():
     ap.add_argument("--no-also", action="store_true", help="skip the extra configs[1] run")
     ap.add_argument("--no-lazy", action="store_true",
                     help="sort every tile in full (fgs_layout.lazy_sort = 0)")
+    ap.add_argument("--lazy-level", type=int, default=None, choices=[0, 1, 2],
+                    help="force the lazy_sort level instead of letting the pipeline choose (A/B runs)")
     ap.add_argument("--no-spatial", action="store_true",
                     help="keep the scene in the caller's order (no Morton slot order)")
     ap.add_argument("--streams", type=int, default=3,

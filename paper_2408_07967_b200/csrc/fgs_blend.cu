@@ -465,8 +465,11 @@ __device__ __noinline__ float2 alpha_exact_pair(const float4 *row, float fx, flo
                        alpha_exact(r0, r1, r2, fx, fy1, tau, tab));
 }
 
+#ifndef FGS_B2_REDO_MINCTAS
+#define FGS_B2_REDO_MINCTAS FGS_B2_MINCTAS
+#endif
 template <bool CONTRIB, bool EXTRAS, bool REDO = false>
-__global__ void __launch_bounds__(FGS_B2_THREADS, FGS_B2_MINCTAS)
+__global__ void __launch_bounds__(FGS_B2_THREADS, REDO ? FGS_B2_REDO_MINCTAS : FGS_B2_MINCTAS)
 k_blend2(const float *__restrict__ splat, const float *__restrict__ gdepth,
          const uint32_t *__restrict__ vals, const uint32_t *__restrict__ inv,
          const int32_t *__restrict__ starts, const uint32_t *__restrict__ order, int width,
