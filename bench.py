@@ -444,7 +444,10 @@ def measure(env, name, steps, warmup, args, with_cpu, short=False):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    Ke = K if not short else min(K, 32)
+    # views/s of a pipelined batch: measured over at least 60 views so that the fill of the
+    # pipeline (the first frame's kernels before the first read-back can start, ~2 frame times)
+    # is amortised as it is in the device-timed value's streams; `e2e.steps` says how many
+    Ke = max(K, 60) if not short else min(K, 32)
     t0 = time.perf_counter()
     if band is None:
         # the batch call a views/s user makes: the views through Pipeline.render_iter
