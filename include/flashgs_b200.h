@@ -140,7 +140,7 @@ typedef struct fgs_layout {
     uint64_t off_tilecount;    /* uint32 [tiles][8]: TILE_BUCKET per-tile counters, one 32-byte
                                   sector each: [0] pairs reserved through the CTAs' tile
                                   tables, [1] fallback pairs, [2] fallback cursor       */
-    uint64_t off_cursor;       /* uint32 [tiles][8]: size-class tile lists (words 1..4), slice totals of the tile scan (5, 6) */
+    uint64_t off_cursor;       /* uint32 [tiles][8]: size-class tile lists (words 1..4 and 7), slice totals of the tile scan (5, 6) */
     uint64_t off_ctainfo;      /* uint32 [preprocess blocks][4]: TILE_BUCKET, each K1 CTA's
                                   (first table entry, entries, write-combined records, 0) */
     uint64_t off_tileorder;    /* uint32 [160 + tiles]: TILE_BUCKET, 64 size-bin counts, 64 bin

@@ -47,7 +47,7 @@
 #define FGS_WORK_LARGE    0
 #define FGS_WORK_MEDIUM_TICKET 2   // (+1: CTAs out) tile tickets of the persistent sort kernels
 #define FGS_WORK_LARGE_TICKET  4   // (+1: CTAs out)
-#define FGS_WORK_SORT_DONE     6   // bit 0: medium class finished, bit 1: large class finished
+#define FGS_WORK_SORT_DONE     6   // bit 0: medium class finished, bit 1: large class, bit 2: small class
 #define FGS_WORK_TAIL_OUT      7   // tail-kernel CTAs past their wait on FGS_WORK_SORT_DONE
 #define FGS_WORK_STAGE_USED    8   // records the preprocess CTAs have reserved in the stage
 #define FGS_WORK_FB_CTAS       9   // preprocess CTAs left to the placement walk (fallback list length)
@@ -55,6 +55,8 @@
                                    // entries of the dense list -- tiles a class gave up on -- are the tail's)
 #define FGS_WORK_REDO     11   // lazy_sort: cursor of the redo list (tiles unsaturated at the end of their front)
 #define FGS_WORK_REDO_OUT 12   // lazy_sort: CTAs of the second blend pass that have left
+#define FGS_WORK_SMALL       13   // tiles of the small sort class (1..2048 pairs) the tile scan queued
+#define FGS_WORK_SMALL_TICKET 14  // (+1: CTAs out)
 #define FGS_CTA_NO_STAGE  0xffffffffu   // ctainfo.w of a CTA whose records were not staged
 // blend tile order: tiles are binned by pair count (quarter-octave bins, heaviest = bin 0,
 // empty = last) and the blend's CTAs take them in bin order, so the long tiles start first

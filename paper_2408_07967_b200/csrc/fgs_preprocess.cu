@@ -1407,7 +1407,8 @@ k_tile_blocksums(const uint32_t *__restrict__ counts, uint32_t *__restrict__ cur
 __global__ void __launch_bounds__(1024)
 k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
              uint32_t *__restrict__ cursor, uint32_t *__restrict__ bincount, int tiles,
-             unsigned long long capacity, fgs_stats *__restrict__ stats, int use_sums)
+             unsigned long long capacity, fgs_stats *__restrict__ stats, int use_sums,
+             int32_t *__restrict__ limit)
 {
     __shared__ unsigned long long s_w[32];
     __shared__ uint32_t s_bin[FGS_ORDER_BINS];
@@ -1476,6 +1477,22 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
         else if (v > FGS_SMALL_TILE)
             cursor[(size_t)atomicAdd(&stats->medium_tiles, 1u) * FGS_CTR_STRIDE + 2] = (uint32_t)i;
     }
+    // the small class gets a list too (word 7 of the cursor slots): two thirds of a frame's
+    // tiles are empty, and a sort kernel with one CTA per TILE spent most of its time starting
+    // CTAs that found nothing to do.  One atomic per warp.
+    {
+        const bool is_small = i < tiles && v > 0ull && v <= (unsigned long long)FGS_SMALL_TILE;
+        const uint32_t sm = __ballot_sync(FGS_FULL, is_small);
+        if (sm) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(&fgs_work(stats)[FGS_WORK_SMALL], (uint32_t)__popc(sm));
+            base = __shfl_sync(FGS_FULL, base, 0);
+            if (is_small)
+                cursor[(size_t)(base + (uint32_t)__popc(sm & lanemask_lt())) * FGS_CTR_STRIDE + 7] = (uint32_t)i;
+        }
+        // lazy_sort: every pair of a tile counts as sorted unless the front kernel says otherwise
+        if (i < tiles) limit[i] = 0x7fffffff;
+    }
     const uint32_t nonempty = __reduce_add_sync(FGS_FULL, v ? 1u : 0u);
     if (lane == 0 && nonempty) atomicAdd(&stats->tiles_nonempty, nonempty);
     if (i == tiles - 1) {                       // the thread that owns the last tile knows M
@@ -1498,7 +1515,7 @@ int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaSt
                   f.cursor, tiles);
     FGS_CHAIN(k_scan_tiles, dim3(slices), dim3(1024), 0, st,
               f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats,
-              use_sums);
+              use_sums, f.limit);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }

@@ -853,29 +853,35 @@ struct TileTickets {
 __global__ void __launch_bounds__(256, 6)
 k_tile_sort(const uint64_t *__restrict__ rec, uint32_t *__restrict__ vals_out,
             uint64_t *__restrict__ keys_out, const int32_t *__restrict__ starts,
-            uint32_t *__restrict__ hard_list, int write_keys, fgs_stats *__restrict__ stats,
-            int32_t *__restrict__ limit, int front_min)
+            const uint32_t *__restrict__ small_list, uint32_t *__restrict__ hard_list,
+            int write_keys, fgs_stats *__restrict__ stats)
 {
     // one buffer, two instantiations: up to 1024 records with 4 per thread, up to 2048 with 8
-    // (35 KB, still 6 CTAs per SM; the grid's dynamic CTA dispatch balances these tiles
-    // better than the medium class's persistent CTAs, which keep 69 KB each)
+    // (35 KB, 6 CTAs per SM).  Persistent CTAs over the list of small tiles the tile scan
+    // queued (tickets: the tiles differ 1 : 2048 in size): two thirds of a frame's tiles are
+    // empty and a sixth is heavy, and with one CTA per tile of the grid this kernel spent more
+    // time starting CTAs that found nothing to do (10M / 4K: 55 -> 48 us, 8K frame:
+    // 241 -> 184 us; C2, a grid of 8160 tiles: 24.5 -> 27 us -- the tickets cost a little).
     __shared__ __align__(16) unsigned char raw[sizeof(BucketSmem<256, 8, true, FGS_SMALL_NBDIV>)];
-    const uint32_t over = stats->overflow;               // one round trip with the range lookup
-    const int tile = blockIdx.x;
-    const int n = starts[tile + 1] - starts[tile];
-    if (over) return;
-    // lazy_sort: this grid visits every tile, so it is the one that marks the tiles sorted in
-    // full (the front kernel writes the entry of every tile beyond front_min itself)
-    if (limit != nullptr && threadIdx.x == 0 && n <= front_min) limit[tile] = 0x7fffffff;
-    if (n <= 0 || n > FGS_SMALL_TILE) return;
-    const bool ok = n <= BucketSmem<256, 4>::CAP
-        ? tb_sort_tile<256, 4, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 4, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
-                               keys_out, starts, write_keys)
-        : tb_sort_tile<256, 8, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 8, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
-                               keys_out, starts, write_keys);
-    if (!ok &&
-        threadIdx.x == 0)
-        hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+    __shared__ uint32_t s_ticket;
+    if (stats->overflow) return;
+    const uint32_t count = fgs_work(stats)[FGS_WORK_SMALL];
+    TileTickets tk;
+    if (!tk.open(stats, FGS_WORK_SMALL_TICKET, count)) return;
+    for (uint32_t i = tk.take(&s_ticket); i < count; i = tk.take(&s_ticket)) {
+        const int tile = (int)small_list[(size_t)i * FGS_CTR_STRIDE];
+        const int n = starts[tile + 1] - starts[tile];
+        const bool ok = n <= BucketSmem<256, 4>::CAP
+            ? tb_sort_tile<256, 4, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 4, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
+                                   keys_out, starts, write_keys)
+            : tb_sort_tile<256, 8, true, FGS_SMALL_NBDIV>(*reinterpret_cast<BucketSmem<256, 8, true, FGS_SMALL_NBDIV> *>(raw), tile, rec, vals_out,
+                                   keys_out, starts, write_keys);
+        if (!ok &&
+            threadIdx.x == 0)
+            hard_list[(size_t)atomicAdd(&stats->hard_tiles, 1u) * FGS_CTR_STRIDE] = (uint32_t)tile;
+        __syncthreads();
+    }
+    tk.close(stats, 4u);
 }
 
 // medium class: threads per CTA x records per thread = 4096 (tuning knobs)
@@ -1207,8 +1213,9 @@ k_tile_sort_tail(uint64_t *__restrict__ rec, uint64_t *__restrict__ alt,
         // extra launches
         if (blockIdx.x == 0)
             stats->front_tiles = nd + work[FGS_WORK_LARGE];      // (level 2 adds stats->medium_tiles)
-        const uint32_t need = lazy ? ((nmed ? 1u : 0u) | ((nd | work[FGS_WORK_LARGE] | (stats->medium_tiles - nmed)) ? 2u : 0u))
-                                   : (((nmed | nd) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u));
+        const uint32_t need = (lazy ? ((nmed ? 1u : 0u) | ((nd | work[FGS_WORK_LARGE] | (stats->medium_tiles - nmed)) ? 2u : 0u))
+                                    : (((nmed | nd) ? 1u : 0u) | (work[FGS_WORK_LARGE] ? 2u : 0u))) |
+                              (work[FGS_WORK_SMALL] ? 4u : 0u);
         volatile uint32_t *done = work + FGS_WORK_SORT_DONE;
         uint32_t ok = 1u;
         for (uint32_t spin = 0; (*done & need) != need; ++spin) {
@@ -1351,13 +1358,13 @@ int fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, int lazy,
         FGS_AFTER_LAUNCH(st);
     }
     {
-        cfg.gridDim = dim3((unsigned)tiles);
+        cfg.gridDim = dim3((unsigned)(tiles < 6 * sms ? tiles : 6 * sms));
         cfg.blockDim = dim3(256);
         cfg.dynamicSmemBytes = 0;
         cfg.numAttrs = overlap ? 1 : 0;
         const cudaError_t e = cudaLaunchKernelEx(&cfg, k_tile_sort, (const uint64_t *)f.keys[0],
-            f.vals[0], f.keys[1], (const int32_t *)f.starts, hard_list, write_keys, f.stats,
-            lazy ? f.limit : (int32_t *)nullptr, lazy == 2 ? FGS_SMALL_TILE : FGS_DENSE_TILE);
+            f.vals[0], f.keys[1], (const int32_t *)f.starts, (const uint32_t *)(f.cursor + 7), hard_list,
+            write_keys, f.stats);
         if (e != cudaSuccess) { fgs_set_cuda_error(e); return FGS_E_CUDA; }
         FGS_AFTER_LAUNCH(st);
     }
