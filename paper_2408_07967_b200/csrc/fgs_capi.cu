@@ -55,6 +55,13 @@ static int fgs_lazy(const fgs_layout *L)
     return L->lazy_sort >= 2 ? 2 : 1;
 }
 
+// pair count beyond which lazy_sort sorts only a front of a tile (0: every tile in full)
+static uint32_t fgs_heavy_thr(const fgs_layout *L)
+{
+    const int lazy = fgs_lazy(L);
+    return lazy == 2 ? FGS_SMALL_TILE : lazy == 1 ? FGS_DENSE_TILE : 0u;
+}
+
 static int check_frame(const fgs_layout *L, const fgs_camera *c)
 {
     if (!L) return FGS_E_ARG;
@@ -290,7 +297,7 @@ int fgs_scan(void *ws, const fgs_layout *L, void *stream)
     if (!ws || !L) return FGS_E_ARG;
     if (L->sort_mode == FGS_SORT_TILE_BUCKET)
         return fgs_launch_scan_tiles(fgs_frame_view(ws, L), L->tiles, L->capacity,
-                                     (cudaStream_t)stream);
+                                     (cudaStream_t)stream, fgs_heavy_thr(L));
     return fgs_launch_scan(fgs_frame_view(ws, L), L->preprocess_blocks, L->capacity,
                            (cudaStream_t)stream);
 }
@@ -306,7 +313,7 @@ int fgs_emit(const void *packed, const fgs_camera *cam, int32_t strategy, int32_
     return fgs_launch_emit(fgs_scene_view(packed, L->gaussians), L->gaussians, make_cam(cam),
                            strategy, band0, band1,
                            L->sort_mode == FGS_SORT_TILE_BUCKET, fgs_frame_view(ws, L),
-                           (cudaStream_t)stream);
+                           (cudaStream_t)stream, fgs_heavy_thr(L));
 }
 
 int fgs_sort(void *ws, const fgs_layout *L, uint32_t epoch, void *stream)

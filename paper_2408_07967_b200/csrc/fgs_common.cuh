@@ -198,10 +198,12 @@ int  fgs_launch_preprocess(const SceneDev &sc, const float *kcut, int64_t P, con
                            double tau, int sh_degree, int strategy, int band0, int band1,
                            int bucket, int tiles, const FrameDev &f, cudaStream_t st);
 int  fgs_launch_scan(const FrameDev &f, int nblocks, int64_t capacity, cudaStream_t st);
-int  fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st);
-int  fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st);
+int  fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st,
+                           uint32_t heavy_thr = 0);
+int  fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st,
+                           uint32_t heavy_thr = 0);
 int  fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
-                     int band1, int bucket, const FrameDev &f, cudaStream_t st);
+                     int band1, int bucket, const FrameDev &f, cudaStream_t st, uint32_t heavy_thr = 0);
 int  fgs_launch_tile_sort(const FrameDev &f, int tiles, int write_keys, int lazy, cudaStream_t st);
 int  fgs_launch_tile_sort_redo(const FrameDev &f, int tiles, cudaStream_t st);
 // (lazy: 0 off; 1 = tiles beyond FGS_DENSE_TILE pairs get a front only; 2 = beyond FGS_SMALL_TILE)
@@ -323,6 +325,16 @@ __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
 // size bin of a tile with v pairs: quarter-octave bins, heaviest first, empty last
+// lazy_sort: the blend composites at most the sorted front of a heavy tile (~1100 pairs), so
+// for its place in the blend order a tile beyond `heavy_thr` pairs weighs that much, not its
+// pair count (0 = no threshold); a tile just below the threshold may need all of its pairs and
+// goes first
+#define FGS_FRONT_WEIGHT 1152u
+__device__ __forceinline__ uint32_t fgs_order_weight(uint32_t v, uint32_t heavy_thr)
+{
+    return (heavy_thr && v > heavy_thr) ? FGS_FRONT_WEIGHT : v;
+}
+
 __device__ __forceinline__ int fgs_order_bin(uint32_t v)
 {
     if (v == 0) return FGS_ORDER_BINS - 1;

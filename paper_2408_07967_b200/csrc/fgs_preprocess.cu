@@ -1408,7 +1408,7 @@ __global__ void __launch_bounds__(1024)
 k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
              uint32_t *__restrict__ cursor, uint32_t *__restrict__ bincount, int tiles,
              unsigned long long capacity, fgs_stats *__restrict__ stats, int use_sums,
-             int32_t *__restrict__ limit)
+             int32_t *__restrict__ limit, uint32_t heavy_thr)
 {
     __shared__ unsigned long long s_w[32];
     __shared__ uint32_t s_bin[FGS_ORDER_BINS];
@@ -1461,7 +1461,8 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     __syncthreads();
     const unsigned long long excl = carry + s_w[w] + incl - v;
     // size-bin histogram for the blend's tile order (placement: k_tile_order)
-    if (i < tiles) atomicAdd(&s_bin[fgs_order_bin(v > 0xffffffffull ? 0xffffffffu : (uint32_t)v)], 1u);
+    if (i < tiles)
+        atomicAdd(&s_bin[fgs_order_bin(fgs_order_weight(v > 0xffffffffull ? 0xffffffffu : (uint32_t)v, heavy_thr))], 1u);
     __syncthreads();
     if (threadIdx.x < FGS_ORDER_BINS && s_bin[threadIdx.x])
         atomicAdd(&bincount[threadIdx.x], s_bin[threadIdx.x]);
@@ -1506,7 +1507,8 @@ k_scan_tiles(const uint32_t *__restrict__ counts, int32_t *__restrict__ starts,
     }
 }
 
-int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st)
+int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaStream_t st,
+                          uint32_t heavy_thr)
 {
     const unsigned slices = (unsigned)((tiles + 1023) / 1024);
     const int use_sums = slices > FGS_SCAN_DIRECT_CTAS ? 1 : 0;
@@ -1515,7 +1517,7 @@ int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaSt
                   f.cursor, tiles);
     FGS_CHAIN(k_scan_tiles, dim3(slices), dim3(1024), 0, st,
               f.tilecount, f.starts, f.cursor, f.tileorder, tiles, (unsigned long long)capacity, f.stats,
-              use_sums, f.limit);
+              use_sums, f.limit, heavy_thr);
     FGS_AFTER_LAUNCH(st);
     return FGS_OK;
 }
@@ -1526,7 +1528,8 @@ int fgs_launch_scan_tiles(const FrameDev &f, int tiles, int64_t capacity, cudaSt
 // Order inside a bin is arbitrary (every tile's output is independent of it).
 __global__ void __launch_bounds__(1024)
 k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int first_tile,
-             int band_tiles, uint32_t *__restrict__ tile_ctr, const fgs_stats *__restrict__ stats)
+             int band_tiles, uint32_t *__restrict__ tile_ctr, const fgs_stats *__restrict__ stats,
+             uint32_t heavy_thr)
 {
     __shared__ uint32_t s_base[FGS_ORDER_BINS], s_cnt[FGS_ORDER_BINS], s_off[FGS_ORDER_BINS];
     fgs_pdl_wait();
@@ -1551,7 +1554,7 @@ k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int
     uint32_t rank = 0;
     if (i < band_tiles) {
         const int tile = first_tile + i;
-        bin = fgs_order_bin((uint32_t)(starts[tile + 1] - starts[tile]));
+        bin = fgs_order_bin(fgs_order_weight((uint32_t)(starts[tile + 1] - starts[tile]), heavy_thr));
         rank = atomicAdd(&s_cnt[bin], 1u);
         // the placement kernel's per-pair fallback cursor (word 2) starts at zero every time
         // the stage is issued, not only on the frame's first pass (fgs_emit is idempotent)
@@ -1572,12 +1575,13 @@ k_tile_order(const int32_t *__restrict__ starts, uint32_t *__restrict__ hdr, int
     }
 }
 
-int fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st)
+int fgs_launch_tile_order(const FrameDev &f, int grid_w, int band0, int band1, cudaStream_t st,
+                          uint32_t heavy_thr)
 {
     if (band1 < band0) return FGS_OK;
     const int band_tiles = (band1 - band0 + 1) * grid_w;
     FGS_CHAIN(k_tile_order, dim3((unsigned)((band_tiles + 1023) / 1024)), dim3(1024), 0, st,
-              f.starts, f.tileorder, band0 * grid_w, band_tiles, f.tilecount, f.stats);
+              f.starts, f.tileorder, band0 * grid_w, band_tiles, f.tilecount, f.stats, heavy_thr);
     FGS_CHECK_LAUNCH();
     return FGS_OK;
 }
@@ -1800,10 +1804,10 @@ k_place(int P, int width, int height, int grid_w, int band0, int band1,
 }
 
 int fgs_launch_emit(const SceneDev &sc, int64_t P, const CamDev &cam, int strategy, int band0,
-                    int band1, int bucket, const FrameDev &f, cudaStream_t st)
+                    int band1, int bucket, const FrameDev &f, cudaStream_t st, uint32_t heavy_thr)
 {
     if (bucket) {                       // also for an empty scene: the blend reads the order
-        const int rc = fgs_launch_tile_order(f, cam.grid_w, band0, band1, st);
+        const int rc = fgs_launch_tile_order(f, cam.grid_w, band0, band1, st, heavy_thr);
         if (rc) return rc;
     }
     if (P == 0) return FGS_OK;
