@@ -325,11 +325,16 @@ __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
 // size bin of a tile with v pairs: quarter-octave bins, heaviest first, empty last
-// lazy_sort: the blend composites at most the sorted front of a heavy tile (~1100 pairs), so
-// for its place in the blend order a tile beyond `heavy_thr` pairs weighs that much, not its
-// pair count (0 = no threshold); a tile just below the threshold may need all of its pairs and
-// goes first
-#define FGS_FRONT_WEIGHT 1152u
+// lazy_sort: the blend composites at most the sorted front of a heavy tile and usually stops
+// after a few hundred pairs (the tile is opaque), so for its place in the blend order a tile
+// beyond `heavy_thr` pairs weighs what it is expected to consume, not its pair count (0 = no
+// threshold); a tile below the threshold may need all of its pairs and goes first.  Measured
+// (blend, us): weight 1152 / 768 / 640 / 512 / 448 / 320 -> C2 170 / 157 / 151 / 144 / 144 / 148,
+// 1M dense scene 211 / 198 / 190 / 185 / 183 / -, C5 217 at every weight (267 by pair count),
+// no change where the blend is throughput-bound (10M / 4K, C3, 8K).
+#ifndef FGS_FRONT_WEIGHT
+#define FGS_FRONT_WEIGHT 448u
+#endif
 __device__ __forceinline__ uint32_t fgs_order_weight(uint32_t v, uint32_t heavy_thr)
 {
     return (heavy_thr && v > heavy_thr) ? FGS_FRONT_WEIGHT : v;
