@@ -176,3 +176,22 @@ def test_lazy_stages_can_be_repeated_on_one_frame():
         s = np.frombuffer(ws.stats_tensor().cpu().numpy().tobytes(), dtype=_capi.STATS_DTYPE)[0]
         assert int(s["redo_tiles"]) == swant.redo_tiles
         assert np.array_equal(ws.rgb.cpu().numpy(), want.image)
+
+
+def test_lazy_with_caller_order_slots():
+    """Slots in the caller's order: CTA tile tables overflow and the placement walk (k_place)
+    fills the buckets the front kernel then reads -- same frame as the full sort's and the
+    oracle's."""
+    act = _scene("mixed")
+    cam = identity_camera(64, 64, focal=32)
+    oimg, ost = orc.render(act, cam)
+    lazy = fgs.Pipeline(act, spatial_order=False)
+    full = fgs.Pipeline(act, spatial_order=False, lazy_sort=False)
+    for level in (2, 1):
+        lazy.lazy_sort = level
+        fl, sl = lazy.render(cam, exact=True)
+        ff, sf = full.render(cam, exact=True)
+        assert sl.front_tiles == sf.front_tiles > 0 and sl.redo_tiles > 0
+        assert np.array_equal(fl.image.view(np.uint32), ff.image.view(np.uint32))
+        assert np.array_equal(fl.image.view(np.uint32), oimg.view(np.uint32))
+        assert sl.pairs_contributing == sf.pairs_contributing == ost["pairs_contributing"]
